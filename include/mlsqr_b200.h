@@ -1,0 +1,221 @@
+/*
+ * include/mlsqr_b200.h -- C-ABI of the B200-native priorconditioned-LSQR path.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv 1308.6634 reference,
+ * /root/reference/proj).  Every entry point below replaces one reference
+ * interface; the file:line of that interface is cited.  No C++ or torch types
+ * cross this boundary: plain pointers, sizes and int status codes.  Errors
+ * never throw; they return a status and leave a thread-local message in
+ * mlsqr_last_error().  include/mlsqr_b200.hpp rethrows them as the
+ * reference's exception types (errors.hpp:9-41).
+ *
+ * Pointer kinds: MLSQR_HOST buffers are copied in/out around the call (the
+ * reference's std::span contract, linop.hpp:33-36); MLSQR_DEVICE buffers are
+ * cudaMalloc'ed memory on the context's device and stay resident.
+ *
+ * Arithmetic: fp64 everywhere, in the canonical device order documented in
+ * DESIGN.md (bit-exact with the oracle's DEVICE order).
+ */
+#ifndef MLSQR_B200_H
+#define MLSQR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:9-41) ---- */
+#define MLSQR_OK 0
+#define MLSQR_EDIM 1        /* DimensionError            (errors.hpp:9-13)  */
+#define MLSQR_EINVAL 2      /* std::invalid_argument     (krylov.cpp:219-226) */
+#define MLSQR_EBREAKDOWN 3  /* BreakdownError(iteration) (errors.hpp:27-36) */
+#define MLSQR_ECUDA 4       /* CUDA runtime failure / no device              */
+#define MLSQR_ENCCL 5       /* collective failure                            */
+#define MLSQR_ECALLBACK 6   /* a host callback (plugin SpdMap) failed        */
+
+#define MLSQR_HOST 0
+#define MLSQR_DEVICE 1
+
+/* penalty kinds (penalty.hpp:6-12) */
+#define MLSQR_PEN_TIKHONOV 0
+#define MLSQR_PEN_TV 1
+#define MLSQR_PEN_PM_LOG 2
+#define MLSQR_PEN_PM_EXP 3
+
+/* stop reasons (krylov.hpp:38) */
+#define MLSQR_STOP_S1 0
+#define MLSQR_STOP_S2 1
+#define MLSQR_STOP_S3 2
+#define MLSQR_STOP_S4 3
+#define MLSQR_STOP_MAX_ITERS 4
+#define MLSQR_STOP_BREAKDOWN 5
+
+typedef struct mlsqr_ctx mlsqr_ctx;
+typedef struct mlsqr_op mlsqr_op;
+typedef struct mlsqr_pc mlsqr_pc;
+
+/* thread-local message of the last failing call */
+const char* mlsqr_last_error(void);
+/* library/build identification, e.g. "mlsqr_b200 sm_100a fp64" */
+const char* mlsqr_version(void);
+
+/* ---- context: device + stream (+ optional communicator, see mlsqr_ctx_set_comm) ---- */
+int mlsqr_ctx_create(int device, void* cuda_stream /* NULL: library-owned stream */,
+                     mlsqr_ctx** out);
+int mlsqr_ctx_destroy(mlsqr_ctx* ctx);
+int mlsqr_ctx_synchronize(mlsqr_ctx* ctx);
+/* device memory helpers for callers without their own allocator */
+int mlsqr_dev_alloc(mlsqr_ctx* ctx, size_t bytes, void** ptr);
+int mlsqr_dev_free(mlsqr_ctx* ctx, void* ptr);
+int mlsqr_copy(mlsqr_ctx* ctx, void* dst, int dst_kind, const void* src, int src_kind,
+               size_t bytes);
+/* count of this library's kernel launches since the last reset (bench gpu_launches) */
+uint64_t mlsqr_ctx_launch_count(mlsqr_ctx* ctx, int reset);
+/* per-kernel-class device timing with CUDA events inside the solve (0 = off) */
+int mlsqr_ctx_set_timing(mlsqr_ctx* ctx, int enable);
+/* accumulated [ms, launches] for timing class `cls` (see MLSQR_TCLASS_*) */
+int mlsqr_ctx_get_timing(mlsqr_ctx* ctx, int cls, double* ms, uint64_t* launches);
+#define MLSQR_TCLASS_BLUR 0    /* A / A^T blur applications + fused epilogue   */
+#define MLSQR_TCLASS_DENSE 1   /* dense GEMV / GEMV^T + fused epilogue          */
+#define MLSQR_TCLASS_SMOOTH 2  /* V-cycle level-0 smoothing sweeps              */
+#define MLSQR_TCLASS_MG 3      /* whole V-cycle (all levels)                    */
+#define MLSQR_TCLASS_UPDATE 4  /* LSQR vector update (f, w, q) + w.q           */
+#define MLSQR_TCLASS_ITER 5    /* whole LSQR iteration                          */
+#define MLSQR_TCLASS_COUNT 6
+
+/* ---- LinearOperator (linop.hpp:21-47) ----------------------------------- */
+/* Separable Gaussian blur with explicit taps (SeparableGaussianBlur2D, linop.hpp:110-126,
+ * GaussianConvolution1D, linop.hpp:83-105; 3D = third z pass).  taps: 2*radius+1 host
+ * values, identical on every axis; zero extension; self-adjoint. */
+int mlsqr_blur_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
+                      const double* taps, int radius, mlsqr_op** out);
+/* DenseOperator (linop.hpp:59-71): row-major rows x cols.  a_kind HOST copies to device.
+ * sol_row_len: row length of solution-space vectors for the canonical reductions
+ * (the x-extent of the voxel grid; 0 = cols). */
+int mlsqr_dense_create(mlsqr_ctx* ctx, size_t rows, size_t cols, const double* a, int a_kind,
+                       size_t sol_row_len, mlsqr_op** out);
+/* fDOT-like dense operator formed on the device: A[s*n_det+d, x] = gs[s,x] * gd[d,x]
+ * (host tables from mlsqr_fdot_tables). */
+int mlsqr_dense_create_fdot(mlsqr_ctx* ctx, size_t n_vox, int n_src, int n_det,
+                            const double* gs, const double* gd, size_t sol_row_len,
+                            mlsqr_op** out);
+/* IdentityOperator (linop.hpp:49-56) */
+int mlsqr_identity_create(mlsqr_ctx* ctx, size_t n, size_t row_len, mlsqr_op** out);
+int mlsqr_op_destroy(mlsqr_op* op);
+int mlsqr_op_shape(const mlsqr_op* op, size_t* rows, size_t* cols);
+/* LinearOperator::apply / apply_adjoint (linop.cpp:30-40): EDIM on length mismatch */
+int mlsqr_op_apply(mlsqr_op* op, const double* x, size_t x_len, double* y, size_t y_len,
+                   int ptr_kind);
+int mlsqr_op_apply_adjoint(mlsqr_op* op, const double* y, size_t y_len, double* x,
+                           size_t x_len, int ptr_kind);
+
+/* ---- SpdMap (spdsolve.hpp:11-33) ----------------------------------------- */
+int mlsqr_identity_map_create(mlsqr_ctx* ctx, size_t n, mlsqr_pc** out);
+/* Multigrid V-cycle on the edge-based diffusion operator M (diffusion.hpp:12-20):
+ * 2^d aggregation, Galerkin edge sums, omega-Jacobi nu_pre/nu_post sweeps, fixed coarse
+ * sweeps.  The SpdMap plug point named at spdsolve.hpp:13-14. */
+int mlsqr_vcycle_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz, double h,
+                        int levels, int nu_pre, int nu_post, double omega, int coarse_sweeps,
+                        mlsqr_pc** out);
+/* explicit level-0 edge coefficients (one array per axis, zero where no edge) + shift */
+int mlsqr_vcycle_set_coefficients(mlsqr_pc* pc, const double* cx, const double* cy,
+                                  const double* cz, double eps, int ptr_kind);
+/* assemble_m + auto_shift (diffusion.cpp:59-87) on the device from a field f:
+ * c_e = diffusivity(|grad f|) w_e/h^2; eps < 0 selects 1e-8 * max diagonal. */
+int mlsqr_vcycle_update(mlsqr_pc* pc, const double* f, int ptr_kind, int pen_kind, double T,
+                        double eps, double* eps_used);
+/* host plug-in SpdMap: fn(ctx, p, v) with host vectors (parity / test fakes) */
+typedef int (*mlsqr_host_map_fn)(void* user, const double* p, double* v);
+int mlsqr_callback_map_create(mlsqr_ctx* ctx, size_t n, mlsqr_host_map_fn fn, void* user,
+                              mlsqr_pc** out);
+int mlsqr_pc_destroy(mlsqr_pc* pc);
+int mlsqr_pc_dimension(const mlsqr_pc* pc, size_t* n);
+/* SpdMap::solve: v ~= M^{-1} p */
+int mlsqr_pc_solve(mlsqr_pc* pc, const double* p, double* v, size_t n, int ptr_kind);
+/* y = (M + eps I) x for the level-0 operator of a V-cycle (tests / R(f) gradient) */
+int mlsqr_vcycle_m_apply(mlsqr_pc* pc, const double* x, double* y, size_t n, int ptr_kind);
+
+/* ---- Krylov (krylov.hpp:19-95) ------------------------------------------- */
+typedef struct {            /* StoppingConfig (krylov.hpp:19-36) */
+  double atol, btol, conlim, delta, eta;
+  int max_iters;
+  int use_s1, use_s2, use_s3, use_s4;
+} mlsqr_stop;
+
+typedef struct {            /* IterationRecord (krylov.hpp:41-52) */
+  int iteration;
+  int res_data_exact;
+  double res_damped, res_data, s2_value, anorm_est, cond_est, xnorm_est, alpha, beta;
+} mlsqr_iter_rec;
+
+typedef struct {
+  int iterations;
+  int stop_reason;          /* MLSQR_STOP_* */
+  int n_alphas, n_betas;    /* BidiagEntries sizes after trim (krylov.cpp:182-186) */
+  int breakdown_iteration;  /* BreakdownError::iteration() when MLSQR_EBREAKDOWN */
+} mlsqr_solve_info;
+
+/* mlsqr (krylov.hpp:94-95, krylov.cpp:335-440): device-resident loop.
+ * g: n_rows; f: n_cols; trace: max_iters rows; alphas: max_iters+1; betas: max_iters+2.
+ * trace/alphas/betas/info are host arrays (may be NULL); g/f follow ptr_kind. */
+int mlsqr_solve(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau,
+                const mlsqr_stop* stop, double* f, mlsqr_iter_rec* trace, double* alphas,
+                double* betas, mlsqr_solve_info* info, int ptr_kind);
+/* lsqr (krylov.hpp:86-87): the M = I path without a preconditioner solve */
+int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop* stop,
+                     double* f, mlsqr_iter_rec* trace, double* alphas, double* betas,
+                     mlsqr_solve_info* info, int ptr_kind);
+
+/* ---- lagged-diffusivity outer loop (outer.hpp:13-62) --------------------- */
+typedef struct {            /* OuterConfig (outer.hpp:13-28) with a V-cycle M^{-1} */
+  double tau;
+  int pen_kind;
+  double T;
+  mlsqr_stop inner_stop;
+  int inner_cap;
+  double rel_decrease_threshold;  /* <= 0: fixed outer count (no stagnation break) */
+  int max_outer;
+  double epsilon;                 /* < 0: auto shift */
+  int mg_levels, nu_pre, nu_post, coarse_sweeps;
+  double omega;
+} mlsqr_outer_cfg;
+
+typedef struct {            /* OuterStep (outer.hpp:33-41) */
+  int k;
+  int inner_iterations;
+  int inner_stop;
+  double penalty_value;
+  double final_residual;
+  double eps_used;
+} mlsqr_outer_step;
+
+/* solve_nonlinear (outer.hpp:61-62, outer.cpp:40-100).  steps: max_outer; alphas/betas
+ * optional host blocks (max_outer x (inner_cap+1) / (inner_cap+2)). */
+int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, size_t ny,
+                          size_t nz, double h, const mlsqr_outer_cfg* cfg, double* f_out,
+                          mlsqr_outer_step* steps, int* n_steps, int* stop_reason,
+                          int* triggered_at, double* alphas, double* betas, int ptr_kind);
+
+/* ---- R(f) (diffusion.cpp:89-101) on the device --------------------------- */
+int mlsqr_penalty_functional(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
+                             double h, const double* f, int ptr_kind, int pen_kind, double T,
+                             double* value);
+
+/* ---- seeded synthetic inputs (host; problems.cpp conventions) ------------ */
+int mlsqr_taps(size_t n, double sigma_f, double domain_length, int radius, double* taps,
+               int* radius_out);
+int mlsqr_gauss_fill(uint64_t seed, size_t n, double stddev, double* out);
+int mlsqr_phantom_rects2d(size_t nx, size_t ny, int count, uint64_t seed, double* out);
+int mlsqr_phantom_shapes2d(size_t nx, size_t ny, int count, uint64_t seed, double* out);
+int mlsqr_phantom_ellipsoids3d(size_t nx, size_t ny, size_t nz, int count, double semi_lo,
+                               double semi_hi, double vlo, double vhi, uint64_t seed,
+                               double* out);
+int mlsqr_fdot_tables(size_t n, int n_src, int n_det, double mu, uint64_t seed, double* gs,
+                      double* gd);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,454 @@
+// capi.cu -- the extern "C" boundary (include/mlsqr_b200.h).  Every entry
+// point converts C++ exceptions into status codes + a thread-local message,
+// validates lengths like LinearOperator::apply (linop.cpp:15-40), and moves
+// host buffers in/out when ptr_kind == MLSQR_HOST.
+#include <cstring>
+#include <memory>
+
+#include "internal.cuh"
+
+using namespace mlsqr_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& fn) {
+  try {
+    g_err.clear();
+    fn();
+    return MLSQR_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return MLSQR_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MLSQR_EINVAL;
+  }
+}
+
+void check_len(size_t got, size_t want, const char* what) {
+  if (got != want)
+    throw Error(MLSQR_EDIM, std::string(what) + ": expected length " + std::to_string(want) +
+                                ", got " + std::to_string(got));
+}
+
+void set_device(Ctx* c) { MLSQR_CUDA(cudaSetDevice(c->device)); }
+
+// stage a host or device input as a device pointer
+struct In {
+  const double* d = nullptr;
+  DevBuf<double> own;
+  In(Ctx* c, const double* p, size_t n, int kind) {
+    if (kind == MLSQR_DEVICE || n == 0) {
+      d = p;
+      return;
+    }
+    own.alloc(n);
+    MLSQR_CUDA(cudaMemcpyAsync(own.p, p, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    d = own.p;
+  }
+};
+
+struct Out {
+  double* d = nullptr;
+  double* host = nullptr;
+  size_t n;
+  Ctx* c;
+  DevBuf<double> own;
+  Out(Ctx* cc, double* p, size_t nn, int kind) : n(nn), c(cc) {
+    if (kind == MLSQR_DEVICE) {
+      d = p;
+      return;
+    }
+    host = p;
+    own.alloc(n);
+    d = own.p;
+  }
+  void finish() {
+    if (host) MLSQR_CUDA(cudaMemcpyAsync(host, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host plug-in SpdMap (spdsolve.hpp:15-22 implemented by the caller)
+// ---------------------------------------------------------------------------
+namespace mlsqr_b200 {
+class CallbackMap final : public Pc {
+ public:
+  CallbackMap(Ctx* c, size_t nn, mlsqr_host_map_fn fn, void* user) : fn_(fn), user_(user) {
+    ctx = c;
+    n = nn;
+    hp_.resize(n);
+    hv_.resize(n);
+  }
+  bool host_callback() const override { return true; }
+  void solve(const double* p, double* v, double* seg, const int* gate, RowShape shape) override {
+    int on = 1;
+    if (gate) MLSQR_CUDA(cudaMemcpyAsync(&on, gate, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    MLSQR_CUDA(cudaMemcpyAsync(hp_.data(), p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    MLSQR_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!on) return;
+    if (fn_(user_, hp_.data(), hv_.data()) != 0) throw Error(MLSQR_ECALLBACK, "host SpdMap callback failed");
+    MLSQR_CUDA(cudaMemcpyAsync(v, hv_.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (seg) seg_dot(ctx, v, p, shape, seg, gate);
+  }
+
+ private:
+  mlsqr_host_map_fn fn_;
+  void* user_;
+  std::vector<double> hp_, hv_;
+};
+Pc* make_callback_map(Ctx* c, size_t n, mlsqr_host_map_fn fn, void* user) {
+  return new CallbackMap(c, n, fn, user);
+}
+}  // namespace mlsqr_b200
+
+extern "C" {
+
+const char* mlsqr_last_error(void) { return g_err.c_str(); }
+
+const char* mlsqr_version(void) { return "mlsqr_b200 0.1 sm_100a fp64 canonical-order"; }
+
+int mlsqr_ctx_create(int device, void* stream, mlsqr_ctx** out) {
+  return guard([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      throw Error(MLSQR_ECUDA, "no CUDA device visible: the B200 path has no CPU fallback");
+    require(device >= 0 && device < n, MLSQR_EINVAL, "device index out of range");
+    auto* c = new mlsqr_ctx();
+    c->impl.device = device;
+    MLSQR_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    MLSQR_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+      delete c;
+      throw Error(MLSQR_ECUDA, std::string("device ") + prop.name + " is not sm_100-class (this build targets sm_100a)");
+    }
+    c->impl.sm_count = prop.multiProcessorCount;
+    c->impl.l2_bytes = (size_t)prop.l2CacheSize;
+    if (stream) {
+      c->impl.stream = (cudaStream_t)stream;
+    } else {
+      MLSQR_CUDA(cudaStreamCreateWithFlags(&c->impl.stream, cudaStreamNonBlocking));
+      c->impl.own_stream = true;
+    }
+    *out = c;
+  });
+}
+
+int mlsqr_ctx_destroy(mlsqr_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->impl.device);
+    if (ctx->impl.own_stream) cudaStreamDestroy(ctx->impl.stream);
+    delete ctx;
+  });
+}
+
+int mlsqr_ctx_synchronize(mlsqr_ctx* ctx) {
+  return guard([&] { MLSQR_CUDA(cudaStreamSynchronize(ctx->impl.stream)); });
+}
+
+int mlsqr_dev_alloc(mlsqr_ctx* ctx, size_t bytes, void** ptr) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    MLSQR_CUDA(cudaMalloc(ptr, bytes));
+  });
+}
+
+int mlsqr_dev_free(mlsqr_ctx* ctx, void* ptr) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    MLSQR_CUDA(cudaFree(ptr));
+  });
+}
+
+int mlsqr_copy(mlsqr_ctx* ctx, void* dst, int dk, const void* src, int sk, size_t bytes) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    cudaMemcpyKind k = dk == MLSQR_DEVICE ? (sk == MLSQR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice)
+                                          : (sk == MLSQR_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost);
+    MLSQR_CUDA(cudaMemcpyAsync(dst, src, bytes, k, ctx->impl.stream));
+    MLSQR_CUDA(cudaStreamSynchronize(ctx->impl.stream));
+  });
+}
+
+uint64_t mlsqr_ctx_launch_count(mlsqr_ctx* ctx, int reset) {
+  const uint64_t n = ctx->impl.launches;
+  if (reset) ctx->impl.launches = 0;
+  return n;
+}
+
+int mlsqr_ctx_set_timing(mlsqr_ctx* ctx, int enable) {
+  return guard([&] {
+    ctx->impl.timing = enable != 0;
+    for (int i = 0; i < MLSQR_TCLASS_COUNT; ++i) {
+      ctx->impl.t_ms[i] = 0.0;
+      ctx->impl.t_n[i] = 0;
+    }
+  });
+}
+
+int mlsqr_ctx_get_timing(mlsqr_ctx* ctx, int cls, double* ms, uint64_t* launches) {
+  return guard([&] {
+    require(cls >= 0 && cls < MLSQR_TCLASS_COUNT, MLSQR_EINVAL, "bad timing class");
+    TimedRegion::collect(&ctx->impl);
+    *ms = ctx->impl.t_ms[cls];
+    *launches = ctx->impl.t_n[cls];
+  });
+}
+
+// ---- operators ----
+int mlsqr_blur_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
+                      const double* taps, int radius, mlsqr_op** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    require(taps != nullptr, MLSQR_EINVAL, "taps must not be null");
+    *out = new mlsqr_op{make_blur(&ctx->impl, dims, nx, ny, nz, taps, radius)};
+  });
+}
+
+int mlsqr_dense_create(mlsqr_ctx* ctx, size_t rows, size_t cols, const double* a, int a_kind,
+                       size_t sol_row_len, mlsqr_op** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    *out = new mlsqr_op{make_dense(&ctx->impl, rows, cols, a, a_kind == MLSQR_DEVICE, sol_row_len)};
+  });
+}
+
+int mlsqr_dense_create_fdot(mlsqr_ctx* ctx, size_t n_vox, int n_src, int n_det, const double* gs,
+                            const double* gd, size_t sol_row_len, mlsqr_op** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    require(n_src >= 1 && n_det >= 1 && n_vox >= 1, MLSQR_EDIM, "fDOT operator needs sources, detectors and voxels");
+    *out = new mlsqr_op{make_dense_fdot(&ctx->impl, n_vox, n_src, n_det, gs, gd, sol_row_len)};
+  });
+}
+
+int mlsqr_identity_create(mlsqr_ctx* ctx, size_t n, size_t row_len, mlsqr_op** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    *out = new mlsqr_op{make_identity(&ctx->impl, n, row_len)};
+  });
+}
+
+int mlsqr_op_destroy(mlsqr_op* op) {
+  return guard([&] {
+    if (!op) return;
+    delete op->impl;
+    delete op;
+  });
+}
+
+int mlsqr_op_shape(const mlsqr_op* op, size_t* rows, size_t* cols) {
+  return guard([&] {
+    *rows = op->impl->rows;
+    *cols = op->impl->cols;
+  });
+}
+
+int mlsqr_op_apply(mlsqr_op* op, const double* x, size_t x_len, double* y, size_t y_len, int kind) {
+  return guard([&] {
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    check_len(x_len, o->cols, "apply input");
+    check_len(y_len, o->rows, "apply output");
+    In in(c, x, x_len, kind);
+    Out out(c, y, y_len, kind);
+    o->apply(in.d, out.d, Epi{});
+    out.finish();
+    TimedRegion::collect(c);
+  });
+}
+
+int mlsqr_op_apply_adjoint(mlsqr_op* op, const double* y, size_t y_len, double* x, size_t x_len,
+                           int kind) {
+  return guard([&] {
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    check_len(y_len, o->rows, "apply_adjoint input");
+    check_len(x_len, o->cols, "apply_adjoint output");
+    In in(c, y, y_len, kind);
+    Out out(c, x, x_len, kind);
+    o->adjoint(in.d, out.d, Epi{});
+    out.finish();
+    TimedRegion::collect(c);
+  });
+}
+
+// ---- maps ----
+int mlsqr_identity_map_create(mlsqr_ctx* ctx, size_t n, mlsqr_pc** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    require(n >= 1, MLSQR_EDIM, "map dimension must be at least 1");
+    *out = new mlsqr_pc{make_identity_map(&ctx->impl, n), nullptr};
+  });
+}
+
+int mlsqr_vcycle_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz, double h,
+                        int levels, int nu_pre, int nu_post, double omega, int coarse_sweeps,
+                        mlsqr_pc** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    VCycle* v = make_vcycle(&ctx->impl, dims, nx, ny, nz, h, levels, nu_pre, nu_post, omega, coarse_sweeps);
+    *out = new mlsqr_pc{vcycle_as_pc(v), v};
+  });
+}
+
+int mlsqr_vcycle_set_coefficients(mlsqr_pc* pc, const double* cx, const double* cy,
+                                  const double* cz, double eps, int kind) {
+  return guard([&] {
+    require(pc && pc->vc, MLSQR_EINVAL, "not a V-cycle map");
+    Ctx* c = pc->impl->ctx;
+    set_device(c);
+    require(eps >= 0.0, MLSQR_EINVAL, "diagonal shift must be nonnegative");
+    const size_t n = pc->impl->n;
+    In a(c, cx, n, kind), b(c, cy, cy ? n : 0, kind), d(c, cz, cz ? n : 0, kind);
+    vcycle_set_coefficients(pc->vc, a.d, b.d, d.d, eps);
+    MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int mlsqr_vcycle_update(mlsqr_pc* pc, const double* f, int kind, int pen_kind, double T, double eps,
+                        double* eps_used) {
+  return guard([&] {
+    require(pc && pc->vc, MLSQR_EINVAL, "not a V-cycle map");
+    require(pen_kind >= 0 && pen_kind <= 3, MLSQR_EINVAL, "unknown penalty kind");
+    require(pen_kind == MLSQR_PEN_TIKHONOV || T > 0.0, MLSQR_EINVAL, "penalty threshold T must be positive");
+    Ctx* c = pc->impl->ctx;
+    set_device(c);
+    In in(c, f, pc->impl->n, kind);
+    const double e = vcycle_update(pc->vc, in.d, pen_kind, T, eps);
+    if (eps_used) *eps_used = e;
+  });
+}
+
+int mlsqr_callback_map_create(mlsqr_ctx* ctx, size_t n, mlsqr_host_map_fn fn, void* user,
+                              mlsqr_pc** out) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    require(fn != nullptr, MLSQR_EINVAL, "callback must not be null");
+    *out = new mlsqr_pc{make_callback_map(&ctx->impl, n, fn, user), nullptr};
+  });
+}
+
+int mlsqr_pc_destroy(mlsqr_pc* pc) {
+  return guard([&] {
+    if (!pc) return;
+    delete pc->impl;
+    delete pc;
+  });
+}
+
+int mlsqr_pc_dimension(const mlsqr_pc* pc, size_t* n) {
+  return guard([&] { *n = pc->impl->n; });
+}
+
+int mlsqr_pc_solve(mlsqr_pc* pc, const double* p, double* v, size_t n, int kind) {
+  return guard([&] {
+    Ctx* c = pc->impl->ctx;
+    set_device(c);
+    check_len(n, pc->impl->n, "solve");
+    In in(c, p, n, kind);
+    Out out(c, v, n, kind);
+    pc->impl->solve(in.d, out.d, nullptr, nullptr, RowShape{n, 1});
+    out.finish();
+    TimedRegion::collect(c);
+  });
+}
+
+int mlsqr_vcycle_m_apply(mlsqr_pc* pc, const double* x, double* y, size_t n, int kind) {
+  return guard([&] {
+    require(pc && pc->vc, MLSQR_EINVAL, "not a V-cycle map");
+    Ctx* c = pc->impl->ctx;
+    set_device(c);
+    check_len(n, pc->impl->n, "M apply");
+    In in(c, x, n, kind);
+    Out out(c, y, n, kind);
+    vcycle_m_apply(pc->vc, in.d, out.d);
+    out.finish();
+  });
+}
+
+// ---- solvers ----
+static int run_solve(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                     double* f, mlsqr_iter_rec* trace, double* alphas, double* betas,
+                     mlsqr_solve_info* info, int kind, bool plain) {
+  int bd_iter = 0;
+  if (info) std::memset(info, 0, sizeof(*info));
+  const int st = guard([&] {
+    require(op && stop, MLSQR_EINVAL, "operator and stopping config are required");
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    In gin(c, g, o->rows, kind);
+    Out fout(c, f, o->cols, kind);
+    try {
+      solve_mlsqr(o, plain ? nullptr : pc->impl, gin.d, tau, *stop, fout.d, trace, alphas, betas, info);
+    } catch (const Error& e) {
+      if (e.code == MLSQR_EBREAKDOWN) bd_iter = e.iteration;
+      throw;
+    }
+    fout.finish();
+  });
+  if (st == MLSQR_EBREAKDOWN && info) info->breakdown_iteration = bd_iter;
+  return st;
+}
+
+int mlsqr_solve(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                double* f, mlsqr_iter_rec* trace, double* alphas, double* betas,
+                mlsqr_solve_info* info, int ptr_kind) {
+  if (!pc) {
+    g_err = "mlsqr needs a preconditioner map (use mlsqr_identity_map_create for M = I)";
+    return MLSQR_EINVAL;
+  }
+  return run_solve(op, pc, g, tau, stop, f, trace, alphas, betas, info, ptr_kind, false);
+}
+
+int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop* stop, double* f,
+                     mlsqr_iter_rec* trace, double* alphas, double* betas, mlsqr_solve_info* info,
+                     int ptr_kind) {
+  return run_solve(op, nullptr, g, tau, stop, f, trace, alphas, betas, info, ptr_kind, true);
+}
+
+int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, size_t ny,
+                          size_t nz, double h, const mlsqr_outer_cfg* cfg, double* f_out,
+                          mlsqr_outer_step* steps, int* n_steps, int* stop_reason,
+                          int* triggered_at, double* alphas, double* betas, int kind) {
+  return guard([&] {
+    require(op && cfg && steps && n_steps && stop_reason && triggered_at, MLSQR_EINVAL,
+            "nonlinear_solve: null argument");
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    In gin(c, g, o->rows, kind);
+    Out fout(c, f_out, o->cols, kind);
+    nonlinear_solve(o, gin.d, dims, nx, ny, nz, h, *cfg, fout.d, steps, n_steps, stop_reason,
+                    triggered_at, alphas, betas);
+    fout.finish();
+  });
+}
+
+int mlsqr_penalty_functional(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz, double h,
+                             const double* f, int kind, int pen_kind, double T, double* value) {
+  return guard([&] {
+    Ctx* c = &ctx->impl;
+    set_device(c);
+    require(dims >= 1 && dims <= 3, MLSQR_EINVAL, "grid must be 1D, 2D or 3D");
+    const size_t n = nx * (dims >= 2 ? ny : 1) * (dims >= 3 ? nz : 1);
+    In in(c, f, n, kind);
+    *value = penalty_functional_dev(c, dims, nx, ny, nz, h, in.d, pen_kind, T);
+  });
+}
+
+}  // extern "C"

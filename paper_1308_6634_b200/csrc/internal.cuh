@@ -1,0 +1,334 @@
+// internal.cuh -- shared device helpers and host-side object model of the
+// B200-native MLSQR path.  See DESIGN.md for the data layout and the
+// "canonical arithmetic order" every kernel here implements (bit-exact with
+// the oracle's DEVICE order).  Compiled with -fmad=false: no mul+add pair is
+// ever contracted, exactly like the reference's scalar backend.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mlsqr_b200.h"
+
+namespace mlsqr_b200 {
+
+// ---------------------------------------------------------------------------
+// errors: C++ exceptions inside the library, status codes at the C-ABI
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  int iteration;
+  Error(int c, const std::string& m, int it = 0) : std::runtime_error(m), code(c), iteration(it) {}
+};
+
+#define MLSQR_CUDA(call)                                                                  \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::mlsqr_b200::Error(MLSQR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+// ---------------------------------------------------------------------------
+// canonical reductions: segments of 32 consecutive row elements
+// reduced by the shuffle-down tree; then tree-32 levels over partials.
+// ---------------------------------------------------------------------------
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// lane 0 receives v[0]+v[16] ... : the canonical tree32
+__device__ __forceinline__ double tree32(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_down_sync(kFull, v, off);
+  return v;
+}
+
+// serial emulation of tree32 over 32 values held by one thread
+__device__ __forceinline__ double tree32_serial(double* v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int l = 0; l < off; ++l) v[l] = v[l] + v[l + off];
+  return v[0];
+}
+
+// vector layout for reductions: `rows` rows of `len` elements, row-major
+struct RowShape {
+  size_t len;   // elements per row (x extent)
+  size_t rows;  // number of rows (ny * nz)
+  size_t chunks() const { return (len + 31) / 32; }
+  size_t segments() const { return chunks() * rows; }
+  size_t n() const { return len * rows; }
+};
+
+// deterministic hypot from IEEE basic operations (oracle orc_dhypot)
+__host__ __device__ inline double dhypot(double a, double b) {
+  a = fabs(a);
+  b = fabs(b);
+  if (a < b) {
+    const double t = a;
+    a = b;
+    b = t;
+  }
+  if (a == 0.0) return 0.0;
+  if (isinf(a)) return a;
+  const double r = b / a;
+  return a * sqrt(1.0 + r * r);
+}
+
+// penalty.cpp:60-84 with the device hypot
+__host__ __device__ inline double diffusivity(int kind, double T, double t) {
+  double c = 1.0;
+  switch (kind) {
+    case MLSQR_PEN_TIKHONOV: return 1.0;
+    case MLSQR_PEN_TV: c = 1.0 / dhypot(T, t); break;
+    case MLSQR_PEN_PM_LOG: {
+      const double u = t / T;
+      c = u > 1e8 ? (T / t) * (T / t) : 1.0 / (1.0 + u * u);
+      break;
+    }
+    case MLSQR_PEN_PM_EXP: {
+      const double u = t / T;
+      c = exp(-u * u);
+      break;
+    }
+  }
+  const double dmin = 2.2250738585072014e-308;  // DBL_MIN (penalty.cpp:83)
+  return c > dmin ? c : dmin;
+}
+
+// penalty.cpp:35-53
+__host__ __device__ inline double r_value(int kind, double T, double t) {
+  switch (kind) {
+    case MLSQR_PEN_TIKHONOV: return 0.5 * t * t;
+    case MLSQR_PEN_TV: return dhypot(T, t);
+    case MLSQR_PEN_PM_LOG: {
+      const double u = t / T;
+      return 0.5 * T * T * log1p(u * u);
+    }
+    case MLSQR_PEN_PM_EXP: {
+      const double u = t / T;
+      return 0.5 * T * T * (1.0 - exp(-u * u));
+    }
+  }
+  return 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// host object model
+// ---------------------------------------------------------------------------
+struct Ctx;
+
+// Fused epilogue of an operator application:
+//   out = A (x * sx)  [+ coef * (old * so)],  seg <- canonical segment partials of out^2
+// All scalars are DEVICE pointers (the iteration never syncs with the host); a null
+// pointer means "1" for sx/so and "no term" for old.  gate: skip when *gate == 0.
+struct Epi {
+  const double* sx = nullptr;
+  const double* old = nullptr;
+  const double* so = nullptr;
+  const double* coef = nullptr;
+  double* seg = nullptr;
+  const int* gate = nullptr;
+};
+
+class Op {
+ public:
+  virtual ~Op() = default;
+  Ctx* ctx = nullptr;
+  size_t rows = 0, cols = 0;
+  RowShape data_shape{}, sol_shape{};
+  virtual void apply(const double* x, double* y, const Epi& e) = 0;
+  virtual void adjoint(const double* y, double* x, const Epi& e) = 0;
+  virtual int tclass() const { return MLSQR_TCLASS_BLUR; }
+};
+
+class Pc {
+ public:
+  virtual ~Pc() = default;
+  Ctx* ctx = nullptr;
+  size_t n = 0;
+  // v = B p on the device; seg (optional) <- segment partials of v*p laid out over
+  // `shape` (the operator's solution space); gate as in Epi
+  virtual void solve(const double* p, double* v, double* seg, const int* gate, RowShape shape) = 0;
+  virtual bool host_callback() const { return false; }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint64_t launches = 0;
+  bool timing = false;
+  double t_ms[MLSQR_TCLASS_COUNT] = {};
+  uint64_t t_n[MLSQR_TCLASS_COUNT] = {};
+  int sm_count = 148;
+  size_t l2_bytes = 0;
+
+  void count(int k = 1) { launches += (uint64_t)k; }
+  void check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(MLSQR_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+};
+
+// scoped timing of one kernel class (CUDA events on the context stream)
+class TimedRegion {
+ public:
+  TimedRegion(Ctx* c, int cls) : c_(c), cls_(cls) {
+    if (!c_->timing || cls_ < 0) return;
+    cudaEventCreate(&a_);
+    cudaEventCreate(&b_);
+    cudaEventRecord(a_, c_->stream);
+  }
+  ~TimedRegion() {
+    if (!c_->timing || cls_ < 0) return;
+    cudaEventRecord(b_, c_->stream);
+    pending().push_back({a_, b_, cls_});
+  }
+  struct Pending {
+    cudaEvent_t a, b;
+    int cls;
+  };
+  static std::vector<Pending>& pending() {
+    static thread_local std::vector<Pending> p;
+    return p;
+  }
+  static void collect(Ctx* c) {
+    auto& p = pending();
+    if (p.empty()) return;
+    cudaEventSynchronize(p.back().b);
+    for (auto& e : p) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      c->t_ms[e.cls] += ms;
+      c->t_n[e.cls] += 1;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    p.clear();
+  }
+
+ private:
+  Ctx* c_;
+  int cls_;
+  cudaEvent_t a_{}, b_{};
+};
+
+// device buffer (RAII)
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count) MLSQR_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+// ---------------------------------------------------------------------------
+// kernels shared across translation units (defined in reduce.cu / vec.cu)
+// ---------------------------------------------------------------------------
+// canonical reduction of `nseg` segment partials -> out (device scalar)
+void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, double* out,
+                     const int* gate);
+size_t reduce_scratch_size(size_t nseg);
+// segment partials of (x .* y) over a row shape (both unscaled)
+void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, const int* gate);
+// out = x * sx + coef * (old * so) elementwise (identity operator / copies), with seg of out^2
+void axpby_epi(Ctx* c, const double* x, double* out, RowShape s, const Epi& e);
+
+// ---------------------------------------------------------------------------
+// operator / map factories (blur.cu, dense.cu, vcycle.cu)
+// ---------------------------------------------------------------------------
+Op* make_blur(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, const double* taps, int radius);
+Op* make_dense(Ctx* c, size_t rows, size_t cols, const double* a, bool a_on_device,
+               size_t sol_row_len);
+Op* make_dense_fdot(Ctx* c, size_t nvox, int nsrc, int ndet, const double* gs, const double* gd,
+                    size_t sol_row_len);
+Op* make_identity(Ctx* c, size_t n, size_t row_len);
+
+class VCycle;
+Pc* make_identity_map(Ctx* c, size_t n);
+VCycle* make_vcycle(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h, int levels,
+                    int nu_pre, int nu_post, double omega, int coarse_sweeps);
+void vcycle_set_coefficients(VCycle* v, const double* cx, const double* cy, const double* cz,
+                             double eps);  // device pointers
+double vcycle_update(VCycle* v, const double* f_dev, int pen_kind, double T, double eps);
+void vcycle_m_apply(VCycle* v, const double* x, double* y);
+void vcycle_update_async(VCycle* v, const double* f_dev, int pen_kind, double T, double eps);
+const double* vcycle_eps_dev(VCycle* v);
+Pc* vcycle_as_pc(VCycle* v);
+size_t vcycle_sol_len(VCycle* v);
+void penalty_functional_async(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
+                              const double* f, int kind, double T, double* seg, double* scratch,
+                              double* out);
+Pc* make_callback_map(Ctx* c, size_t n, mlsqr_host_map_fn fn, void* user);
+double penalty_functional_dev(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
+                              const double* f, int pen_kind, double T);
+
+// solvers (lsqr.cu)
+struct Workspace;  // per-solve device buffers, reusable across outer steps
+Workspace* workspace_new(Ctx* c, size_t rows, size_t cols, RowShape data, RowShape sol,
+                         int max_iters);
+void workspace_free(Workspace* w);
+// Runs mlsqr (or lsqr when pc == nullptr) fully on the device.  Outputs to host arrays
+// when non-null.  `sync_out`: copy results back and return status; when false the solve
+// stays queued (outer loop) and results must be fetched with solve_fetch().
+int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
+                double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
+                mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true);
+void validate_stop(const mlsqr_stop& s);
+// solve_nonlinear (outer.cu)
+void nonlinear_solve(Op* o, const double* g_dev, int dims, size_t nx, size_t ny, size_t nz,
+                     double h, const mlsqr_outer_cfg& cfg, double* f_dev, mlsqr_outer_step* steps,
+                     int* n_steps, int* stop_reason, int* triggered_at, double* alphas,
+                     double* betas);
+
+}  // namespace mlsqr_b200
+
+struct mlsqr_ctx {
+  mlsqr_b200::Ctx impl;
+};
+struct mlsqr_op {
+  mlsqr_b200::Op* impl;
+};
+struct mlsqr_pc {
+  mlsqr_b200::Pc* impl;
+  mlsqr_b200::VCycle* vc;  // non-null for V-cycle maps
+};

@@ -1,0 +1,560 @@
+// lsqr.cu -- the device-resident priorconditioned LSQR loop (mlsqr,
+// krylov.cpp:335-440) and its M = I reduction (lsqr, krylov.cpp:256-333).
+//
+// Every scalar of the reference loop lives in device memory (DevState); the
+// LsqrRecurrence (krylov.cpp:24-108), finish_iteration (krylov.cpp:131-180)
+// and evaluate_stopping (krylov.cpp:240-254) run in one device thread after
+// each canonical reduction, so an iteration never waits on the host and the
+// whole iteration is one replayable CUDA graph.  Vectors are stored
+// UNSCALED (u_s, p_s, v_s) with their 1/beta, 1/alpha factors kept on the
+// device; every consumer multiplies on load, which reproduces the
+// reference's scal() results bit-for-bit while saving a full pass each.
+//
+// Per iteration (gates skip work once stopped / on clean breakdown):
+//   K_A   u_s <- A(v_s*sv) - alpha (u_s*su)     + |u|^2 segments   (krylov.cpp:389-391)
+//   F_b   beta = sqrt(.), su = 1/beta
+//   K_B   p_s <- A^T(u_s*su) - beta (p_s*sv)    + |p|^2 segments   (krylov.cpp:395-398)
+//   F_p   p != 0 ?
+//   MG    v_s <- M^{-1} p_s                     + v.p segments     (krylov.cpp:399-400)
+//   F_a   alpha' = sqrt(v.p), LsqrRecurrence::advance               (krylov.cpp:401-415)
+//   K_U   f += phi/rho w; w <- v - theta/rho w; q <- p - theta/rho q + w.q segments
+//   [K_R  |g - A f| when S4 needs the exact residual (krylov.cpp:142-144)]
+//   F_i   trace row + stopping                                        (krylov.cpp:131-180)
+#include "internal.cuh"
+#include "vec.cuh"
+
+namespace mlsqr_b200 {
+
+struct DevState {
+  // LSQR scalars
+  double alpha, beta, sv, su, neg_alpha, neg_beta, sc, neg_dc, wnorm2, alpha_next;
+  double minus_one;
+  // reduction outputs
+  double red_u, red_p, red_vp, red_wq, red_res;
+  // LsqrRecurrence (krylov.cpp:101-117)
+  double tau, damp, alpha_cur, phibar, rhobar, bnorm, rnorm, arnorm, anorm2, ddnorm, res2, cs2,
+      sn2, z, xxnorm, xnorm;
+  // flags: 0 active, 1 beta > 0, 2 p != 0 (run M^-1), 3 no breakdown (update w, q)
+  int flags[4];
+  int iter, iterations, stop_reason, error, error_iter, n_alphas, n_betas, breakdown;
+};
+
+struct Workspace {
+  Ctx* ctx;
+  size_t rows, cols;
+  RowShape data, sol;
+  int max_iters;
+  DevBuf<double> u, p, v, w, q, tmp_rows;
+  DevBuf<double> seg_u, seg_p, seg_vp, seg_wq, seg_res, scratch;
+  DevBuf<DevState> st;
+  DevBuf<mlsqr_iter_rec> trace;
+  DevBuf<double> alphas, betas;
+  DevBuf<double> g;  // device copy of host data
+  DevBuf<double> f;
+};
+
+Workspace* workspace_new(Ctx* c, size_t rows, size_t cols, RowShape data, RowShape sol,
+                         int max_iters) {
+  auto* w = new Workspace();
+  w->ctx = c;
+  w->rows = rows;
+  w->cols = cols;
+  w->data = data;
+  w->sol = sol;
+  w->max_iters = max_iters;
+  w->u.alloc(rows);
+  w->p.alloc(cols);
+  w->v.alloc(cols);
+  w->w.alloc(cols);
+  w->q.alloc(cols);
+  w->seg_u.alloc(data.segments());
+  w->seg_res.alloc(data.segments());
+  w->seg_p.alloc(sol.segments());
+  w->seg_vp.alloc(sol.segments());
+  w->seg_wq.alloc(sol.segments());
+  const size_t sc = reduce_scratch_size(data.segments() > sol.segments() ? data.segments() : sol.segments());
+  w->scratch.alloc(sc);
+  w->st.alloc(1);
+  w->trace.alloc((size_t)max_iters);
+  w->alphas.alloc((size_t)max_iters + 1);
+  w->betas.alloc((size_t)max_iters + 2);
+  return w;
+}
+
+void workspace_free(Workspace* w) { delete w; }
+
+// ---------------------------------------------------------------------------
+// device scalar logic
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void rec_init(DevState& s, double alpha1, double beta1, double tau) {
+  s.tau = tau;
+  s.damp = sqrt(tau);
+  s.alpha_cur = alpha1;
+  s.phibar = beta1;
+  s.rhobar = alpha1;
+  s.bnorm = beta1;
+  s.rnorm = beta1;
+  s.arnorm = 0.0;
+  s.anorm2 = 0.0;
+  s.ddnorm = 0.0;
+  s.res2 = 0.0;
+  s.cs2 = -1.0;
+  s.sn2 = 0.0;
+  s.z = 0.0;
+  s.xxnorm = 0.0;
+  s.xnorm = 0.0;
+}
+
+// LsqrRecurrence::advance (krylov.cpp:40-81), same operation order; hypot -> dhypot
+__device__ __forceinline__ void rec_advance(DevState& r, double beta_next, double alpha_next,
+                                            double wnorm2, double* sol_coeff, double* dir_coeff) {
+  r.anorm2 = r.anorm2 + (r.alpha_cur * r.alpha_cur + beta_next * beta_next + r.tau);
+  double rhobar1 = r.rhobar, psi = 0.0;
+  if (r.damp > 0.0) {
+    rhobar1 = dhypot(r.rhobar, r.damp);
+    const double cs1 = r.rhobar / rhobar1;
+    psi = (r.damp / rhobar1) * r.phibar;
+    r.phibar = cs1 * r.phibar;
+  }
+  const double rho = dhypot(rhobar1, beta_next);
+  const double cs = rhobar1 / rho;
+  const double sn = beta_next / rho;
+  const double theta = sn * alpha_next;
+  r.rhobar = -cs * alpha_next;
+  const double phi = cs * r.phibar;
+  r.phibar = sn * r.phibar;
+  r.ddnorm = r.ddnorm + wnorm2 / (rho * rho);
+  const double delta = r.sn2 * rho;
+  const double gambar = -r.cs2 * rho;
+  const double rhs = phi - delta * r.z;
+  const double zbar = rhs / gambar;
+  r.xnorm = sqrt(r.xxnorm + zbar * zbar);
+  const double gamma = dhypot(gambar, theta);
+  r.cs2 = gambar / gamma;
+  r.sn2 = theta / gamma;
+  r.z = rhs / gamma;
+  r.xxnorm = r.xxnorm + r.z * r.z;
+  r.res2 = r.res2 + psi * psi;
+  r.rnorm = sqrt(r.phibar * r.phibar + r.res2);
+  r.arnorm = alpha_next * fabs(sn * phi);
+  r.alpha_cur = alpha_next;
+  *sol_coeff = phi / rho;
+  *dir_coeff = theta / rho;
+}
+
+__global__ void init_state_kernel(DevState* s, double tau) {
+  DevState z = {};
+  z.tau = tau;
+  z.minus_one = -1.0;
+  z.flags[0] = 1;
+  z.stop_reason = MLSQR_STOP_MAX_ITERS;
+  *s = z;
+}
+
+// FI1: beta1 = |g|
+__global__ void fin_beta1_kernel(DevState* s, double* betas) {
+  s->beta = sqrt(s->red_u);
+  betas[0] = s->beta;
+  s->n_betas = 1;
+  if (s->beta == 0.0) {
+    s->stop_reason = MLSQR_STOP_BREAKDOWN;
+    s->flags[0] = 0;
+    return;
+  }
+  s->su = 1.0 / s->beta;
+}
+
+// FI2: |A^T u| == 0 -> clean breakdown before the first iteration
+__global__ void fin_p0_kernel(DevState* s) {
+  if (!s->flags[0]) return;
+  if (sqrt(s->red_p) == 0.0) {
+    s->stop_reason = MLSQR_STOP_BREAKDOWN;
+    s->flags[0] = 0;
+  }
+}
+
+// FI3: alpha1 = sqrt(v.p) > 0 else BreakdownError(0)
+__global__ void fin_alpha1_kernel(DevState* s, double* alphas) {
+  if (!s->flags[0]) return;
+  const double s0 = s->red_vp;
+  if (!(s0 > 0.0)) {
+    s->error = 1;
+    s->error_iter = 0;
+    s->flags[0] = 0;
+    return;
+  }
+  const double alpha1 = sqrt(s0);
+  s->sv = 1.0 / alpha1;
+  alphas[0] = alpha1;
+  s->n_alphas = 1;
+  rec_init(*s, alpha1, s->beta, s->tau);
+  s->alpha = alpha1;
+  s->neg_alpha = -alpha1;
+  s->iter = 1;
+}
+
+__global__ void fin_wq0_kernel(DevState* s) {
+  if (!s->flags[0]) return;
+  s->wnorm2 = s->red_wq;
+}
+
+// F_b (krylov.cpp:391-395)
+__global__ void fin_beta_kernel(DevState* s) {
+  if (!s->flags[0]) return;
+  const double beta = sqrt(s->red_u);
+  s->beta = beta;
+  s->flags[1] = beta > 0.0 ? 1 : 0;
+  s->flags[2] = 0;
+  if (beta > 0.0) {
+    s->su = 1.0 / beta;
+    s->neg_beta = -beta;
+  }
+}
+
+// F_p (krylov.cpp:398)
+__global__ void fin_p_kernel(DevState* s) {
+  if (!s->flags[0] || !s->flags[1]) return;
+  s->flags[2] = sqrt(s->red_p) > 0.0 ? 1 : 0;
+}
+
+// F_a (krylov.cpp:399-431)
+__global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) {
+  if (!s->flags[0]) return;
+  double alpha_next = 0.0;
+  int breakdown = 1;
+  if (s->flags[2]) {
+    const double sv = s->red_vp;
+    if (!(sv > 0.0)) {
+      s->error = 1;
+      s->error_iter = s->iter;
+      s->flags[0] = s->flags[1] = s->flags[2] = s->flags[3] = 0;
+      return;
+    }
+    alpha_next = sqrt(sv);
+    s->sv = 1.0 / alpha_next;
+    breakdown = 0;
+  }
+  double sc, dc;
+  rec_advance(*s, s->beta, alpha_next, s->wnorm2, &sc, &dc);
+  s->sc = sc;
+  s->neg_dc = -dc;
+  s->breakdown = breakdown;
+  s->flags[3] = breakdown ? 0 : 1;
+  if (!breakdown) alphas[s->n_alphas++] = alpha_next;
+  betas[s->n_betas++] = s->beta;
+  s->alpha_next = alpha_next;
+  s->alpha = alpha_next;
+  s->neg_alpha = -alpha_next;
+}
+
+// F_i: finish_iteration (krylov.cpp:131-180) + evaluate_stopping (krylov.cpp:240-254)
+__global__ void fin_iter_kernel(DevState* s, mlsqr_iter_rec* trace, mlsqr_stop stop) {
+  if (!s->flags[0]) return;
+  if (s->flags[3]) s->wnorm2 = s->red_wq;
+  const int iter = s->iter;
+  mlsqr_iter_rec row;
+  row.iteration = iter;
+  row.res_damped = s->rnorm;
+  if (s->tau == 0.0) {
+    row.res_data = s->rnorm;
+    row.res_data_exact = 1;
+  } else if (stop.use_s4) {
+    row.res_data = sqrt(s->red_res);
+    row.res_data_exact = 1;
+  } else {
+    const double est = s->rnorm * s->rnorm - s->tau * s->xnorm * s->xnorm;
+    row.res_data = sqrt(est > 0.0 ? est : 0.0);
+    row.res_data_exact = 0;
+  }
+  const double anorm = sqrt(s->anorm2);
+  const double acond = anorm * sqrt(s->ddnorm);
+  const double den = anorm * s->rnorm;
+  row.s2_value = den > 0.0 ? s->arnorm / den : 0.0;
+  row.anorm_est = anorm;
+  row.cond_est = acond;
+  row.xnorm_est = s->xnorm;
+  row.alpha = s->alpha_next;
+  row.beta = s->beta;
+  trace[iter - 1] = row;
+  s->iterations = iter;
+  int fired = -1;
+  if (stop.use_s4 && row.res_data <= stop.eta * stop.delta) fired = MLSQR_STOP_S4;
+  else if (stop.use_s1 && s->rnorm <= stop.btol * s->bnorm + stop.atol * anorm * s->xnorm) fired = MLSQR_STOP_S1;
+  else if (stop.use_s2 && (s->arnorm <= stop.atol * den || den == 0.0)) fired = MLSQR_STOP_S2;
+  else if (stop.use_s3 && stop.conlim > 0.0 && acond >= stop.conlim) fired = MLSQR_STOP_S3;
+  else if (iter >= stop.max_iters) fired = MLSQR_STOP_MAX_ITERS;
+  if (fired < 0 && s->breakdown) fired = MLSQR_STOP_BREAKDOWN;
+  if (fired >= 0) {
+    s->stop_reason = fired;
+    s->flags[0] = s->flags[1] = s->flags[2] = s->flags[3] = 0;
+  }
+  s->iter = iter + 1;
+}
+
+// K_U (krylov.cpp:416-419): f += sc w; [w <- v*sv - dc w; q <- p*sv - dc q; w.q partials]
+__global__ void __launch_bounds__(256) update_kernel(const DevState* __restrict__ s,
+                                                     double* __restrict__ f,
+                                                     double* __restrict__ w,
+                                                     double* __restrict__ q,
+                                                     const double* __restrict__ v,
+                                                     const double* __restrict__ p, size_t len,
+                                                     size_t rows, double* __restrict__ seg) {
+  if (!s->flags[0]) return;
+  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+  const bool upd = s->flags[3] != 0;
+  double prod = 0.0;
+  if (xi < len) {
+    const size_t i = row * len + xi;
+    const double wi = w[i];
+    f[i] = f[i] + s->sc * wi;
+    if (upd) {
+      const double sv = s->sv, ndc = s->neg_dc;
+      const double wn = v[i] * sv + ndc * wi;
+      const double qn = p[i] * sv + ndc * q[i];
+      w[i] = wn;
+      q[i] = qn;
+      prod = wn * qn;
+    }
+  }
+  if (upd) {
+    const double t = tree32(prod);
+    if (threadIdx.x == 0) seg[row * ((len + 31) / 32) + blockIdx.x] = t;
+  }
+}
+
+// init: w = v*sv, q = p*sv, f = 0, w.q partials
+__global__ void init_wq_kernel(const DevState* __restrict__ s, double* __restrict__ f,
+                               double* __restrict__ w, double* __restrict__ q,
+                               const double* __restrict__ v, const double* __restrict__ p,
+                               size_t len, size_t rows, double* __restrict__ seg) {
+  if (!s->flags[0]) return;
+  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+  double prod = 0.0;
+  if (xi < len) {
+    const size_t i = row * len + xi;
+    const double sv = s->sv;
+    const double wn = v[i] * sv, qn = p[i] * sv;
+    w[i] = wn;
+    q[i] = qn;
+    f[i] = 0.0;
+    prod = wn * qn;
+  }
+  const double t = tree32(prod);
+  if (threadIdx.x == 0) seg[row * ((len + 31) / 32) + blockIdx.x] = t;
+}
+
+__global__ void zero_kernel(double* __restrict__ f, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = 0.0;
+}
+
+void validate_stop(const mlsqr_stop& s) {  // StoppingConfig::validate (krylov.cpp:219-226)
+  require(s.max_iters >= 1, MLSQR_EINVAL, "max_iters must be at least 1");
+  require(!s.use_s4 || s.eta > 1.0, MLSQR_EINVAL, "discrepancy stopping needs a safety factor eta > 1");
+  require(!s.use_s4 || s.delta >= 0.0, MLSQR_EINVAL, "noise level delta must be >= 0");
+  require(s.atol >= 0.0 && s.btol >= 0.0, MLSQR_EINVAL, "tolerances must be >= 0");
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Runner {
+  Op* op;
+  Pc* pc;  // nullptr: plain lsqr (v aliases p)
+  Workspace* ws;
+  double tau;
+  mlsqr_stop stop;
+  DevState* st;
+  Ctx* c;
+
+  const int* flag(int k) const { return &st->flags[k]; }
+  const int* gate_active() const { return flag(0); }
+
+  void reduce(double* seg, size_t nseg, double* out, const int* gate) {
+    reduce_segments(c, seg, nseg, ws->scratch.p, out, gate);
+  }
+
+  double* vbuf() const { return pc ? ws->v.p : ws->p.p; }
+
+  void precond(const int* gate) {
+    if (pc) {
+      pc->solve(ws->p.p, ws->v.p, ws->seg_vp.p, gate, ws->sol);
+    } else {
+      seg_dot(c, ws->p.p, ws->p.p, ws->sol, ws->seg_vp.p, gate);
+    }
+    reduce(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate);
+  }
+
+  void init(const double* g) {
+    init_state_kernel<<<1, 1, 0, c->stream>>>(st, tau);
+    // u_s = g, |g|^2
+    Epi e;
+    e.seg = ws->seg_u.p;
+    axpby_epi(c, g, ws->u.p, ws->data, e);
+    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, nullptr);
+    fin_beta1_kernel<<<1, 1, 0, c->stream>>>(st, ws->betas.p);
+    // p_s = A^T (u_s * su), |p|^2
+    Epi eb;
+    eb.sx = &st->su;
+    eb.seg = ws->seg_p.p;
+    eb.gate = gate_active();
+    op->adjoint(ws->u.p, ws->p.p, eb);
+    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, gate_active());
+    fin_p0_kernel<<<1, 1, 0, c->stream>>>(st);
+    precond(gate_active());
+    fin_alpha1_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p);
+    dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
+    init_wq_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
+                                               ws->sol.len, ws->sol.rows, ws->seg_wq.p);
+    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, gate_active());
+    fin_wq0_kernel<<<1, 1, 0, c->stream>>>(st);
+    c->count(6);
+    c->check_launch();
+  }
+
+  void iteration(const double* g) {
+    TimedRegion it(c, MLSQR_TCLASS_ITER);
+    // K_A: u_s <- A(v_s*sv) + (-alpha)(u_s*su)
+    Epi ea;
+    ea.sx = &st->sv;
+    ea.old = ws->u.p;
+    ea.so = &st->su;
+    ea.coef = &st->neg_alpha;
+    ea.seg = ws->seg_u.p;
+    ea.gate = gate_active();
+    op->apply(vbuf(), ws->u.p, ea);
+    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active());
+    fin_beta_kernel<<<1, 1, 0, c->stream>>>(st);
+    // K_B: p_s <- A^T(u_s*su) + (-beta)(p_s*sv)
+    Epi eb;
+    eb.sx = &st->su;
+    eb.old = ws->p.p;
+    eb.so = &st->sv;
+    eb.coef = &st->neg_beta;
+    eb.seg = ws->seg_p.p;
+    eb.gate = flag(1);
+    op->adjoint(ws->u.p, ws->p.p, eb);
+    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1));
+    fin_p_kernel<<<1, 1, 0, c->stream>>>(st);
+    // M^{-1}
+    precond(flag(2));
+    fin_alpha_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p, ws->betas.p);
+    // K_U
+    {
+      TimedRegion tr(c, MLSQR_TCLASS_UPDATE);
+      dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
+      update_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
+                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
+    }
+    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3));
+    if (tau != 0.0 && stop.use_s4) {
+      // exact data residual |g - A f| (krylov.cpp:142-144): (A f - g)^2 partials
+      Epi er;
+      er.old = g;
+      er.coef = &st->minus_one;
+      er.seg = ws->seg_res.p;
+      er.gate = gate_active();
+      op->apply(ws->f.p, ws->tmp_rows.p, er);
+      reduce(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active());
+    }
+    fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
+    c->count(5);
+    c->check_launch();
+  }
+};
+
+}  // namespace
+
+int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
+                double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
+                mlsqr_solve_info* info, Workspace* ws_in, bool use_graph) {
+  Ctx* c = op->ctx;
+  validate_stop(stop);
+  require(tau >= 0.0, MLSQR_EINVAL, "tau must be nonnegative");
+  if (pc) require(pc->n == op->cols, MLSQR_EDIM, "preconditioner dimension does not match operator columns");
+  std::unique_ptr<Workspace> own;
+  Workspace* ws = ws_in;
+  if (!ws || ws->rows != op->rows || ws->cols != op->cols || ws->max_iters < stop.max_iters) {
+    own.reset(workspace_new(c, op->rows, op->cols, op->data_shape, op->sol_shape, stop.max_iters));
+    ws = own.get();
+  }
+  if (tau != 0.0 && stop.use_s4) ws->tmp_rows.ensure(op->rows);
+  // f lives in the caller's buffer
+  struct FGuard {
+    Workspace* ws;
+    double* saved;
+    size_t n;
+    ~FGuard() { ws->f.p = saved; ws->f.n = n; }
+  } fg{ws, ws->f.p, ws->f.n};
+  ws->f.p = f_dev;
+  ws->f.n = op->cols;
+
+  Runner r{op, pc, ws, tau, stop, ws->st.p, c};
+  const bool host_cb = pc && pc->host_callback();
+  const bool graph = use_graph && !host_cb && !c->timing;
+  r.init(g_dev);
+  if (graph) {
+    cudaGraph_t gr = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    MLSQR_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      r.iteration(g_dev);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &gr);
+      if (gr) cudaGraphDestroy(gr);
+      throw;
+    }
+    MLSQR_CUDA(cudaStreamEndCapture(c->stream, &gr));
+    MLSQR_CUDA(cudaGraphInstantiate(&ge, gr, 0));
+    for (int i = 0; i < stop.max_iters; ++i) MLSQR_CUDA(cudaGraphLaunch(ge, c->stream));
+    MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(gr);
+  } else {
+    for (int i = 0; i < stop.max_iters; ++i) {
+      if (host_cb) {
+        // a host plug-in map must see every iteration's state: stop enqueueing once done
+        int active = 0;
+        MLSQR_CUDA(cudaMemcpyAsync(&active, &ws->st.p->flags[0], sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+        if (!active) break;
+      }
+      r.iteration(g_dev);
+    }
+  }
+  DevState hs;
+  MLSQR_CUDA(cudaMemcpyAsync(&hs, ws->st.p, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+  TimedRegion::collect(c);
+  const int na = hs.n_alphas > hs.iterations ? hs.iterations : hs.n_alphas;  // trim_bidiag
+  if (trace && hs.iterations > 0)
+    MLSQR_CUDA(cudaMemcpy(trace, ws->trace.p, sizeof(mlsqr_iter_rec) * hs.iterations, cudaMemcpyDeviceToHost));
+  if (alphas && hs.n_alphas > 0)
+    MLSQR_CUDA(cudaMemcpy(alphas, ws->alphas.p, sizeof(double) * hs.n_alphas, cudaMemcpyDeviceToHost));
+  if (betas && hs.n_betas > 0)
+    MLSQR_CUDA(cudaMemcpy(betas, ws->betas.p, sizeof(double) * hs.n_betas, cudaMemcpyDeviceToHost));
+  if (info) {
+    info->iterations = hs.iterations;
+    info->stop_reason = hs.stop_reason;
+    info->n_alphas = hs.error ? hs.n_alphas : na;
+    info->n_betas = hs.n_betas;
+    info->breakdown_iteration = hs.error_iter;
+  }
+  if (hs.error) {
+    throw Error(MLSQR_EBREAKDOWN,
+                "nonpositive M-weighted square norm at " +
+                    (hs.error_iter == 0 ? std::string("initialization")
+                                        : "iteration " + std::to_string(hs.error_iter)) +
+                    "; the preconditioner map is not symmetric positive definite",
+                hs.error_iter);
+  }
+  return MLSQR_OK;
+}
+
+}  // namespace mlsqr_b200

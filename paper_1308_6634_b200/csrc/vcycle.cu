@@ -1,0 +1,513 @@
+// vcycle.cu -- the priorconditioner M^{-1} as a multigrid V-cycle on the
+// edge-based diffusion operator M = L_D^T L_D + eps I, plus the per-outer-step
+// diffusivity update (SURVEY.md §2.1 K_D, K_H, K_S, K_R, K_P, K_alpha).
+//
+//  - K_D  edge_coeffs_kernel: c_e = c(|d_e|) w_e / h^2 per axis
+//         (assemble_m / for_each_edge, diffusion.cpp:27-79; penalty.cpp:60-84)
+//  - max diagonal -> eps = 1e-8 max diag (auto_shift, diffusion.cpp:81)
+//  - K_H  coarsen_kernel: Galerkin edge sums under 2^d aggregation
+//  - K_S  sweep_kernel: omega-Jacobi on the 5/7-point stencil, row sums in
+//         the CSR ascending-column order of sparse.cpp:65-74; the first sweep
+//         from zero, the prolongation and the final <v, p> partials are fused
+//  - K_R  restrict_kernel: r = b - M x summed over the 2^d children
+//  - R(f) penalty_kernel: diffusion.cpp:89-101 in canonical order
+// Storage: per level the d edge-coefficient arrays (cx, cy, cz), zero where
+// an edge is missing; no CSR is ever built (sparse.cpp's std::map assembly
+// is replaced by one pass over the field).
+#include "internal.cuh"
+#include "vec.cuh"
+
+namespace mlsqr_b200 {
+
+struct Lvl {  // POD view of one level for kernels
+  int nx, ny, nz;
+  const double* cx;
+  const double* cy;  // nullptr below 2D
+  const double* cz;  // nullptr below 3D
+  const double* eps; // device scalar
+};
+
+__device__ __forceinline__ double diag_at(const Lvl& L, int x, int y, int z, size_t i) {
+  const size_t nxy = (size_t)L.nx * L.ny;
+  double d = 0.0;
+  if (x > 0) d = d + L.cx[i - 1];
+  if (x + 1 < L.nx) d = d + L.cx[i];
+  if (L.cy) {
+    if (y > 0) d = d + L.cy[i - L.nx];
+    if (y + 1 < L.ny) d = d + L.cy[i];
+  }
+  if (L.cz) {
+    if (z > 0) d = d + L.cz[i - nxy];
+    if (z + 1 < L.nz) d = d + L.cz[i];
+  }
+  return d;
+}
+
+// value of the (possibly prolongated) iterate at fine index j
+template <bool PROLONG>
+__device__ __forceinline__ double xval(const double* __restrict__ x, const double* __restrict__ xc,
+                                       const Lvl& L, int cnx, int cny, int xx, int yy, int zz,
+                                       size_t j) {
+  double v = x[j];
+  if (PROLONG) {
+    const int Z = L.cz ? zz / 2 : 0, Y = L.cy ? yy / 2 : 0;
+    v = v + xc[((size_t)Z * cny + Y) * cnx + xx / 2];
+  }
+  return v;
+}
+
+// (M x)_i in ascending column order: z-, y-, x-, diag, x+, y+, z+
+template <bool PROLONG>
+__device__ __forceinline__ double m_row(const Lvl& L, const double* __restrict__ x,
+                                        const double* __restrict__ xc, int cnx, int cny, int xx,
+                                        int yy, int zz, size_t i, double diag) {
+  const size_t nxy = (size_t)L.nx * L.ny;
+  double acc = 0.0;
+  if (L.cz && zz > 0) acc = acc + -L.cz[i - nxy] * xval<PROLONG>(x, xc, L, cnx, cny, xx, yy, zz - 1, i - nxy);
+  if (L.cy && yy > 0) acc = acc + -L.cy[i - L.nx] * xval<PROLONG>(x, xc, L, cnx, cny, xx, yy - 1, zz, i - L.nx);
+  if (xx > 0) acc = acc + -L.cx[i - 1] * xval<PROLONG>(x, xc, L, cnx, cny, xx - 1, yy, zz, i - 1);
+  acc = acc + diag * xval<PROLONG>(x, xc, L, cnx, cny, xx, yy, zz, i);
+  if (xx + 1 < L.nx) acc = acc + -L.cx[i] * xval<PROLONG>(x, xc, L, cnx, cny, xx + 1, yy, zz, i + 1);
+  if (L.cy && yy + 1 < L.ny) acc = acc + -L.cy[i] * xval<PROLONG>(x, xc, L, cnx, cny, xx, yy + 1, zz, i + L.nx);
+  if (L.cz && zz + 1 < L.nz) acc = acc + -L.cz[i] * xval<PROLONG>(x, xc, L, cnx, cny, xx, yy, zz + 1, i + nxy);
+  return acc;
+}
+
+enum SweepMode { kFirst = 0, kNormal = 1, kProlong = 2, kProlongOnly = 3 };
+
+// one omega-Jacobi sweep: out = x + (omega * (b - M x)) / D   (x = 0 for kFirst,
+// x = x + P xc for kProlong); seg (optional) <- partials of out * b
+template <int MODE>
+__global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restrict__ x,
+                                                    const double* __restrict__ xc, int cnx, int cny,
+                                                    const double* __restrict__ b,
+                                                    double* __restrict__ out, double omega,
+                                                    double* __restrict__ seg, const int* gate) {
+  if (gate && *gate == 0) return;
+  const int rows = L.ny * L.nz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const int xx = blockIdx.x * 32 + threadIdx.x;
+  const int yy = row % L.ny, zz = row / L.ny;
+  double v = 0.0, bi = 0.0;
+  if (xx < L.nx) {
+    const size_t i = (size_t)row * L.nx + xx;
+    bi = b[i];
+    if (MODE == kProlongOnly) {
+      v = xval<true>(x, xc, L, cnx, cny, xx, yy, zz, i);
+    } else {
+      const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
+      if (MODE == kFirst) {
+        // M * 0 = +0 exactly, so x1 = 0 + (omega * (b - 0)) / d
+        const double mx = 0.0;
+        v = 0.0 + (omega * (bi - mx)) / d;
+      } else {
+        const bool P = MODE == kProlong;
+        const double mx = P ? m_row<true>(L, x, xc, cnx, cny, xx, yy, zz, i, d)
+                            : m_row<false>(L, x, xc, cnx, cny, xx, yy, zz, i, d);
+        const double xi = P ? xval<true>(x, xc, L, cnx, cny, xx, yy, zz, i) : x[i];
+        v = xi + (omega * (bi - mx)) / d;
+      }
+    }
+    out[i] = v;
+  }
+  if (seg) {
+    const double s = tree32(v * bi);
+    if (threadIdx.x == 0) seg[(size_t)row * ((L.nx + 31) / 32) + blockIdx.x] = s;
+  }
+}
+
+// y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
+__global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
+  const int rows = L.ny * L.nz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int xx = blockIdx.x * 32 + threadIdx.x;
+  if (row >= rows || xx >= L.nx) return;
+  const int yy = row % L.ny, zz = row / L.ny;
+  const size_t i = (size_t)row * L.nx + xx;
+  const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
+  y[i] = m_row<false>(L, x, nullptr, 0, 0, xx, yy, zz, i, d);
+}
+
+// b_c[I] = sum over the children (ascending fine index) of (b - M x)
+__global__ void __launch_bounds__(256) restrict_kernel(Lvl L, const double* __restrict__ x,
+                                                       const double* __restrict__ b, int cnx,
+                                                       int cny, int cnz, double* __restrict__ bc,
+                                                       const int* gate) {
+  if (gate && *gate == 0) return;
+  const int crows = cny * cnz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int X = blockIdx.x * 32 + threadIdx.x;
+  if (row >= crows || X >= cnx) return;
+  const int Y = row % cny, Z = row / cny;
+  const int zc = L.cz ? 2 : 1, yc = L.cy ? 2 : 1;
+  double s = 0.0;
+  for (int dz = 0; dz < zc; ++dz)
+    for (int dy = 0; dy < yc; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const int zz = zc * Z + dz, yy = yc * Y + dy, xx = 2 * X + dx;
+        const size_t i = ((size_t)zz * L.ny + yy) * L.nx + xx;
+        const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
+        const double r = b[i] - m_row<false>(L, x, nullptr, 0, 0, xx, yy, zz, i, d);
+        s = s + r;
+      }
+  bc[(size_t)row * cnx + X] = s;
+}
+
+// Galerkin coarse edges (oracle coarsen()): sum of the fine edges crossing each coarse face
+__global__ void coarsen_kernel(Lvl F, int cnx, int cny, int cnz, double* __restrict__ ccx,
+                               double* __restrict__ ccy, double* __restrict__ ccz) {
+  const int crows = cny * cnz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int X = blockIdx.x * 32 + threadIdx.x;
+  if (row >= crows || X >= cnx) return;
+  const int Y = row % cny, Z = row / cny;
+  const size_t fnx = F.nx, fnxy = (size_t)F.nx * F.ny;
+  const int zc = F.cz ? 2 : 1, yc = F.cy ? 2 : 1;
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  for (int dz = 0; dz < zc; ++dz)
+    for (int dy = 0; dy < yc; ++dy)
+      if (X + 1 < cnx) sx = sx + F.cx[(size_t)(zc * Z + dz) * fnxy + (size_t)(yc * Y + dy) * fnx + 2 * X + 1];
+  if (F.cy)
+    for (int dz = 0; dz < zc; ++dz)
+      for (int dx = 0; dx < 2; ++dx)
+        if (Y + 1 < cny) sy = sy + F.cy[(size_t)(zc * Z + dz) * fnxy + (size_t)(2 * Y + 1) * fnx + 2 * X + dx];
+  if (F.cz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx)
+        if (Z + 1 < cnz) sz = sz + F.cz[(size_t)(2 * Z + 1) * fnxy + (size_t)(2 * Y + dy) * fnx + 2 * X + dx];
+  const size_t I = (size_t)row * cnx + X;
+  ccx[I] = sx;
+  if (ccy) ccy[I] = sy;
+  if (ccz) ccz[I] = sz;
+}
+
+// K_D: edge coefficients from a field, plus the max unshifted diagonal (atomic max on
+// the bit pattern of non-negative doubles: order-independent, deterministic)
+__global__ void edge_coeffs_kernel(const double* __restrict__ f, int nx, int ny, int nz, int dims,
+                                   int kind, double T, double h, double scale,
+                                   double* __restrict__ cx, double* __restrict__ cy,
+                                   double* __restrict__ cz) {
+  const int rows = ny * nz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int xx = blockIdx.x * 32 + threadIdx.x;
+  if (row >= rows || xx >= nx) return;
+  const int yy = row % ny, zz = row / ny;
+  const size_t i = (size_t)row * nx + xx, nxy = (size_t)nx * ny;
+  const double fi = f[i];
+  cx[i] = xx + 1 < nx ? diffusivity(kind, T, fabs((f[i + 1] - fi) / h)) * scale : 0.0;
+  if (dims >= 2) cy[i] = yy + 1 < ny ? diffusivity(kind, T, fabs((f[i + nx] - fi) / h)) * scale : 0.0;
+  if (dims >= 3) cz[i] = zz + 1 < nz ? diffusivity(kind, T, fabs((f[i + nxy] - fi) / h)) * scale : 0.0;
+}
+
+__global__ void max_diag_kernel(Lvl L, unsigned long long* __restrict__ out) {
+  const int rows = L.ny * L.nz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int xx = blockIdx.x * 32 + threadIdx.x;
+  double d = 0.0;
+  if (row < rows && xx < L.nx) {
+    const size_t i = (size_t)row * L.nx + xx;
+    d = diag_at(L, xx, row % L.ny, row / L.ny, i);
+  }
+  // warp max (exact), then one atomic per warp
+  for (int off = 16; off >= 1; off >>= 1) d = fmax(d, __shfl_down_sync(kFull, d, off));
+  if ((threadIdx.x & 31) == 0 && d > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(d));
+}
+
+// eps_0 = given (>= 0) or 1e-8 * max diag; eps_l = eps_{l-1} * 2^d (exact)
+__global__ void set_eps_kernel(const unsigned long long* __restrict__ maxd, double eps_cfg,
+                               double mult, int levels, double* __restrict__ eps) {
+  double e = eps_cfg >= 0.0 ? eps_cfg : 1e-8 * __longlong_as_double((long long)*maxd);
+  for (int l = 0; l < levels; ++l) {
+    eps[l] = e;
+    e = e * mult;
+  }
+}
+
+// R(f): per-node sum of its x/y/z edge terms, canonical segment partials
+__global__ void penalty_kernel(const double* __restrict__ f, int nx, int ny, int nz, int dims,
+                               int kind, double T, double h, double w, double* __restrict__ seg) {
+  const int rows = ny * nz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const int xx = blockIdx.x * 32 + threadIdx.x;
+  double v = 0.0;
+  if (xx < nx) {
+    const int yy = row % ny, zz = row / ny;
+    const size_t i = (size_t)row * nx + xx, nxy = (size_t)nx * ny;
+    const double fi = f[i];
+    if (xx + 1 < nx) v = v + w * r_value(kind, T, fabs((f[i + 1] - fi) / h));
+    if (dims >= 2 && yy + 1 < ny) v = v + w * r_value(kind, T, fabs((f[i + nx] - fi) / h));
+    if (dims >= 3 && zz + 1 < nz) v = v + w * r_value(kind, T, fabs((f[i + nxy] - fi) / h));
+  }
+  const double s = tree32(v);
+  if (threadIdx.x == 0) seg[(size_t)row * ((nx + 31) / 32) + blockIdx.x] = s;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static inline dim3 row_grid(int nx, int rows) {
+  return dim3((unsigned)((nx + 31) / 32), (unsigned)((rows + 7) / 8));
+}
+
+class VCycle final : public Pc {
+ public:
+  struct Level {
+    int nx, ny, nz;
+    size_t n;
+    DevBuf<double> cx, cy, cz, xa, xb, b;
+  };
+
+  VCycle(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h, int levels, int nu_pre,
+         int nu_post, double omega, int kc)
+      : dims_(dims), h_(h), nu_pre_(nu_pre), nu_post_(nu_post), kc_(kc), omega_(omega) {
+    ctx = c;
+    require(dims >= 1 && dims <= 3, MLSQR_EINVAL, "grid must be 1D, 2D or 3D");
+    const size_t ey = dims >= 2 ? ny : 1, ez = dims >= 3 ? nz : 1;
+    require(nx >= 2 && (dims < 2 || ey >= 2) && (dims < 3 || ez >= 2), MLSQR_EDIM,
+            "grid extents must be at least 2");
+    require(h > 0.0, MLSQR_EINVAL, "grid spacing must be positive");
+    require(levels >= 1 && levels <= 16 && nu_pre >= 1 && nu_post >= 0 && kc >= 1, MLSQR_EINVAL,
+            "V-cycle needs levels >= 1, nu_pre >= 1, nu_post >= 0, coarse sweeps >= 1");
+    const size_t f = (size_t)1 << (levels - 1);
+    require(nx % f == 0 && nx / f >= 2 && (dims < 2 || (ey % f == 0 && ey / f >= 2)) &&
+                (dims < 3 || (ez % f == 0 && ez / f >= 2)),
+            MLSQR_EINVAL, "every active grid extent must halve evenly down to the coarsest level");
+    n = nx * ey * ez;
+    lv_.resize((size_t)levels);
+    for (int l = 0; l < levels; ++l) {
+      Level& L = lv_[(size_t)l];
+      L.nx = (int)(nx >> l);
+      L.ny = (int)(dims >= 2 ? ey >> l : 1);
+      L.nz = (int)(dims >= 3 ? ez >> l : 1);
+      L.n = (size_t)L.nx * L.ny * L.nz;
+      L.cx.alloc(L.n);
+      if (dims >= 2) L.cy.alloc(L.n);
+      if (dims >= 3) L.cz.alloc(L.n);
+      L.xa.alloc(L.n);
+      L.xb.alloc(L.n);
+      if (l > 0) L.b.alloc(L.n);
+    }
+    eps_.alloc((size_t)levels);
+    maxd_.alloc(1);
+    MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
+  }
+
+  Lvl view(int l) const {
+    const Level& L = lv_[(size_t)l];
+    return Lvl{L.nx, L.ny, L.nz, L.cx.p, dims_ >= 2 ? L.cy.p : nullptr,
+               dims_ >= 3 ? L.cz.p : nullptr, eps_.p + l};
+  }
+
+  double mult() const {
+    double m = 2.0;
+    if (dims_ >= 2) m *= 2.0;
+    if (dims_ >= 3) m *= 2.0;
+    return m;
+  }
+
+  // build coarse levels from level 0 (device-resident); eps_cfg < 0 -> auto shift
+  void build(double eps_cfg) {
+    Level& L0 = lv_[0];
+    MLSQR_CUDA(cudaMemsetAsync(maxd_.p, 0, sizeof(unsigned long long), ctx->stream));
+    max_diag_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(view(0), maxd_.p);
+    set_eps_kernel<<<1, 1, 0, ctx->stream>>>(maxd_.p, eps_cfg, mult(), (int)lv_.size(), eps_.p);
+    ctx->count(2);
+    for (size_t l = 1; l < lv_.size(); ++l) {
+      Level& C = lv_[l];
+      coarsen_kernel<<<row_grid(C.nx, C.ny * C.nz), dim3(32, 8), 0, ctx->stream>>>(
+          view((int)l - 1), C.nx, C.ny, C.nz, C.cx.p, dims_ >= 2 ? C.cy.p : nullptr,
+          dims_ >= 3 ? C.cz.p : nullptr);
+      ctx->count();
+    }
+    ctx->check_launch();
+  }
+
+  void set_coefficients(const double* cx, const double* cy, const double* cz, double eps) {
+    Level& L0 = lv_[0];
+    MLSQR_CUDA(cudaMemcpyAsync(L0.cx.p, cx, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (dims_ >= 2) MLSQR_CUDA(cudaMemcpyAsync(L0.cy.p, cy, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (dims_ >= 3) MLSQR_CUDA(cudaMemcpyAsync(L0.cz.p, cz, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    build(eps);
+  }
+
+  double update(const double* f, int kind, double T, double eps_cfg) {
+    Level& L0 = lv_[0];
+    const double h = h_;
+    double w = h;
+    if (dims_ >= 2) w = h * h;
+    if (dims_ >= 3) w = h * h * h;
+    const double scale = w / (h * h);
+    edge_coeffs_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(
+        f, L0.nx, L0.ny, L0.nz, dims_, kind, T, h, scale, L0.cx.p, L0.cy.p, L0.cz.p);
+    ctx->count();
+    build(eps_cfg);
+    double e = 0.0;
+    MLSQR_CUDA(cudaMemcpyAsync(&e, eps_.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MLSQR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return e;
+  }
+
+  // device-resident variant used by the outer loop (no host sync); eps stays on device
+  void update_async(const double* f, int kind, double T, double eps_cfg) {
+    Level& L0 = lv_[0];
+    const double h = h_;
+    double w = h;
+    if (dims_ >= 2) w = h * h;
+    if (dims_ >= 3) w = h * h * h;
+    const double scale = w / (h * h);
+    edge_coeffs_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(
+        f, L0.nx, L0.ny, L0.nz, dims_, kind, T, h, scale, L0.cx.p, L0.cy.p, L0.cz.p);
+    ctx->count();
+    build(eps_cfg);
+  }
+  const double* eps_dev() const { return eps_.p; }
+
+  void m_apply(const double* x, double* y) {
+    const Level& L0 = lv_[0];
+    m_apply_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(view(0), x, y);
+    ctx->count();
+    ctx->check_launch();
+  }
+
+  void solve(const double* p, double* v, double* seg, const int* gate, RowShape) override {
+    TimedRegion tr(ctx, MLSQR_TCLASS_MG);
+    level(0, p, v, seg, gate);
+    ctx->check_launch();
+  }
+
+ private:
+  template <int MODE>
+  void sweep(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
+             const int* gate) {
+    const Level& L = lv_[(size_t)l];
+    int cnx = 0, cny = 0;
+    if (l + 1 < (int)lv_.size()) {
+      cnx = lv_[(size_t)l + 1].nx;
+      cny = lv_[(size_t)l + 1].ny;
+    }
+    TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    sweep_kernel<MODE><<<row_grid(L.nx, L.ny * L.nz), dim3(32, 8), 0, ctx->stream>>>(
+        view(l), x, xc, cnx, cny, b, out, omega_, seg, gate);
+    ctx->count();
+  }
+
+  // returns the device pointer holding this level's result (== out when out != nullptr)
+  const double* level(int l, const double* b, double* out, double* seg, const int* gate) {
+    Level& L = lv_[(size_t)l];
+    const bool coarsest = l + 1 == (int)lv_.size();
+    const int pre = coarsest ? kc_ : nu_pre_;
+    double* bufs[2] = {L.xa.p, L.xb.p};
+    int nb = 0;
+    // pre-smoothing (or the whole coarse solve) from zero
+    const double* cur = nullptr;
+    for (int s = 0; s < pre; ++s) {
+      const bool last_here = coarsest && s + 1 == pre;
+      double* dst = (last_here && out) ? out : bufs[nb];
+      double* sg = (last_here && out) ? seg : nullptr;
+      if (s == 0) sweep<kFirst>(l, nullptr, nullptr, b, dst, sg, gate);
+      else sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
+      cur = dst;
+      if (dst == bufs[nb]) nb ^= 1;
+    }
+    if (coarsest) return cur;
+    Level& C = lv_[(size_t)l + 1];
+    restrict_kernel<<<row_grid(C.nx, C.ny * C.nz), dim3(32, 8), 0, ctx->stream>>>(
+        view(l), cur, b, C.nx, C.ny, C.nz, C.b.p, gate);
+    ctx->count();
+    const double* xc = level(l + 1, C.b.p, nullptr, nullptr, gate);
+    if (nu_post_ == 0) {
+      double* dst = out ? out : bufs[nb];
+      sweep<kProlongOnly>(l, cur, xc, b, dst, out ? seg : nullptr, gate);
+      return dst;
+    }
+    for (int s = 0; s < nu_post_; ++s) {
+      const bool last = s + 1 == nu_post_;
+      double* dst = (last && out) ? out : bufs[nb];
+      double* sg = (last && out) ? seg : nullptr;
+      if (s == 0) sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
+      else sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
+      cur = dst;
+      if (dst == bufs[nb]) nb ^= 1;
+    }
+    return cur;
+  }
+
+  int dims_;
+  double h_;
+  int nu_pre_, nu_post_, kc_;
+  double omega_;
+  std::vector<Level> lv_;
+  DevBuf<double> eps_;
+  DevBuf<unsigned long long> maxd_;
+};
+
+VCycle* make_vcycle(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h, int levels,
+                    int nu_pre, int nu_post, double omega, int coarse_sweeps) {
+  return new VCycle(c, dims, nx, ny, nz, h, levels, nu_pre, nu_post, omega, coarse_sweeps);
+}
+void vcycle_set_coefficients(VCycle* v, const double* cx, const double* cy, const double* cz,
+                             double eps) {
+  v->set_coefficients(cx, cy, cz, eps);
+}
+double vcycle_update(VCycle* v, const double* f, int kind, double T, double eps) {
+  return v->update(f, kind, T, eps);
+}
+void vcycle_update_async(VCycle* v, const double* f, int kind, double T, double eps) {
+  v->update_async(f, kind, T, eps);
+}
+const double* vcycle_eps_dev(VCycle* v) { return v->eps_dev(); }
+Pc* vcycle_as_pc(VCycle* v) { return v; }
+void vcycle_m_apply(VCycle* v, const double* x, double* y) { v->m_apply(x, y); }
+
+// ---------------------------------------------------------------------------
+class IdentityMap final : public Pc {
+ public:
+  IdentityMap(Ctx* c, size_t nn) {
+    ctx = c;
+    n = nn;
+  }
+  void solve(const double* p, double* v, double* seg, const int* gate, RowShape shape) override {
+    Epi e;
+    e.gate = gate;
+    axpby_epi(ctx, p, v, shape, e);
+    if (seg) seg_dot(ctx, v, p, shape, seg, gate);
+  }
+};
+Pc* make_identity_map(Ctx* c, size_t n) { return new IdentityMap(c, n); }
+
+// R(f) on the device, canonical order; returns to the host (synchronizes)
+double penalty_functional_dev(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
+                              const double* f, int kind, double T) {
+  const size_t ey = dims >= 2 ? ny : 1, ez = dims >= 3 ? nz : 1;
+  RowShape s{nx, ey * ez};
+  DevBuf<double> seg(s.segments()), scratch(reduce_scratch_size(s.segments())), out(1);
+  double w = h;
+  if (dims >= 2) w = h * h;
+  if (dims >= 3) w = h * h * h;
+  penalty_kernel<<<row_grid((int)nx, (int)(ey * ez)), dim3(32, 8), 0, c->stream>>>(
+      f, (int)nx, (int)ey, (int)ez, dims, kind, T, h, w, seg.p);
+  c->count();
+  reduce_segments(c, seg.p, s.segments(), scratch.p, out.p, nullptr);
+  double r = 0.0;
+  MLSQR_CUDA(cudaMemcpyAsync(&r, out.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+  return r;
+}
+
+void penalty_functional_async(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
+                              const double* f, int kind, double T, double* seg, double* scratch,
+                              double* out) {
+  const size_t ey = dims >= 2 ? ny : 1, ez = dims >= 3 ? nz : 1;
+  RowShape s{nx, ey * ez};
+  double w = h;
+  if (dims >= 2) w = h * h;
+  if (dims >= 3) w = h * h * h;
+  penalty_kernel<<<row_grid((int)nx, (int)(ey * ez)), dim3(32, 8), 0, c->stream>>>(
+      f, (int)nx, (int)ey, (int)ez, dims, kind, T, h, w, seg);
+  c->count();
+  reduce_segments(c, seg, s.segments(), scratch, out, nullptr);
+}
+
+}  // namespace mlsqr_b200

@@ -1,0 +1,109 @@
+// vec.cu -- canonical reductions and fused BLAS-1 passes (kernels.hpp:15-31
+// replaced).  Every dot / nrm2 of the reference (kernels_scalar.cpp:7-23)
+// becomes (1) per-32-element segment partials produced inside the kernel that
+// writes the vector, then (2) tree-32 levels over the partials, all on the
+// device with a fixed shape -> run-to-run bitwise deterministic, no atomics.
+#include "internal.cuh"
+#include "vec.cuh"
+
+namespace mlsqr_b200 {
+
+// ---------------------------------------------------------------------------
+// segment partials of x .* y over a row shape: block (32, 8) = 8 row segments
+// ---------------------------------------------------------------------------
+__global__ void seg_dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                               size_t len, size_t rows, size_t chunks, double* __restrict__ seg,
+                               const int* gate) {
+  if (gate && *gate == 0) return;
+  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (row >= rows) return;  // whole warp leaves together (warp == one row segment)
+  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+  double v = 0.0;
+  if (xi < len) {
+    const size_t i = row * len + xi;
+    v = x[i] * y[i];
+  }
+  v = tree32(v);
+  if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
+}
+
+void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, const int* gate) {
+  if (s.n() == 0) return;
+  dim3 blk(32, 8), grd((unsigned)s.chunks(), (unsigned)((s.rows + 7) / 8));
+  seg_dot_kernel<<<grd, blk, 0, c->stream>>>(x, y, s.len, s.rows, s.chunks(), seg, gate);
+  c->count();
+  c->check_launch();
+}
+
+// ---------------------------------------------------------------------------
+// out = x*sx + coef*(old*so)  (+ segment partials of out^2)
+// ---------------------------------------------------------------------------
+__global__ void axpby_epi_kernel(const double* __restrict__ x, double* __restrict__ out,
+                                 size_t len, size_t rows, size_t chunks, EpiArgs e) {
+  if (e.gate && *e.gate == 0) return;
+  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+  double v = 0.0;
+  if (xi < len) {
+    const size_t i = row * len + xi;
+    double a = x[i];
+    if (e.sx) a = a * *e.sx;
+    v = epilogue(a, e, i);
+    out[i] = v;
+  }
+  if (e.seg) {
+    const double s = tree32(v * v);
+    if (threadIdx.x == 0) e.seg[row * chunks + blockIdx.x] = s;
+  }
+}
+
+void axpby_epi(Ctx* c, const double* x, double* out, RowShape s, const Epi& e) {
+  if (s.n() == 0) return;
+  dim3 blk(32, 8), grd((unsigned)s.chunks(), (unsigned)((s.rows + 7) / 8));
+  axpby_epi_kernel<<<grd, blk, 0, c->stream>>>(x, out, s.len, s.rows, s.chunks(), to_args(e));
+  c->count();
+  c->check_launch();
+}
+
+// ---------------------------------------------------------------------------
+// tree-32 levels: one block of 1024 threads folds 32768 consecutive inputs
+// (3 levels) into one value; inputs past J are +0 padding.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) reduce3_kernel(const double* __restrict__ in, size_t J,
+                                                       double* __restrict__ out, const int* gate) {
+  if (gate && *gate == 0) return;
+  const double r = block_reduce3(in + (size_t)blockIdx.x * 32768,
+                                 J > (size_t)blockIdx.x * 32768 ? J - (size_t)blockIdx.x * 32768 : 0);
+  if (threadIdx.x == 0) out[blockIdx.x] = r;
+}
+
+size_t reduce_scratch_size(size_t nseg) {
+  size_t tot = 0;
+  while (nseg > 32768) {
+    nseg = (nseg + 32767) / 32768;
+    tot += nseg;
+  }
+  return tot + 1;
+}
+
+void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, double* out,
+                     const int* gate) {
+  const double* cur = seg;
+  size_t J = nseg;
+  double* s = scratch;
+  while (J > 32768) {
+    const size_t K = (J + 32767) / 32768;
+    reduce3_kernel<<<(unsigned)K, 1024, 0, c->stream>>>(cur, J, s, gate);
+    c->count();
+    c->check_launch();
+    cur = s;
+    s += K;
+    J = K;
+  }
+  reduce3_kernel<<<1, 1024, 0, c->stream>>>(cur, J, out, gate);
+  c->count();
+  c->check_launch();
+}
+
+}  // namespace mlsqr_b200

@@ -1,0 +1,51 @@
+// vec.cuh -- device-side pieces shared by the operator / stencil / solver kernels.
+#pragma once
+
+#include "internal.cuh"
+
+namespace mlsqr_b200 {
+
+// POD copy of Epi passed by value to kernels
+struct EpiArgs {
+  const double* sx;
+  const double* old;
+  const double* so;
+  const double* coef;
+  double* seg;
+  const int* gate;
+};
+
+inline EpiArgs to_args(const Epi& e) { return {e.sx, e.old, e.so, e.coef, e.seg, e.gate}; }
+
+// xpby (kernels_scalar.cpp:19-21): out = a + coef * (old * so)
+__device__ __forceinline__ double epilogue(double a, const EpiArgs& e, size_t i) {
+  if (!e.old) return a;
+  double o = e.old[i];
+  if (e.so) o = o * *e.so;
+  return a + *e.coef * o;
+}
+
+// Three tree-32 levels over in[0 .. 32768) (zero padded past J); result in thread 0.
+// Requires blockDim.x == 1024.
+__device__ __forceinline__ double block_reduce3(const double* __restrict__ in, size_t J) {
+  __shared__ double wres[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double keep = 0.0;
+#pragma unroll 4
+  for (int g = 0; g < 32; ++g) {
+    const size_t k = (size_t)w * 1024 + (size_t)g * 32 + (size_t)lane;
+    double v = k < J ? in[k] : 0.0;
+    v = tree32(v);
+    v = __shfl_sync(kFull, v, 0);
+    if (lane == g) keep = v;
+  }
+  keep = tree32(keep);
+  if (lane == 0) wres[w] = keep;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) r = tree32(wres[lane]);
+  __syncthreads();
+  return r;
+}
+
+}  // namespace mlsqr_b200

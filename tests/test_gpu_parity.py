@@ -1,0 +1,368 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+The CUDA kernels implement the canonical DEVICE arithmetic order,
+which the oracle restates on the CPU (orc.device_order()).  Every comparison
+below is therefore BIT-EXACT (np.array_equal) -- far inside north_star's
+1e-9 (alpha/beta, iterate) and 1e-6 (reconstruction) tolerances, which are
+asserted as well.  The one exception is noted (PM-exp uses exp(), whose
+CUDA and glibc implementations may differ by an ulp).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_1308_6634_b200 as mb
+from pyoracle import stop as ostop
+
+pytestmark = pytest.mark.gpu
+
+TOL_AB = 1e-9   # north_star: alpha/beta sequence and iterate, relative l2
+TOL_F = 1e-6    # north_star: final reconstruction, relative l2
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return mb.default_context()
+
+
+@pytest.fixture()
+def dev(orc):
+    orc.set_device_order(True)
+    yield orc
+    orc.set_device_order(False)
+
+
+def gstop(n, **kw):
+    return mb.StoppingConfig(max_iters=n, **kw)
+
+
+def ostop_from(s: mb.StoppingConfig):
+    return ostop(s.max_iters, s.atol, s.btol, s.conlim, s.delta, s.eta, s.use_s1, s.use_s2, s.use_s3, s.use_s4)
+
+
+# ---------------------------------------------------------------------------
+# operators
+# ---------------------------------------------------------------------------
+BLUR_CASES = [
+    (1, (50,), 0.05, 3), (1, (128,), 0.03, -1), (1, (1000,), 0.01, 12),
+    (2, (40, 40), 0.05, 6), (2, (33, 21), 0.04, 4), (2, (128, 128), 2 / 128, 6),
+    (2, (96, 64), 3 / 96, 9), (2, (64, 64), 0.05, 36),
+    (3, (16, 12, 10), 0.08, 3), (3, (32, 32, 32), 2 / 32, 6), (3, (40, 24, 20), 0.05, 4),
+]
+
+
+@pytest.mark.parametrize("dims,shape,sigma,R", BLUR_CASES)
+def test_blur_bit_exact(ctx, orc, dims, shape, sigma, R):
+    taps = orc.taps(shape[0], sigma, radius=R)
+    g = mb.SeparableGaussianBlur(shape, taps=taps)
+    o = orc.blur(dims, shape, taps)
+    x = np.random.default_rng(dims * 100 + len(taps)).uniform(-1, 1, int(np.prod(shape)))
+    assert np.array_equal(g.apply(x), o.apply(x))
+    assert np.array_equal(g.apply_adjoint(x), o.adjoint(x))
+
+
+def test_blur_reference_radius_matches_reference_2d(ctx, orc, golden):
+    # the reference's own 2D blur (6 sigma radius), scalar backend, 40x40
+    g = mb.SeparableGaussianBlur((40, 40), sigma_f=0.05)
+    assert np.array_equal(g.apply(golden["scalar_blur2d_40x40_x"]), golden["scalar_blur2d_40x40_y"])
+    g1 = mb.SeparableGaussianBlur((50,), sigma_f=0.05)
+    assert np.array_equal(g1.apply(golden["scalar_conv1d_x"]), golden["scalar_conv1d_y"])
+
+
+def test_operator_dimension_errors(ctx):
+    g = mb.SeparableGaussianBlur((16, 16), sigma_f=0.1, radius=2)
+    with pytest.raises(mb.DimensionError):
+        g.apply(np.zeros(255))
+    with pytest.raises(mb.DimensionError):
+        g.apply_adjoint(np.zeros(257))
+    with pytest.raises(ValueError):
+        mb.SeparableGaussianBlur((16, 16), taps=np.ones(2 * 40 + 1))  # radius > 36
+
+
+@pytest.mark.parametrize("m,n,L", [(17, 23, 0), (40, 30, 0), (64, 512, 8), (96, 4096, 16), (8, 100000, 0)])
+def test_dense_bit_exact(ctx, dev, m, n, L):
+    rng = np.random.default_rng(m + n)
+    a = rng.uniform(-1, 1, (m, n))
+    g = mb.DenseOperator(a, sol_row_len=L)
+    o = dev.dense(a)
+    x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, m)
+    assert np.array_equal(g.apply(x), o.apply(x))
+    assert np.array_equal(g.apply_adjoint(y), o.adjoint(y))
+
+
+def test_fdot_operator_bit_exact(ctx, dev):
+    gs, gd = mb.fdot_tables(8, 4, 4, 1.0, 3)
+    g = mb.FdotOperator(8, 4, 4, tables=(gs, gd))
+    _, _, a = dev.fdot(8, 4, 4, 1.0, 3)
+    o = dev.dense(a)
+    x = np.random.default_rng(1).uniform(0, 1, 512)
+    assert np.array_equal(g.apply(x), o.apply(x))
+    y = np.random.default_rng(2).uniform(-1, 1, 16)
+    assert np.array_equal(g.apply_adjoint(y), o.adjoint(y))
+
+
+# ---------------------------------------------------------------------------
+# diffusion operator, V-cycle
+# ---------------------------------------------------------------------------
+MG_CASES = [(1, (64,), 4), (2, (32, 32), 3), (2, (48, 16), 3), (2, (128, 128), 5),
+            (3, (16, 16, 16), 3), (3, (32, 16, 8), 3), (3, (32, 32, 32), 4)]
+PENS = [("tikhonov", 1.0), ("tv", 0.5), ("pm_log", 0.3)]
+
+
+@pytest.mark.parametrize("dims,shape,levels", MG_CASES)
+@pytest.mark.parametrize("pen,T", PENS)
+def test_vcycle_bit_exact(ctx, dev, dims, shape, levels, pen, T):
+    n = int(np.prod(shape))
+    h = 1.0 / shape[0]
+    grid = dev.grid(dims, shape, h)
+    rng = np.random.default_rng(n + levels)
+    f = rng.standard_normal(n) * 0.3
+    vc = mb.VCycleMap(shape, h, levels)
+    eps = vc.update(f, mb.PenaltySpec(pen, T))
+    cx, cy, cz = dev.edge_coeffs(grid, f, pen, T)
+    oeps = 1e-8 * dev.max_diag(grid, cx, cy, cz)
+    assert eps == oeps
+    x = rng.uniform(-1, 1, n)
+    assert np.array_equal(vc.m_apply(x), dev.m_apply(grid, cx, cy, cz, eps, x))
+    om = dev.vcycle(grid, levels)
+    om.set(cx, cy, cz, eps)
+    assert np.array_equal(vc.solve(x), om.solve(x))
+
+
+def test_vcycle_explicit_coefficients_and_variants(ctx, dev):
+    shape, h = (32, 32), 1 / 32
+    grid = dev.grid(2, shape, h)
+    rng = np.random.default_rng(7)
+    f = rng.standard_normal(1024)
+    cx, cy, cz = dev.edge_coeffs(grid, f, "tv", 0.1)
+    for levels, pre, post, kc in [(1, 2, 2, 5), (2, 1, 0, 1), (3, 3, 1, 2), (4, 2, 2, 4)]:
+        vc = mb.VCycleMap(shape, h, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
+        vc.set_coefficients(cx, cy, None, 1e-3)
+        om = dev.vcycle(grid, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
+        om.set(cx, cy, cz, 1e-3)
+        x = rng.uniform(-1, 1, 1024)
+        assert np.array_equal(vc.solve(x), om.solve(x)), (levels, pre, post, kc)
+
+
+def test_vcycle_rejects_bad_hierarchy(ctx):
+    with pytest.raises(ValueError):
+        mb.VCycleMap((24, 24), 1 / 24, 5)  # 24 does not halve 4 times
+    with pytest.raises(mb.DimensionError):
+        mb.VCycleMap((1, 8), 1.0, 1)
+
+
+@pytest.mark.parametrize("dims,shape,pen,T", [(2, (64, 64), "tv", 0.01), (3, (16, 16, 16), "pm_log", 0.05),
+                                               (1, (128,), "tikhonov", 1.0)])
+def test_penalty_functional_bit_exact(ctx, dev, dims, shape, pen, T):
+    n = int(np.prod(shape))
+    f = np.random.default_rng(n).standard_normal(n)
+    h = 1.0 / shape[0]
+    v = mb.penalty_functional(f, shape, h, mb.PenaltySpec(pen, T))
+    assert v == dev.penalty_functional(dev.grid(dims, shape, h), f, pen, T)
+
+
+# ---------------------------------------------------------------------------
+# mlsqr / lsqr
+# ---------------------------------------------------------------------------
+def deblur_problem(orc, shape, sigma_px, R, seed=1, noise=0.01):
+    dims = len(shape)
+    n = int(np.prod(shape))
+    taps = orc.taps(shape[0], sigma_px / shape[0], radius=R)
+    if dims == 2:
+        f = orc.rects2d(shape[0], shape[1], 8, seed)
+    else:
+        f = orc.ellipsoids3d(*shape, 6, shape[0] / 16, shape[0] / 4, 0.2, 1.0, seed)
+    o = orc.blur(dims, shape, taps)
+    af = o.apply(f)
+    g = af + orc.gauss(seed + 100, n, noise * np.abs(af).max())
+    return taps, f, g, o
+
+
+def compare_solves(gres, ores, exact=True):
+    assert gres.iterations == ores.iterations
+    assert gres.stop_reason == ores.stop_reason
+    if exact:
+        assert np.array_equal(gres.alphas, ores.alphas)
+        assert np.array_equal(gres.betas, ores.betas)
+        assert np.array_equal(gres.solution, ores.f)
+        for a, b in zip(gres.trace, ores.trace):
+            for k in ("res_damped", "res_data", "s2_value", "anorm_est", "cond_est", "xnorm_est", "alpha", "beta"):
+                assert getattr(a, k) == b[k], k
+    assert rel(gres.alphas, ores.alphas) <= TOL_AB
+    assert rel(gres.betas, ores.betas) <= TOL_AB
+    assert rel(gres.solution, ores.f) <= TOL_AB
+
+
+@pytest.mark.parametrize("tau", [0.0, 1e-2, 1.0])
+def test_mlsqr_c1_like_bit_exact(ctx, dev, tau):
+    """C1 shape class: 2D deblur, sigma 2 px / 13 taps, Tikhonov M at f=0, V(2,2), 50 its."""
+    shape = (64, 64)
+    taps, f, g, o = deblur_problem(dev, shape, 2.0, 6)
+    h = 1 / 64
+    vc = mb.VCycleMap(shape, h, 4)
+    vc.update(np.zeros(4096), mb.PenaltySpec.tikhonov())
+    gop = mb.SeparableGaussianBlur(shape, taps=taps)
+    st = gstop(50)
+    gres = mb.mlsqr(gop, vc, g, tau, st)
+    grid = dev.grid(2, shape, h)
+    cx, cy, cz = dev.edge_coeffs(grid, np.zeros(4096), "tikhonov", 1.0)
+    om = dev.vcycle(grid, 4)
+    om.set(cx, cy, cz, 1e-8 * dev.max_diag(grid, cx, cy, cz))
+    ores = dev.mlsqr(o, om, g, tau, ostop_from(st))
+    compare_solves(gres, ores)
+
+
+def test_mlsqr_3d_bit_exact(ctx, dev):
+    shape = (32, 32, 32)
+    taps, f, g, o = deblur_problem(dev, shape, 1.5, 4, seed=3, noise=0.02)
+    h = 1 / 32
+    grid = dev.grid(3, shape, h)
+    vc = mb.VCycleMap(shape, h, 3)
+    vc.update(f, mb.PenaltySpec.perona_malik_log(0.05))
+    cx, cy, cz = dev.edge_coeffs(grid, f, "pm_log", 0.05)
+    om = dev.vcycle(grid, 3)
+    om.set(cx, cy, cz, 1e-8 * dev.max_diag(grid, cx, cy, cz))
+    st = gstop(40)
+    compare_solves(mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), vc, g, 1e-2, st),
+                   dev.mlsqr(o, om, g, 1e-2, ostop_from(st)))
+
+
+def test_lsqr_and_identity_map_bit_exact(ctx, dev):
+    shape = (48, 40)
+    taps, f, g, o = deblur_problem(dev, shape, 2.0, 6, seed=5)
+    gop = mb.SeparableGaussianBlur(shape, taps=taps)
+    for tau in (0.0, 0.1):
+        st = gstop(30)
+        compare_solves(mb.lsqr(gop, g, tau, st), dev.mlsqr(o, None, g, tau, ostop_from(st), lsqr=True))
+        compare_solves(mb.mlsqr(gop, mb.IdentityMap(gop.n_cols), g, tau, st),
+                       dev.mlsqr(o, dev.identity_map(gop.n_cols), g, tau, ostop_from(st)))
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.05])
+def test_stopping_rules_bit_exact(ctx, dev, tau):
+    shape = (32, 32)
+    taps, f, g, o = deblur_problem(dev, shape, 1.5, 4, seed=9)
+    gop = mb.SeparableGaussianBlur(shape, taps=taps)
+    delta = 0.01 * np.abs(o.apply(f)).max() * 32
+    for st in (gstop(60, use_s4=True, delta=delta, eta=1.1),
+               gstop(200, use_s1=True, use_s2=True, use_s3=True, atol=1e-6, btol=1e-6, conlim=1e6)):
+        compare_solves(mb.lsqr(gop, g, tau, st), dev.mlsqr(o, None, g, tau, ostop_from(st), lsqr=True))
+
+
+def test_dense_mlsqr_bit_exact(ctx, dev):
+    """C4 shape class (fDOT-like dense A on a 3D grid + V-cycle), reduced size."""
+    n, ns, nd = 8, 4, 4
+    gs, gd = mb.fdot_tables(n, ns, nd, 1.0, 11)
+    _, _, a = dev.fdot(n, ns, nd, 1.0, 11)
+    f = dev.ellipsoids3d(n, n, n, 3, 1.5, 2.5, 1.0, 1.0, 4)
+    o = dev.dense(a)
+    af = o.apply(f)
+    g = af + dev.gauss(5, ns * nd, 0.01 * np.abs(af).max())
+    h = 1 / n
+    grid = dev.grid(3, (n, n, n), h)
+    vc = mb.VCycleMap((n, n, n), h, 2)
+    vc.update(np.zeros(n ** 3), mb.PenaltySpec.tv_smoothed(0.01))
+    cx, cy, cz = dev.edge_coeffs(grid, np.zeros(n ** 3), "tv", 0.01)
+    om = dev.vcycle(grid, 2)
+    om.set(cx, cy, cz, 1e-8 * dev.max_diag(grid, cx, cy, cz))
+    st = gstop(12)
+    compare_solves(mb.mlsqr(mb.FdotOperator(n, ns, nd, tables=(gs, gd)), vc, g, 1e-3, st),
+                   dev.mlsqr(o, om, g, 1e-3, ostop_from(st)))
+
+
+def test_breakdown_and_errors(ctx, golden):
+    a = mb.DenseOperator(golden["signflip_A"])
+    flip = mb.CallbackMap(8, lambda p: -p)
+    with pytest.raises(mb.BreakdownError) as ei:
+        mb.mlsqr(a, flip, golden["signflip_g"], 0.0, gstop(5))
+    assert ei.value.iteration == 0  # reference: BreakdownError(0) (test_krylov.cpp:131-145)
+    with pytest.raises(mb.DimensionError):
+        mb.mlsqr(a, mb.IdentityMap(9), golden["signflip_g"], 0.0, gstop(5))
+    with pytest.raises(mb.DimensionError):
+        mb.mlsqr(a, mb.IdentityMap(8), np.ones(11), 0.0, gstop(5))
+    with pytest.raises(ValueError):
+        mb.mlsqr(a, mb.IdentityMap(8), golden["signflip_g"], -1.0, gstop(5))
+    # zero data: clean breakdown, zero iterate (test_krylov.cpp:49-56)
+    r = mb.lsqr(mb.IdentityOperator(4), np.zeros(4), 0.0, gstop(5))
+    assert r.iterations == 0 and r.stop_reason == "breakdown" and not r.solution.any()
+    # identity converges in one iteration (test_krylov.cpp:29-37)
+    g = np.random.default_rng(1).uniform(-1, 1, 7)
+    r = mb.lsqr(mb.IdentityOperator(7), g, 0.0, gstop(10))
+    assert r.iterations == 1 and r.stop_reason == "breakdown" and rel(r.solution, g) <= 1e-14
+
+
+def test_callback_map_matches_device_identity(ctx, dev):
+    shape = (32, 32)
+    taps, f, g, o = deblur_problem(dev, shape, 2.0, 6)
+    gop = mb.SeparableGaussianBlur(shape, taps=taps)
+    st = gstop(15)
+    a = mb.mlsqr(gop, mb.CallbackMap(1024, lambda p: p.copy()), g, 0.0, st)
+    b = mb.mlsqr(gop, mb.IdentityMap(1024), g, 0.0, st)
+    assert np.array_equal(a.alphas, b.alphas) and np.array_equal(a.solution, b.solution)
+
+
+# ---------------------------------------------------------------------------
+# nonlinear (lagged diffusivity) outer loop
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,shape,pen,T,tau,K,I,levels", [
+    (2, (32, 32), "tv", 0.01, 5e-3, 3, 10, 3),
+    (2, (64, 64), "tikhonov", 1.0, 1e-2, 1, 50, 4),
+    (3, (16, 16, 16), "pm_log", 0.05, 1e-2, 3, 8, 3),
+])
+def test_nonlinear_fixed_count_bit_exact(ctx, dev, dims, shape, pen, T, tau, K, I, levels):
+    taps, f, g, o = deblur_problem(dev, shape, 2.0 if dims == 2 else 1.5, 6 if dims == 2 else 4, seed=K + I)
+    h = 1.0 / shape[0]
+    cfg = mb.OuterConfig(tau=tau, penalty=mb.PenaltySpec(pen, T), inner_stop=gstop(I), inner_cap=I,
+                         rel_decrease_threshold=0.0, max_outer=K, mg_levels=levels)
+    rep = mb.solve_nonlinear(mb.SeparableGaussianBlur(shape, taps=taps), g, shape, h, cfg)
+    orep = dev.nonlinear(o, g, dev.grid(dims, shape, h), tau=tau, pen=pen, T=T, inner_stop=ostop(I),
+                         inner_cap=I, max_outer=K, threshold=0.0, levels=levels)
+    assert len(rep.steps) == orep["n_steps"] == K
+    for s, os_, oa, ob in zip(rep.steps, orep["steps"], orep["alphas"], orep["betas"]):
+        assert s.eps_used == os_["eps_used"]
+        assert s.penalty_value == os_["penalty_value"]
+        assert s.final_residual == os_["final_residual"]
+        assert np.array_equal(s.alphas[:I], oa[:I]) and np.array_equal(s.betas[:I + 1], ob[:I + 1])
+    assert np.array_equal(rep.solution, orep["f"])
+    assert rel(rep.solution, orep["f"]) <= TOL_F
+
+
+def test_nonlinear_stagnation_rule_bit_exact(ctx, dev, golden):
+    """1D deconvolution with S4 inner stop and the 0.15 stagnation rule (test_outer.cpp:66-93)."""
+    n = 128
+    g = golden["scalar_deconv_g"]
+    taps = dev.taps(n, 0.03)
+    delta = 0.01 / np.sqrt(1 / n)
+    st = mb.StoppingConfig.discrepancy(delta, 1.1, 1000)
+    cfg = mb.OuterConfig(tau=0.0, penalty=mb.PenaltySpec.perona_malik_log(0.005), inner_stop=st,
+                         inner_cap=20, rel_decrease_threshold=0.15, max_outer=25, mg_levels=5)
+    rep = mb.solve_nonlinear(mb.SeparableGaussianBlur((n,), taps=taps), g, (n,), 1 / n, cfg)
+    orep = dev.nonlinear(dev.blur(1, (n,), taps), g, dev.grid(1, (n,), 1 / n), tau=0.0, pen="pm_log",
+                         T=0.005, inner_stop=ostop_from(st), inner_cap=20, max_outer=25, threshold=0.15,
+                         levels=5)
+    assert rep.stop_reason == orep["stop_reason"] and rep.triggered_at == orep["triggered_at"]
+    assert [s.inner_iterations for s in rep.steps] == [s["inner_iterations"] for s in orep["steps"]]
+    assert np.array_equal(rep.solution, orep["f"])
+    # reference semantics: every inner run is capped or discrepancy-stopped
+    for s in rep.steps:
+        assert s.inner_iterations <= 20
+        if s.inner_iterations < 20:
+            assert s.inner_stop == "S4" and s.final_residual <= 1.1 * delta * (1 + 1e-12)
+
+
+def test_device_resident_torch_tensors(ctx, dev):
+    torch = pytest.importorskip("torch")
+    shape = (64, 64)
+    taps, f, g, o = deblur_problem(dev, shape, 2.0, 6)
+    gop = mb.SeparableGaussianBlur(shape, taps=taps)
+    gd = torch.from_numpy(g).cuda()
+    r1 = mb.lsqr(gop, gd, 0.01, gstop(20))
+    r2 = mb.lsqr(gop, g, 0.01, gstop(20))
+    assert np.array_equal(r1.solution.cpu().numpy(), r2.solution)
+    assert np.array_equal(gop.apply(gd).cpu().numpy(), gop.apply(g))
