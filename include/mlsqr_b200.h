@@ -198,6 +198,16 @@ int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, si
                           mlsqr_outer_step* steps, int* n_steps, int* stop_reason,
                           int* triggered_at, double* alphas, double* betas, int ptr_kind);
 
+/* Stateful driver for one outer step at a time (outer.cpp:59-87): D update at f_prev,
+ * hierarchy + auto shift, mlsqr from zero (capped at inner_cap), R(f^k).  Keeps the
+ * V-cycle and the Krylov workspace resident between steps (bench / serving loop). */
+typedef struct mlsqr_outer mlsqr_outer;
+int mlsqr_outer_create(mlsqr_op* op, int dims, size_t nx, size_t ny, size_t nz, double h,
+                       const mlsqr_outer_cfg* cfg, mlsqr_outer** out);
+int mlsqr_outer_advance(mlsqr_outer* o, const double* g, const double* f_prev, double* f_out,
+                     mlsqr_outer_step* step, int ptr_kind);
+int mlsqr_outer_destroy(mlsqr_outer* o);
+
 /* ---- R(f) (diffusion.cpp:89-101) on the device --------------------------- */
 int mlsqr_penalty_functional(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
                              double h, const double* f, int ptr_kind, int pen_kind, double T,

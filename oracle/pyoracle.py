@@ -447,6 +447,8 @@ class Reference:
         L.ref_solve_nonlinear.argtypes = [C.POINTER(RefOp), dp, C.c_int, C.c_size_t, C.c_size_t,
                                           C.c_double, C.POINTER(RefOuterCfg), dp, C.POINTER(OuterStep),
                                           C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), dp]
+        L.ref_mlsqr_timed.argtypes = [C.POINTER(RefOp), C.POINTER(RefMap), dp, C.c_double,
+                                      C.POINTER(Stop), C.c_int, dp, dp, C.POINTER(SolveInfo)]
         L.ref_select_backend.argtypes = [C.c_int]
         L.ref_kernel_backend.restype = C.c_char_p
         self._keep = []
@@ -559,6 +561,18 @@ class Reference:
                         be[:info.n_betas].copy(), _trace_list(tr, info.iterations), status,
                         info.breakdown_iteration,
                         snap.reshape(k, cols)[:info.iterations] if snapshots else None)
+
+    def mlsqr_timed(self, od, md, g, tau, iters, warm, cols):
+        """Reference mlsqr for warm+iters iterations; returns (seconds of the last
+        `iters` iterations, iterations done, f)."""
+        f = np.zeros(cols)
+        secs = C.c_double()
+        info = SolveInfo()
+        st = stop(warm + iters)
+        status = self.lib.ref_mlsqr_timed(C.byref(od), C.byref(md), _ptr(np.ascontiguousarray(g)), tau,
+                                          C.byref(st), warm, _ptr(f), C.byref(secs), C.byref(info))
+        assert status == 0, status
+        return secs.value, info.iterations, f
 
     def solve_nonlinear(self, od, g, dims, shape, h, *, tau, pen, T, inner_stop, inner_cap,
                         threshold, max_outer, spd_mode=0, k_inner=30, epsilon=-1.0, keep=False):

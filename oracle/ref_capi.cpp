@@ -8,6 +8,7 @@
 // restated 3D blur and V-cycle for the CPU baseline, or the CUDA product's
 // C-ABI operators in "parity mode"), and (3) time the reference on the GPU
 // box's host for bench.py --impl reference.
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -84,12 +85,20 @@ typedef struct {
 
 namespace {
 
+// timing hook for the CPU baseline: steady_clock stamp at the mark-th forward apply
+// (the forward apply happens once per mlsqr iteration and never in its init,
+// krylov.cpp:389), so [stamp, end) covers exactly the iterations after the mark.
+thread_local long g_apply_calls = 0;
+thread_local long g_apply_mark = -1;
+thread_local std::chrono::steady_clock::time_point g_mark_time;
+
 class CallbackOperator final : public LinearOperator {
  public:
   CallbackOperator(const ref_op_desc& d) : LinearOperator({d.rows, d.cols}), d_(d) {}
 
  private:
   void do_apply(std::span<const double> x, std::span<double> y) const override {
+    if (++g_apply_calls == g_apply_mark) g_mark_time = std::chrono::steady_clock::now();
     if (d_.apply(d_.ctx, x.data(), y.data()) != 0) throw std::runtime_error("callback apply failed");
   }
   void do_apply_adjoint(std::span<const double> y, std::span<double> x) const override {
@@ -331,6 +340,30 @@ int ref_mlsqr(const ref_op_desc* od, const ref_map_desc* md, const double* g, do
         const auto r = mlsqr::mlsqr(*op, mh.get(), std::span<const double>(g, op->n_rows()),
                                     tau, make_stop(stop), opts);
         export_result(r, op->n_cols(), f, trace, alphas, betas, snapshots, info);
+      },
+      info);
+}
+
+// The reference's own mlsqr, timed: seconds spent in iterations warm+1 .. max_iters
+// (init and the first `warm` iterations excluded).  Single thread, like the reference.
+int ref_mlsqr_timed(const ref_op_desc* od, const ref_map_desc* md, const double* g, double tau,
+                    const ref_stop* stop, int warm, double* f, double* seconds,
+                    ref_solve_info* info) {
+  if (info) std::memset(info, 0, sizeof(*info));
+  return guarded(
+      [&] {
+        auto op = make_op(od);
+        MapHolder mh = make_map(md);
+        g_apply_calls = 0;
+        g_apply_mark = warm + 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto r = mlsqr::mlsqr(*op, mh.get(), std::span<const double>(g, op->n_rows()), tau,
+                                    make_stop(stop), SolveOptions{});
+        const auto t1 = std::chrono::steady_clock::now();
+        const auto start = g_apply_calls >= g_apply_mark ? g_mark_time : t0;
+        *seconds = std::chrono::duration<double>(t1 - start).count();
+        g_apply_mark = -1;
+        export_result(r, op->n_cols(), f, nullptr, nullptr, nullptr, nullptr, info);
       },
       info);
 }

@@ -143,6 +143,11 @@ SIGNATURES = {
                                         C.c_size_t, C.c_double, C.POINTER(_OuterCfg), C.c_void_p,
                                         C.POINTER(_OuterStep), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                         C.POINTER(C.c_int), dp, dp, C.c_int]),
+    "mlsqr_outer_create": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
+                                     C.c_double, C.POINTER(_OuterCfg), C.POINTER(C.c_void_p)]),
+    "mlsqr_outer_advance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.POINTER(_OuterStep), C.c_int]),
+    "mlsqr_outer_destroy": (C.c_int, [C.c_void_p]),
     "mlsqr_penalty_functional": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
                                            C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_double, dp]),
     "mlsqr_taps": (C.c_int, [C.c_size_t, C.c_double, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
@@ -688,6 +693,39 @@ def solve_nonlinear(a: LinearOperator, g, grid_shape, h: float, cfg: OuterConfig
         out.append(OuterStep(s.k, s.penalty_value, s.inner_iterations, s.final_residual,
                              STOP_NAMES[s.inner_stop], s.eps_used, al[i].copy(), be[i].copy()))
     return OuterReport(f, out, "stagnation" if sr.value == 0 else "max_outer", trig.value)
+
+
+class OuterSolver:
+    """One lagged-diffusivity outer step per call (outer.cpp:59-87) with the V-cycle
+    hierarchy and Krylov workspace kept resident: step(g, f_prev, f_out)."""
+
+    def __init__(self, a: LinearOperator, grid_shape, h: float, cfg: OuterConfig):
+        cfg.penalty.validate()
+        shape = tuple(int(s) for s in grid_shape)
+        nx, ny, nz = (list(shape) + [1, 1])[:3]
+        self._cfg = cfg._c()
+        hh = C.c_void_p()
+        _check(lib().mlsqr_outer_create(a.h, len(shape), nx, ny, nz, h, C.byref(self._cfg), C.byref(hh)))
+        self.h, self.op = hh, a
+
+    def step(self, g, f_prev, f_out) -> OuterStep:
+        gp, gn, kind, k1 = _vec_in(g)
+        pp, pn, kind2, k2 = _vec_in(f_prev)
+        op_, on, kind3, k3 = _vec_in(f_out)
+        assert kind == kind2 == kind3, "g, f_prev, f_out must all be host or all device"
+        if kind == HOST:  # the C-ABI writes f_out in place
+            op_ = C.c_void_p(f_out.ctypes.data)
+        s = _OuterStep()
+        _check(lib().mlsqr_outer_advance(self.h, gp, pp, op_, C.byref(s), kind))
+        return OuterStep(s.k, s.penalty_value, s.inner_iterations, s.final_residual,
+                         STOP_NAMES[s.inner_stop], s.eps_used, np.zeros(0), np.zeros(0))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().mlsqr_outer_destroy(self.h)
+        except Exception:
+            pass
 
 
 def penalty_functional(f, grid_shape, h: float, penalty: PenaltySpec, ctx: Optional[Context] = None) -> float:

@@ -439,6 +439,49 @@ int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, si
   });
 }
 
+}  // extern "C"
+
+struct mlsqr_outer {
+  std::unique_ptr<OuterSolver> impl;
+  int k = 0;
+};
+
+extern "C" {
+
+int mlsqr_outer_create(mlsqr_op* op, int dims, size_t nx, size_t ny, size_t nz, double h,
+                       const mlsqr_outer_cfg* cfg, mlsqr_outer** out) {
+  return guard([&] {
+    require(op && cfg && out, MLSQR_EINVAL, "outer_create: null argument");
+    set_device(op->impl->ctx);
+    auto* o = new mlsqr_outer();
+    try {
+      o->impl.reset(new OuterSolver(op->impl, dims, nx, ny, nz, h, *cfg));
+    } catch (...) {
+      delete o;
+      throw;
+    }
+    *out = o;
+  });
+}
+
+int mlsqr_outer_advance(mlsqr_outer* o, const double* g, const double* f_prev, double* f_out,
+                     mlsqr_outer_step* step, int kind) {
+  return guard([&] {
+    Op* op = o->impl->op;
+    Ctx* c = op->ctx;
+    set_device(c);
+    In gin(c, g, op->rows, kind);
+    In fin(c, f_prev, op->cols, kind);
+    Out fout(c, f_out, op->cols, kind);
+    o->impl->step(gin.d, fin.d, fout.d, step, ++o->k);
+    fout.finish();
+  });
+}
+
+int mlsqr_outer_destroy(mlsqr_outer* o) {
+  return guard([&] { delete o; });
+}
+
 int mlsqr_penalty_functional(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz, double h,
                              const double* f, int kind, int pen_kind, double T, double* value) {
   return guard([&] {

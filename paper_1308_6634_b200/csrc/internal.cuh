@@ -162,6 +162,8 @@ class Pc {
   // `shape` (the operator's solution space); gate as in Epi
   virtual void solve(const double* p, double* v, double* seg, const int* gate, RowShape shape) = 0;
   virtual bool host_callback() const { return false; }
+  // row length the map's reduction partials are laid out with (0: follows the caller)
+  virtual size_t row_len() const { return 0; }
 };
 
 struct Ctx {
@@ -314,6 +316,30 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
                 mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true);
 void validate_stop(const mlsqr_stop& s);
+// stateful outer step (outer.cu)
+class OuterSolver {
+ public:
+  OuterSolver(Op* o, int dims, size_t nx, size_t ny, size_t nz, double h, const mlsqr_outer_cfg& cfg);
+  ~OuterSolver();
+  OuterSolver(const OuterSolver&) = delete;
+  OuterSolver& operator=(const OuterSolver&) = delete;
+  void step(const double* g, const double* f_prev, double* f_out, mlsqr_outer_step* st, int k);
+  Op* op;
+  mlsqr_solve_info last_info{};
+  std::vector<double> al_, be_;
+
+ private:
+  int dims_;
+  size_t nx_, ny_, nz_;
+  double h_;
+  mlsqr_outer_cfg cfg_;
+  mlsqr_stop inner_{};
+  VCycle* vc_ = nullptr;
+  Workspace* ws_ = nullptr;
+  DevBuf<double> pseg_, pscr_, pval_;
+  std::vector<mlsqr_iter_rec> trace_;
+};
+
 // solve_nonlinear (outer.cu)
 void nonlinear_solve(Op* o, const double* g_dev, int dims, size_t nx, size_t ny, size_t nz,
                      double h, const mlsqr_outer_cfg& cfg, double* f_dev, mlsqr_outer_step* steps,

@@ -478,6 +478,9 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
   validate_stop(stop);
   require(tau >= 0.0, MLSQR_EINVAL, "tau must be nonnegative");
   if (pc) require(pc->n == op->cols, MLSQR_EDIM, "preconditioner dimension does not match operator columns");
+  if (pc && pc->row_len())
+    require(pc->row_len() == op->sol_shape.len, MLSQR_EDIM,
+            "operator solution-space rows (sol_row_len) must match the V-cycle grid x extent");
   std::unique_ptr<Workspace> own;
   Workspace* ws = ws_in;
   if (!ws || ws->rows != op->rows || ws->cols != op->cols || ws->max_iters < stop.max_iters) {
@@ -503,6 +506,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
     cudaGraph_t gr = nullptr;
     cudaGraphExec_t ge = nullptr;
     MLSQR_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const uint64_t before = c->launches;
     try {
       r.iteration(g_dev);
     } catch (...) {
@@ -512,6 +516,8 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
     }
     MLSQR_CUDA(cudaStreamEndCapture(c->stream, &gr));
     MLSQR_CUDA(cudaGraphInstantiate(&ge, gr, 0));
+    // every replay launches the captured kernels (gated ones exit at once)
+    c->launches += (c->launches - before) * (uint64_t)(stop.max_iters - 1);
     for (int i = 0; i < stop.max_iters; ++i) MLSQR_CUDA(cudaGraphLaunch(ge, c->stream));
     MLSQR_CUDA(cudaStreamSynchronize(c->stream));
     cudaGraphExecDestroy(ge);

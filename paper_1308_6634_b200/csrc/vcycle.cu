@@ -371,6 +371,8 @@ class VCycle final : public Pc {
     ctx->check_launch();
   }
 
+  size_t row_len() const override { return (size_t)lv_[0].nx; }
+
   void solve(const double* p, double* v, double* seg, const int* gate, RowShape) override {
     TimedRegion tr(ctx, MLSQR_TCLASS_MG);
     level(0, p, v, seg, gate);

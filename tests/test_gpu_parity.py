@@ -261,7 +261,7 @@ def test_dense_mlsqr_bit_exact(ctx, dev):
     gs, gd = mb.fdot_tables(n, ns, nd, 1.0, 11)
     _, _, a = dev.fdot(n, ns, nd, 1.0, 11)
     f = dev.ellipsoids3d(n, n, n, 3, 1.5, 2.5, 1.0, 1.0, 4)
-    o = dev.dense(a)
+    o = dev.dense(a).set_row_lengths(ns * nd, n)  # solution vectors are n^3 grids (rows of n)
     af = o.apply(f)
     g = af + dev.gauss(5, ns * nd, 0.01 * np.abs(af).max())
     h = 1 / n
