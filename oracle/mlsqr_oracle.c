@@ -294,20 +294,33 @@ size_t orc_linop_rows(const orc_linop* op) { return op->rows; }
 size_t orc_linop_cols(const orc_linop* op) { return op->cols; }
 
 /* GaussianConvolution1D::convolve (linop.cpp:115-121): zero extension, ascending dot. */
-static void conv_line(const double* taps, int R, size_t n, const double* x, size_t xs, double* y,
-                      size_t ys) {
+static void conv_line_f(const double* taps, int R, size_t n, const double* x, size_t xs, double* y,
+                        size_t ys, int use_fma) {
   for (size_t i = 0; i < n; ++i) {
     const size_t lo = i >= (size_t)R ? i - (size_t)R : 0;
     const size_t hi = (i + (size_t)R < n - 1) ? i + (size_t)R : n - 1;
     const double* t = taps + ((size_t)R + lo - i);
     double acc = 0.0;
-    for (size_t j = lo; j <= hi; ++j) acc += t[j - lo] * x[j * xs];
+    if (use_fma) {
+      for (size_t j = lo; j <= hi; ++j) acc = fma(t[j - lo], x[j * xs], acc);
+    } else {
+      for (size_t j = lo; j <= hi; ++j) acc += t[j - lo] * x[j * xs];
+    }
     y[i * ys] = acc;
   }
 }
 
+/* DEVICE order for 3D blurs (no reference implementation exists): every tap sum is an
+ * fma chain in ascending source index; 1D/2D keep the reference's mul+add order. */
+static int g_conv_fma = 0;
+static void conv_line(const double* taps, int R, size_t n, const double* x, size_t xs, double* y,
+                      size_t ys) {
+  conv_line_f(taps, R, n, x, xs, y, ys, g_conv_fma);
+}
+
 /* SeparableGaussianBlur2D::blur (linop.cpp:151-162): x rows, then y columns, then (3D) z. */
 static void blur_apply(const orc_linop* op, const double* in, double* out) {
+  g_conv_fma = g_device && op->dims == 3;
   const size_t nx = op->nx, ny = op->ny, nz = op->nz;
   const size_t nxy = nx * ny;
   for (size_t z = 0; z < nz; ++z)

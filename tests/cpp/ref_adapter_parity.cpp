@@ -1,0 +1,98 @@
+// tests/cpp/ref_adapter_parity.cpp -- "parity mode" of the drop-in boundary.
+//
+// The UNMODIFIED reference mlsqr() (compiled from /root/reference/proj/src
+// into oracle/_ref) drives the B200 blur through the C++ adapter
+// mlsqr_b200::GpuLinearOperator (include/mlsqr_b200.hpp), with the
+// reference's own envelope-Cholesky SpdSolver as M^{-1}.  With the
+// reference's scalar BLAS-1 backend selected, the result must equal the
+// all-CPU reference run bit for bit (the GPU blur sums each output in the
+// reference's order).  Also checks the exception contract across the
+// boundary and gpu_mlsqr() (throughput mode) against the reference loop.
+//
+// Built by `make -C oracle adapter` into oracle/_ref/ref_adapter_parity;
+// run by tests/test_gpu_reference_adapter.py on the GPU box.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "mlsqr/diffusion.hpp"
+#include "mlsqr/kernels.hpp"
+#include "mlsqr/krylov.hpp"
+#include "mlsqr/linop.hpp"
+#include "mlsqr/problems.hpp"
+#include "mlsqr/spdsolve.hpp"
+#include "mlsqr_b200.hpp"
+
+using namespace mlsqr;
+
+static int failures = 0;
+#define EXPECT(c)                                                  \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      ++failures;                                                  \
+    }                                                              \
+  } while (0)
+
+int main() {
+  kernels::select(kernels::Backend::scalar);
+  mlsqr_b200::Context ctx(0);
+
+  // 2D deblur 48x48 with the reference operator's own taps (6 sigma radius)
+  const std::size_t nx = 48;
+  const double sigma = 0.04;
+  const auto bundle = make_deblur2d(nx, nx, sigma, 0.01, Phantom2D::default_phantom(), 17);
+  const auto& cpu_op = *bundle.op;
+  GaussianConvolution1D k1(nx, sigma, 1.0);
+  auto gpu_op = mlsqr_b200::GpuLinearOperator::blur(ctx, 2, nx, nx, 1, k1.taps());
+
+  // operator parity
+  const auto y_cpu = cpu_op.apply(bundle.f_true);
+  const auto y_gpu = gpu_op.apply(bundle.f_true);
+  EXPECT(y_cpu == y_gpu);
+
+  // reference mlsqr with the reference's Cholesky M^-1 at the truth
+  SparseSpd m = assemble_m(bundle.grid, bundle.f_true, PenaltySpec::tv_smoothed(0.05), 0.0);
+  m = m.with_shift(1.0);
+  const SpdSolver chol = SpdSolver::factorize(m);
+  const auto stop = StoppingConfig::max_iterations(25);
+  const auto r_cpu = mlsqr::mlsqr(cpu_op, chol, bundle.g, 1e-2, stop);
+  const auto r_gpu = mlsqr::mlsqr(gpu_op, chol, bundle.g, 1e-2, stop);
+  EXPECT(r_cpu.solution == r_gpu.solution);
+  EXPECT(r_cpu.bidiag.alphas == r_gpu.bidiag.alphas);
+  EXPECT(r_cpu.bidiag.betas == r_gpu.bidiag.betas);
+
+  // exception contract across the C-ABI (linop.cpp:15-20 -> DimensionError)
+  bool threw = false;
+  try {
+    std::vector<double> bad(nx * nx - 1), out(nx * nx);
+    gpu_op.apply(bad, out);
+  } catch (const DimensionError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+
+  // throughput mode: device-resident mlsqr with the B200 V-cycle vs the reference loop
+  // driving the same V-cycle through the SpdMap adapter (host round trips per call)
+  auto vc = mlsqr_b200::GpuSpdMap::vcycle(ctx, 2, nx, nx, 1, 1.0 / nx, 3);
+  vc.update(bundle.f_true, MLSQR_PEN_TV, 0.05);
+  const auto r_dev = mlsqr_b200::gpu_mlsqr(gpu_op, vc, bundle.g, 1e-2, stop);
+  const auto r_mix = mlsqr::mlsqr(gpu_op, vc, bundle.g, 1e-2, stop);
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < r_dev.solution.size(); ++i) {
+    num += (r_dev.solution[i] - r_mix.solution[i]) * (r_dev.solution[i] - r_mix.solution[i]);
+    den += r_mix.solution[i] * r_mix.solution[i];
+  }
+  const double relf = std::sqrt(num / den);
+  double worst_a = 0.0;
+  for (std::size_t i = 0; i < r_dev.bidiag.alphas.size(); ++i)
+    worst_a = std::fmax(worst_a, std::fabs(r_dev.bidiag.alphas[i] - r_mix.bidiag.alphas[i]) / r_mix.bidiag.alphas[i]);
+  std::printf("device-resident vs reference loop (V-cycle M^-1): rel f %.3e, max rel alpha %.3e\n", relf, worst_a);
+  EXPECT(r_dev.iterations == r_mix.iterations);
+  // canonical tree reductions vs the reference's sequential dots: rounding-level
+  EXPECT(worst_a < 1e-9);
+  EXPECT(relf < 1e-6);
+
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
