@@ -39,18 +39,18 @@ void check_len(size_t got, size_t want, const char* what) {
 
 void set_device(Ctx* c) { MLSQR_CUDA(cudaSetDevice(c->device)); }
 
-// stage a host or device input as a device pointer
+// stage a host or device input as a device pointer (host data goes through the
+// context's grow-only staging buffers: every HOST call completes before returning)
 struct In {
   const double* d = nullptr;
-  DevBuf<double> own;
   In(Ctx* c, const double* p, size_t n, int kind) {
     if (kind == MLSQR_DEVICE || n == 0) {
       d = p;
       return;
     }
-    own.alloc(n);
-    MLSQR_CUDA(cudaMemcpyAsync(own.p, p, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-    d = own.p;
+    double* s = static_cast<double*>(c->staging(sizeof(double) * n));
+    MLSQR_CUDA(cudaMemcpyAsync(s, p, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    d = s;
   }
 };
 
@@ -59,15 +59,13 @@ struct Out {
   double* host = nullptr;
   size_t n;
   Ctx* c;
-  DevBuf<double> own;
   Out(Ctx* cc, double* p, size_t nn, int kind) : n(nn), c(cc) {
     if (kind == MLSQR_DEVICE) {
       d = p;
       return;
     }
     host = p;
-    own.alloc(n);
-    d = own.p;
+    d = static_cast<double*>(c->staging(sizeof(double) * n));
   }
   void finish() {
     if (host) MLSQR_CUDA(cudaMemcpyAsync(host, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -148,6 +146,8 @@ int mlsqr_ctx_destroy(mlsqr_ctx* ctx) {
   return guard([&] {
     if (!ctx) return;
     cudaSetDevice(ctx->impl.device);
+    cudaStreamSynchronize(ctx->impl.stream);
+    ctx->impl.release_staging();
     if (ctx->impl.own_stream) cudaStreamDestroy(ctx->impl.stream);
     delete ctx;
   });

@@ -176,6 +176,27 @@ struct Ctx {
   uint64_t t_n[MLSQR_TCLASS_COUNT] = {};
   int sm_count = 148;
   size_t l2_bytes = 0;
+  // grow-only staging buffers for HOST-pointer calls (no cudaMalloc/cudaFree per call)
+  void* stage[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t stage_bytes[4] = {0, 0, 0, 0};
+  int stage_next = 0;
+  void* staging(size_t bytes) {
+    const int k = stage_next;
+    stage_next = (stage_next + 1) & 3;
+    if (stage_bytes[k] < bytes) {
+      if (stage[k]) cudaFree(stage[k]);
+      stage[k] = nullptr;
+      stage_bytes[k] = 0;
+      if (cudaMalloc(&stage[k], bytes) != cudaSuccess)
+        throw Error(MLSQR_ECUDA, "staging allocation failed");
+      stage_bytes[k] = bytes;
+    }
+    return stage[k];
+  }
+  void release_staging() {
+    for (int k = 0; k < 4; ++k)
+      if (stage[k]) cudaFree(stage[k]);
+  }
 
   void count(int k = 1) { launches += (uint64_t)k; }
   void check_launch() {
