@@ -145,35 +145,45 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   const int n = valid ? 8 : 0;  // src-size 0 -> zero fill
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int R>
 struct B3 {
-  static constexpr int NT = 2 * R + 1;    // taps
-  static constexpr int TX = 32, TY = 32;  // output tile
-  static constexpr int W = TX + 2 * R;    // input x extent
-  static constexpr int H = TY + 2 * R;    // input y extent (rows)
-  static constexpr int HP = H | 1;        // odd pitch: conflict-free x-major access
-  static constexpr int XP = 33;           // x-pass buffer pitch
-  static constexpr int NBUF = 3;          // cp.async ring depth
-  static constexpr int IN_DOUBLES = W * HP;
+  static constexpr int NT = 2 * R + 1;        // taps
+  static constexpr int TX = 32, TY = 32;      // output tile (x, y)
+  static constexpr int THREADS = 512;         // 32 x 16: two y-columns per thread
+  static constexpr int W = TX + 2 * R;        // input x extent (even)
+  static constexpr int H = TY + 2 * R;        // input y extent (rows)
+  static constexpr int P = ((W / 2) % 2) ? W : W + 2;  // row pitch: P/2 odd -> LDS.128 conflict-free
+  static constexpr int XK = 4;                // x outputs per x-pass task
+  static constexpr int XG = TX / XK;          // x groups per row
+  static constexpr int XP = 34;               // x-pass buffer pitch (XP/2 odd)
+  static constexpr int NBUF = 3;              // cp.async ring depth
+  static constexpr int IN_DOUBLES = H * P;
   static constexpr int XS_DOUBLES = H * XP;
   static constexpr int OLD_DOUBLES = TX * TY;
   static constexpr size_t SMEM = sizeof(double) * ((size_t)NBUF * IN_DOUBLES + XS_DOUBLES + (size_t)NBUF * OLD_DOUBLES);
 };
 
-template <int R>
-__global__ void __launch_bounds__(256, 1) blur3d_fused(const double* __restrict__ in,
+// VEC: 16-byte copies (needs R even and nx even so every pair is aligned and either fully
+// inside or fully outside the domain); otherwise 8-byte copies.
+template <int R, bool VEC>
+__global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict__ in,
                                                        double* __restrict__ out, int nx, int ny,
                                                        int nz, int zchunk, Taps taps, EpiArgs e) {
   using C = B3<R>;
   if (e.gate && *e.gate == 0) return;
-  extern __shared__ double sm[];
-  double* inT = sm;                                 // [NBUF][W][HP]   x-major input planes
-  double* xs = sm + C::NBUF * C::IN_DOUBLES;        // [H][XP]         x-pass results
-  double* olds = xs + C::XS_DOUBLES;                // [NBUF][TY][TX]  old-vector planes
+  extern __shared__ __align__(16) double sm[];
+  double* tin = sm;                              // [NBUF][H][P]   input planes (row-major)
+  double* xs = sm + C::NBUF * C::IN_DOUBLES;     // [H][XP]        x-pass results
+  double* olds = xs + C::XS_DOUBLES;             // [NBUF][TY][TX] old-vector planes
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * C::TX, y0 = blockIdx.y * C::TY;
   const int z0 = blockIdx.z * zchunk;
@@ -182,35 +192,55 @@ __global__ void __launch_bounds__(256, 1) blur3d_fused(const double* __restrict_
   const size_t nxy = (size_t)nx * ny;
   const double sx = e.sx ? *e.sx : 1.0;
 
-  // issue the async copies of input plane zz (and the old plane for output zz - R)
   auto issue = [&](int zz) {
+    const int slot = (zz - zlo) % C::NBUF;
     if (zz >= 0 && zz < nz && zz <= zhi) {
-      double* dst = inT + (size_t)(((zz - zlo) % C::NBUF + C::NBUF) % C::NBUF) * C::IN_DOUBLES;
+      double* dst = tin + (size_t)slot * C::IN_DOUBLES;
       const double* src = in + (size_t)zz * nxy;
-      for (int k = tid; k < C::H * C::W; k += 256) {
-        const int ly = k / C::W, lx = k - ly * C::W;
-        const int gx = x0 + lx - R, gy = y0 + ly - R;
-        const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-        cp_async8(dst + lx * C::HP + ly, ok ? src + (size_t)gy * nx + gx : in, ok);
+      if (VEC) {
+        constexpr int PAIRS = C::W / 2;
+        for (int k = tid; k < C::H * PAIRS; k += C::THREADS) {
+          const int ly = k / PAIRS, q = k - ly * PAIRS;
+          const int gx = x0 - R + 2 * q, gy = y0 + ly - R;
+          const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+          cp_async16(dst + ly * C::P + 2 * q, ok ? src + (size_t)gy * nx + gx : in, ok);
+        }
+      } else {
+        for (int k = tid; k < C::H * C::W; k += C::THREADS) {
+          const int ly = k / C::W, lx = k - ly * C::W;
+          const int gx = x0 + lx - R, gy = y0 + ly - R;
+          const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+          cp_async8(dst + ly * C::P + lx, ok ? src + (size_t)gy * nx + gx : in, ok);
+        }
       }
     }
     const int zo = zz - R;
     if (e.old && zo >= z0 && zo < z1) {
-      double* dst = olds + (size_t)(((zz - zlo) % C::NBUF + C::NBUF) % C::NBUF) * C::OLD_DOUBLES;
-      for (int k = tid; k < C::TX * C::TY; k += 256) {
-        const int ly = k >> 5, lx = k & 31;
-        const int gx = x0 + lx, gy = y0 + ly;
-        const bool ok = gx < nx && gy < ny;
-        cp_async8(dst + k, ok ? e.old + (size_t)zo * nxy + (size_t)gy * nx + gx : in, ok);
+      double* dst = olds + (size_t)slot * C::OLD_DOUBLES;
+      const double* src = e.old + (size_t)zo * nxy;
+      if (VEC) {
+        for (int k = tid; k < C::TX * C::TY / 2; k += C::THREADS) {
+          const int ly = k >> 4, q = k & 15;
+          const int gx = x0 + 2 * q, gy = y0 + ly;
+          const bool ok = gx < nx && gy < ny;
+          cp_async16(dst + ly * 32 + 2 * q, ok ? src + (size_t)gy * nx + gx : in, ok);
+        }
+      } else {
+        for (int k = tid; k < C::TX * C::TY; k += C::THREADS) {
+          const int ly = k >> 5, lx = k & 31;
+          const int gx = x0 + lx, gy = y0 + ly;
+          const bool ok = gx < nx && gy < ny;
+          cp_async8(dst + k, ok ? src + (size_t)gy * nx + gx : in, ok);
+        }
       }
     }
     cp_async_commit();
   };
 
-  const int tx = tid & 31, ty = tid >> 5;  // y-pass / z-pass / epilogue: 4 y-columns per thread
-  double ring[4][C::NT];
+  const int tx = tid & 31, ty = tid >> 5;  // y / z pass + epilogue: y = 2ty, 2ty + 1
+  double ring[2][C::NT];
 #pragma unroll
-  for (int o = 0; o < 4; ++o)
+  for (int o = 0; o < 2; ++o)
 #pragma unroll
     for (int k = 0; k < C::NT; ++k) ring[o][k] = 0.0;
 
@@ -219,6 +249,9 @@ __global__ void __launch_bounds__(256, 1) blur3d_fused(const double* __restrict_
   const double so = e.so ? *e.so : 1.0;
   const double coef = e.old ? *e.coef : 0.0;
   const size_t chunks = (size_t)(nx + 31) / 32;
+  // x-pass task of this thread: row xr (lanes = consecutive rows), x group xg
+  const int xr = tid % C::H, xg = tid / C::H;
+  const bool xtask = tid < C::H * C::XG;
 
   for (int base = zlo; base <= zhi; base += C::NT) {
 #pragma unroll
@@ -228,58 +261,60 @@ __global__ void __launch_bounds__(256, 1) blur3d_fused(const double* __restrict_
         issue(zz + 2);
         cp_async_wait<2>();
         __syncthreads();
-        const int slot = ((zz - zlo) % C::NBUF + C::NBUF) % C::NBUF;
-        double yv[4] = {0.0, 0.0, 0.0, 0.0};
-        const bool inside = zz >= 0 && zz < nz;
-        if (inside) {
-          // x pass: tasks (row r, 8-wide x group g), reading x-major -> conflict-free
-          const double* pin = inT + (size_t)slot * C::IN_DOUBLES;
-          if (tid < 4 * C::H) {
-            const int r = tid % C::H, g = tid / C::H;
-            double w[8 + 2 * R];
+        const int slot = (zz - zlo) % C::NBUF;
+        double yv0 = 0.0, yv1 = 0.0;
+        if (zz >= 0 && zz < nz) {
+          if (xtask) {
+            const double* row = tin + (size_t)slot * C::IN_DOUBLES + xr * C::P + C::XK * xg;
+            double w[C::XK + 2 * R];
 #pragma unroll
-            for (int j = 0; j < 8 + 2 * R; ++j) {
-              w[j] = pin[(8 * g + j) * C::HP + r];
-              if (e.sx) w[j] = w[j] * sx;
+            for (int j = 0; j < (C::XK + 2 * R) / 2; ++j) {
+              const double2 p = *reinterpret_cast<const double2*>(row + 2 * j);
+              w[2 * j] = p.x;
+              w[2 * j + 1] = p.y;
             }
+            if (e.sx) {
 #pragma unroll
-            for (int o = 0; o < 8; ++o) {
-              double acc = 0.0;
-#pragma unroll
-              for (int k = 0; k < C::NT; ++k) acc = fma(taps.t[k], w[o + k], acc);
-              xs[r * C::XP + 8 * g + o] = acc;
+              for (int j = 0; j < C::XK + 2 * R; ++j) w[j] = w[j] * sx;
             }
+            double acc[C::XK];
+#pragma unroll
+            for (int o = 0; o < C::XK; ++o) {
+              acc[o] = 0.0;
+#pragma unroll
+              for (int k = 0; k < C::NT; ++k) acc[o] = fma(taps.t[k], w[o + k], acc[o]);
+            }
+            double* xw = xs + xr * C::XP + C::XK * xg;
+            *reinterpret_cast<double2*>(xw) = make_double2(acc[0], acc[1]);
+            *reinterpret_cast<double2*>(xw + 2) = make_double2(acc[2], acc[3]);
           }
           __syncthreads();
-          // y pass: 4 consecutive y outputs per thread from a 4 + 2R register window
-          double c[4 + 2 * R];
+          double c[2 + 2 * R];
 #pragma unroll
-          for (int j = 0; j < 4 + 2 * R; ++j) c[j] = xs[(4 * ty + j) * C::XP + tx];
+          for (int j = 0; j < 2 + 2 * R; ++j) c[j] = xs[(2 * ty + j) * C::XP + tx];
 #pragma unroll
-          for (int o = 0; o < 4; ++o) {
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < C::NT; ++k) acc = fma(taps.t[k], c[o + k], acc);
-            yv[o] = acc;
+          for (int k = 0; k < C::NT; ++k) {
+            yv0 = fma(taps.t[k], c[k], yv0);
+            yv1 = fma(taps.t[k], c[k + 1], yv1);
           }
         }
-#pragma unroll
-        for (int o = 0; o < 4; ++o) ring[o][u] = yv[o];
-        // z pass for output plane zo = zz - R: planes zo-R .. zz sit in slots u+1+k (mod NT)
+        ring[0][u] = yv0;
+        ring[1][u] = yv1;
+        // z pass for output plane zo = zz - R: planes zo-R .. zz sit in ring slots u+1+k (mod NT)
         const int zo = zz - R;
         if (zo >= z0 && zo < z1) {
           const double* po = olds + (size_t)slot * C::OLD_DOUBLES;
 #pragma unroll
-          for (int o = 0; o < 4; ++o) {
+          for (int o = 0; o < 2; ++o) {
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < C::NT; ++k) acc = fma(taps.t[k], ring[o][(u + 1 + k) % C::NT], acc);
-            const int gy = y0 + 4 * ty + o, gx = x0 + tx;
+            const int gy = y0 + 2 * ty + o, gx = x0 + tx;
             double v = 0.0;
             if (gx < nx && gy < ny) {
               v = acc;
               if (e.old) {
-                double ov = po[(4 * ty + o) * 32 + tx];
+                double ov = po[(2 * ty + o) * 32 + tx];
                 if (e.so) ov = ov * so;
                 v = acc + coef * ov;
               }
@@ -297,19 +332,26 @@ __global__ void __launch_bounds__(256, 1) blur3d_fused(const double* __restrict_
   }
 }
 
-template <int R>
-static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
-                      const EpiArgs& a) {
+template <int R, bool VEC>
+static void launch_b3v(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
+                       const EpiArgs& a) {
   using C = B3<R>;
   static bool attr = false;
   if (!attr) {
-    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_fused<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_fused<R, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
   const int zchunk = nz >= 256 ? 64 : (nz >= 64 ? 32 : nz);
   dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
-  blur3d_fused<R><<<grd, 256, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, t, a);
+  blur3d_fused<R, VEC><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, t, a);
   c->count();
+}
+
+template <int R>
+static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
+                      const EpiArgs& a) {
+  if (R % 2 == 0 && nx % 2 == 0) launch_b3v<R, true>(c, in, out, nx, ny, nz, t, a);
+  else launch_b3v<R, false>(c, in, out, nx, ny, nz, t, a);
 }
 
 // radius dispatch for the fused kernel (BASELINE taps: 9 (R=4) and 13 (R=6))

@@ -392,6 +392,8 @@ struct Runner {
   }
 
   void init(const double* g) {
+    // f = 0 before anything can stop the solve (SolveResult::solution.assign(n, 0.0))
+    MLSQR_CUDA(cudaMemsetAsync(ws->f.p, 0, sizeof(double) * ws->cols, c->stream));
     init_state_kernel<<<1, 1, 0, c->stream>>>(st, tau);
     // u_s = g, |g|^2
     Epi e;

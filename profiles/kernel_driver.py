@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--iters", type=int, default=4)
+    ap.add_argument("--time", action="store_true")
     a = ap.parse_args()
     import torch
     import paper_1308_6634_b200 as mb
@@ -37,6 +38,24 @@ def main():
     g = op.apply(x)
     mb.mlsqr(op, vc, g, 5e-3, mb.StoppingConfig.max_iterations(a.iters))
     torch.cuda.synchronize()
+    if a.time:
+        def timed(fn, reps=10):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps
+        nb = 8.0 * n ** 3
+        t_blur = timed(lambda: op.apply(x, y))
+        t_vc = timed(lambda: vc.solve(y, v))
+        print(f"blur apply: {t_blur:.3f} ms  ({2 * nb / t_blur / 1e6:.0f} GB/s on 2 vectors)")
+        print(f"V-cycle   : {t_vc:.3f} ms")
+        it_ms = timed(lambda: mb.mlsqr(op, vc, g, 5e-3, mb.StoppingConfig.max_iterations(20)), reps=2) / 20
+        print(f"mlsqr iteration (20-it solve incl. init): {it_ms:.3f} ms")
     print("driver done", float(v[0]))
 
 
