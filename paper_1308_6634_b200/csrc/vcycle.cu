@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restr
   }
 }
 
+#include "stencil_zm.cuh"
+
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
 __global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
   const int rows = L.ny * L.nz;
@@ -390,8 +392,19 @@ class VCycle final : public Pc {
       cny = lv_[(size_t)l + 1].ny;
     }
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
-    sweep_kernel<MODE><<<row_grid(L.nx, L.ny * L.nz), dim3(32, 8), 0, ctx->stream>>>(
-        view(l), x, xc, cnx, cny, b, out, omega_, seg, gate);
+    const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
+    dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
+    sweep_zm_kernel<MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out,
+                                                               omega_, seg, gate, zc);
+    ctx->count();
+  }
+
+  void restrict_to(int l, const double* x, const double* b, const int* gate) {
+    const Level& L = lv_[(size_t)l];
+    Level& C = lv_[(size_t)l + 1];
+    const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
+    dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
+    restrict_zm_kernel<<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
     ctx->count();
   }
 
@@ -415,9 +428,7 @@ class VCycle final : public Pc {
     }
     if (coarsest) return cur;
     Level& C = lv_[(size_t)l + 1];
-    restrict_kernel<<<row_grid(C.nx, C.ny * C.nz), dim3(32, 8), 0, ctx->stream>>>(
-        view(l), cur, b, C.nx, C.ny, C.nz, C.b.p, gate);
-    ctx->count();
+    restrict_to(l, cur, b, gate);
     const double* xc = level(l + 1, C.b.p, nullptr, nullptr, gate);
     if (nu_post_ == 0) {
       double* dst = out ? out : bufs[nb];
