@@ -191,6 +191,28 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
   const int zlo = z0 - R, zhi = z1 + R - 1;  // planes touched
   const size_t nxy = (size_t)nx * ny;
   const double sx = e.sx ? *e.sx : 1.0;
+  // the taps are bitwise symmetric (t[k] == t[2R-k], checked on the host): only R+1
+  // distinct constants feed the DFMAs, which keeps them in uniform registers
+#define TAP(k) taps.t[(k) <= R ? (k) : 2 * R - (k)]
+
+  // per-thread 16-byte copy descriptors of the input tile, computed once (VEC path)
+  constexpr int PAIRS = C::W / 2;
+  constexpr int NPAIR = C::H * PAIRS;
+  constexpr int PER = (NPAIR + C::THREADS - 1) / C::THREADS;
+  int c_soff[PER];
+  long c_goff[PER];
+  bool c_ok[PER];
+  if (VEC) {
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int k = tid + m * C::THREADS;
+      const int ly = k / PAIRS, q = k - ly * PAIRS;
+      const int gx = x0 - R + 2 * q, gy = y0 + ly - R;
+      c_ok[m] = k < NPAIR && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+      c_soff[m] = k < NPAIR ? ly * C::P + 2 * q : -1;
+      c_goff[m] = c_ok[m] ? (long)gy * nx + gx : 0;
+    }
+  }
 
   auto issue = [&](int zz) {
     const int slot = (zz - zlo) % C::NBUF;
@@ -198,13 +220,9 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
       double* dst = tin + (size_t)slot * C::IN_DOUBLES;
       const double* src = in + (size_t)zz * nxy;
       if (VEC) {
-        constexpr int PAIRS = C::W / 2;
-        for (int k = tid; k < C::H * PAIRS; k += C::THREADS) {
-          const int ly = k / PAIRS, q = k - ly * PAIRS;
-          const int gx = x0 - R + 2 * q, gy = y0 + ly - R;
-          const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-          cp_async16(dst + ly * C::P + 2 * q, ok ? src + (size_t)gy * nx + gx : in, ok);
-        }
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+          if (c_soff[m] >= 0) cp_async16(dst + c_soff[m], c_ok[m] ? src + c_goff[m] : in, c_ok[m]);
       } else {
         for (int k = tid; k < C::H * C::W; k += C::THREADS) {
           const int ly = k / C::W, lx = k - ly * C::W;
@@ -282,7 +300,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
             for (int o = 0; o < C::XK; ++o) {
               acc[o] = 0.0;
 #pragma unroll
-              for (int k = 0; k < C::NT; ++k) acc[o] = fma(taps.t[k], w[o + k], acc[o]);
+              for (int k = 0; k < C::NT; ++k) acc[o] = fma(TAP(k), w[o + k], acc[o]);
             }
             double* xw = xs + xr * C::XP + C::XK * xg;
             *reinterpret_cast<double2*>(xw) = make_double2(acc[0], acc[1]);
@@ -294,8 +312,8 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
           for (int j = 0; j < 2 + 2 * R; ++j) c[j] = xs[(2 * ty + j) * C::XP + tx];
 #pragma unroll
           for (int k = 0; k < C::NT; ++k) {
-            yv0 = fma(taps.t[k], c[k], yv0);
-            yv1 = fma(taps.t[k], c[k + 1], yv1);
+            yv0 = fma(TAP(k), c[k], yv0);
+            yv1 = fma(TAP(k), c[k + 1], yv1);
           }
         }
         ring[0][u] = yv0;
@@ -308,7 +326,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
           for (int o = 0; o < 2; ++o) {
             double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < C::NT; ++k) acc = fma(taps.t[k], ring[o][(u + 1 + k) % C::NT], acc);
+            for (int k = 0; k < C::NT; ++k) acc = fma(TAP(k), ring[o][(u + 1 + k) % C::NT], acc);
             const int gy = y0 + 2 * ty + o, gx = x0 + tx;
             double v = 0.0;
             if (gx < nx && gy < ny) {
@@ -330,6 +348,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
       }
     }
   }
+#undef TAP
 }
 
 template <int R, bool VEC>
@@ -391,8 +410,10 @@ class BlurOp final : public Op {
     }
     // warm the fused 3D kernel's attribute outside any graph capture
     if (dims_ == 3) {
-      fused_ = (radius == 1 || radius == 2 || radius == 3 || radius == 4 || radius == 5 || radius == 6 ||
-                radius == 8 || radius == 12);
+      bool sym = true;  // the fused kernel reads t[min(k, 2R-k)]
+      for (int k = 0; k <= radius; ++k) sym = sym && taps_.t[k] == taps_.t[2 * radius - k];
+      fused_ = sym && (radius == 1 || radius == 2 || radius == 3 || radius == 4 || radius == 5 ||
+                       radius == 6 || radius == 8 || radius == 12);
       if (!fused_) tmp_.alloc(rows);
       else {
         EpiArgs none{};
