@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restr
 }
 
 #include "stencil_zm.cuh"
+#include "sweep2.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
 __global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
@@ -293,6 +294,9 @@ class VCycle final : public Pc {
     }
     eps_.alloc((size_t)levels);
     maxd_.alloc(1);
+    MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(false)));
+    MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(true)));
+    if (const char* e = getenv("MLSQR_NO_FUSED_SWEEPS")) fuse_enabled_ = e[0] == '0';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
   }
 
@@ -417,12 +421,20 @@ class VCycle final : public Pc {
     int nb = 0;
     // pre-smoothing (or the whole coarse solve) from zero
     const double* cur = nullptr;
+    const bool fuse = fused_ok(l);
     for (int s = 0; s < pre; ++s) {
-      const bool last_here = coarsest && s + 1 == pre;
+      const bool pair = fuse && s == 0 && pre >= 2;  // sweeps 1 + 2 in one kernel
+      const bool last_here = coarsest && s + (pair ? 2 : 1) == pre;
       double* dst = (last_here && out) ? out : bufs[nb];
       double* sg = (last_here && out) ? seg : nullptr;
-      if (s == 0) sweep<kFirst>(l, nullptr, nullptr, b, dst, sg, gate);
-      else sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
+      if (pair) {
+        sweep2<false>(l, nullptr, nullptr, b, dst, sg, gate);
+        ++s;
+      } else if (s == 0) {
+        sweep<kFirst>(l, nullptr, nullptr, b, dst, sg, gate);
+      } else {
+        sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
+      }
       cur = dst;
       if (dst == bufs[nb]) nb ^= 1;
     }
@@ -436,16 +448,49 @@ class VCycle final : public Pc {
       return dst;
     }
     for (int s = 0; s < nu_post_; ++s) {
-      const bool last = s + 1 == nu_post_;
+      const bool pair = fuse && s == 0 && nu_post_ >= 2;  // prolong + sweeps 3 + 4 in one kernel
+      const bool last = s + (pair ? 2 : 1) == nu_post_;
       double* dst = (last && out) ? out : bufs[nb];
       double* sg = (last && out) ? seg : nullptr;
-      if (s == 0) sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
-      else sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
+      if (pair) {
+        sweep2<true>(l, cur, xc, b, dst, sg, gate);
+        ++s;
+      } else if (s == 0) {
+        sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
+      } else {
+        sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
+      }
       cur = dst;
       if (dst == bufs[nb]) nb ^= 1;
     }
     return cur;
   }
+
+  // fused two-sweep kernel: 16-byte plane copies need an even x extent
+  bool fused_ok(int l) const { return fuse_enabled_ && lv_[(size_t)l].nx % 2 == 0; }
+
+  template <bool PROLONG>
+  void sweep2(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
+              const int* gate) {
+    const Level& L = lv_[(size_t)l];
+    int cnx = 0, cny = 0;
+    if (l + 1 < (int)lv_.size()) {
+      cnx = lv_[(size_t)l + 1].nx;
+      cny = lv_[(size_t)l + 1].ny;
+    }
+    TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    const int zc = sweep2_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
+    dim3 grd((unsigned)((L.nx + s2::TX - 1) / s2::TX), (unsigned)((L.ny + s2::TY - 1) / s2::TY),
+             (unsigned)((L.nz + zc - 1) / zc));
+    sweep2_kernel<PROLONG><<<grd, s2::THREADS, sweep2_smem(PROLONG), ctx->stream>>>(
+        view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
+    ctx->count();
+  }
+
+ public:
+  bool fuse_enabled_ = true;
+
+ private:
 
   int dims_;
   double h_;

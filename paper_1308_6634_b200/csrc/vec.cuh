@@ -25,6 +25,21 @@ __device__ __forceinline__ double epilogue(double a, const EpiArgs& e, size_t i)
   return a + *e.coef * o;
 }
 
+// cp.async (LDGSTS) helpers: src-size 0 zero-fills the destination
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // Three tree-32 levels over in[0 .. 32768) (zero padded past J); result in thread 0.
 // Requires blockDim.x == 1024.
 __device__ __forceinline__ double block_reduce3(const double* __restrict__ in, size_t J) {
