@@ -1,26 +1,30 @@
-// stencil_zm.cuh -- z-marching versions of the V-cycle stencil kernels
-// (included by vcycle.cu).  A (32 x 8) block owns a column tile and walks a
-// chunk of z planes: the z neighbours of the iterate and cz[z-1] stay in
-// registers, the streams of plane z+1 (x, b, cx, cy, cz) are loaded one plane
-// ahead, and only the in-plane neighbours go through L1.  Arithmetic is
-// operation-for-operation the one of m_row / diag_at (CSR ascending column
-// order, sparse.cpp:65-74), so results are bit-identical to the per-voxel
-// kernels and to the oracle.
+// stencil_zm.cuh -- z-marching V-cycle stencil kernels (included by vcycle.cu).
+//
+// A (32 x 8) block owns a column tile and walks a chunk of z planes: the z
+// neighbours of the iterate and cz[z-1] stay in registers and the streams of
+// plane z+1 (x, b, cx, cy, cz) are loaded one plane ahead.
+//
+// Branch-free rows: every internal V-cycle array (iterates, coefficients,
+// coarse corrections) is allocated with a zero guard zone of one plane (+64)
+// on both sides, and every missing edge has an exactly-zero coefficient.  So
+// all 7 terms of a row are added unconditionally, in the CSR ascending-column
+// order of m_row / diag_at (sparse.cpp:65-74): a skipped term of the reference
+// becomes acc + (+-0), which is acc exactly (the accumulators start at +0 and
+// can never reach -0).  Results are bit-identical to the oracle.
 
 // iterate value at fine index j (plus the prolongated coarse correction)
-template <bool PROLONG>
+template <int D, bool PROLONG>
 __device__ __forceinline__ double xv_zm(const double* __restrict__ x, const double* __restrict__ xc,
-                                        int cnx, int cny, bool has_y, bool has_z, int xx, int yy, int zz,
-                                        size_t j) {
+                                        int cnx, int cny, int xx, int yy, int zz, long j) {
   double v = x[j];
   if (PROLONG) {
-    const int Z = has_z ? zz / 2 : 0, Y = has_y ? yy / 2 : 0;
-    v = v + xc[((size_t)Z * cny + Y) * cnx + xx / 2];
+    const int Z = D >= 3 ? zz / 2 : 0, Y = D >= 2 ? yy / 2 : 0;
+    v = v + xc[((long)Z * cny + Y) * cnx + xx / 2];
   }
   return v;
 }
 
-template <int MODE>
+template <int D, int MODE>
 __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __restrict__ x,
                                                        const double* __restrict__ xc, int cnx, int cny,
                                                        const double* __restrict__ b,
@@ -33,84 +37,87 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
   if (yy >= L.ny) return;  // whole warp (one row)
   const int z0 = blockIdx.z * zc;
   const int z1 = min(L.nz, z0 + zc);
-  const bool hy = L.cy != nullptr, hz = L.cz != nullptr;
-  const size_t nxy = (size_t)L.nx * L.ny;
-  const bool ix = xx < L.nx;
+  const int nx = L.nx;
+  const long nxy = (long)nx * L.ny;
+  const bool ix = xx < nx;
   const double eps = *L.eps;
-  const size_t chunks = (size_t)(L.nx + 31) / 32;
-  size_t i = ((size_t)z0 * L.ny + yy) * L.nx + xx;
-  // rolling registers: iterate at z-1, z, z+1 and cz at z-1
-  double xm = 0.0, xcur = 0.0, czm = 0.0;
-  // streams of the current plane
-  double bc = 0.0, cxc = 0.0, cyc = 0.0, czc = 0.0, xn = 0.0;
-  if (ix) {
-    if (MODE != kFirst) {
-      xcur = xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy, z0, i);
-      if (hz && z0 > 0) xm = xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy, z0 - 1, i - nxy);
-      if (hz && z0 + 1 < L.nz) xn = xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy, z0 + 1, i + nxy);
+  const double* __restrict__ cx = L.cx;
+  const double* __restrict__ cy = L.cy;
+  const double* __restrict__ cz = L.cz;
+  const long chunks = (nx + 31) / 32;
+  long i = ((long)z0 * L.ny + yy) * nx + (ix ? xx : nx - 1);
+  double xm = 0.0, xcur = 0.0, xn = 0.0, czm = 0.0;
+  double bc = b[i], cxc = cx[i], cyc = 0.0, czc = 0.0;
+  if (D >= 2) cyc = cy[i];
+  if (D >= 3) {
+    czc = cz[i];
+    czm = cz[i - nxy];  // guard zone below plane 0
+  }
+  if (MODE != kFirst) {
+    xcur = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z0, i);
+    if (D >= 3) {
+      xm = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z0 - 1, i - nxy);
+      xn = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z0 + 1, i + nxy);
     }
-    if (hz && z0 > 0) czm = L.cz[i - nxy];
-    bc = b[i];
-    cxc = L.cx[i];
-    if (hy) cyc = L.cy[i];
-    if (hz) czc = L.cz[i];
   }
   for (int z = z0; z < z1; ++z, i += nxy) {
-    // prefetch the streams of plane z+1 (one plane of HBM loads in flight)
+    // prefetch the streams of plane z+1 (plane-uniform condition)
     double bn = 0.0, cxn = 0.0, cyn = 0.0, czn = 0.0, xnn = 0.0;
-    if (ix && z + 1 < z1) {
+    if (z + 1 < z1) {
       bn = b[i + nxy];
-      cxn = L.cx[i + nxy];
-      if (hy) cyn = L.cy[i + nxy];
-      if (hz) czn = L.cz[i + nxy];
-      if (MODE != kFirst && MODE != kProlongOnly && hz && z + 2 < L.nz)
-        xnn = xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy, z + 2, i + 2 * nxy);
+      cxn = cx[i + nxy];
+      if (D >= 2) cyn = cy[i + nxy];
+      if (D >= 3) czn = cz[i + nxy];
+      if (D >= 3 && MODE != kFirst && MODE != kProlongOnly)
+        xnn = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z + 2, i + 2 * nxy);  // guard covers z+2 = nz
     }
-    double v = 0.0;
-    if (ix) {
-      if (MODE == kProlongOnly) {
-        v = xcur;
-      } else {
-        // diag_at order: x-, x+, y-, y+, z-, z+ ; then + eps
-        double d = 0.0;
-        if (xx > 0) d = d + L.cx[i - 1];
-        if (xx + 1 < L.nx) d = d + cxc;
-        if (hy) {
-          if (yy > 0) d = d + L.cy[i - L.nx];
-          if (yy + 1 < L.ny) d = d + cyc;
-        }
-        if (hz) {
-          if (z > 0) d = d + czm;
-          if (z + 1 < L.nz) d = d + czc;
-        }
-        d = d + eps;
-        if (MODE == kFirst) {
-          const double mx = 0.0;
-          v = 0.0 + (omega * (bc - mx)) / d;
-        } else {
-          // m_row order: z-, y-, x-, diag, x+, y+, z+
-          double acc = 0.0;
-          if (hz && z > 0) acc = acc + -czm * xm;
-          if (hy && yy > 0) acc = acc + -L.cy[i - L.nx] * xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy - 1, z, i - L.nx);
-          if (xx > 0) acc = acc + -L.cx[i - 1] * xv_zm<P>(x, xc, cnx, cny, hy, hz, xx - 1, yy, z, i - 1);
-          acc = acc + d * xcur;
-          if (xx + 1 < L.nx) acc = acc + -cxc * xv_zm<P>(x, xc, cnx, cny, hy, hz, xx + 1, yy, z, i + 1);
-          if (hy && yy + 1 < L.ny) acc = acc + -cyc * xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy + 1, z, i + L.nx);
-          if (hz && z + 1 < L.nz) acc = acc + -czc * xn;
-          v = xcur + (omega * (bc - acc)) / d;
-        }
+    double v;
+    if (MODE == kProlongOnly) {
+      v = xcur;
+    } else {
+      // diag_at order: x-, x+, y-, y+, z-, z+ ; then + eps
+      const double cxm = cx[i - 1];
+      double d = 0.0;
+      d = d + cxm;
+      d = d + cxc;
+      double cym = 0.0;
+      if (D >= 2) {
+        cym = cy[i - nx];
+        d = d + cym;
+        d = d + cyc;
       }
-      out[i] = v;
+      if (D >= 3) {
+        d = d + czm;
+        d = d + czc;
+      }
+      d = d + eps;
+      if (MODE == kFirst) {
+        const double mx = 0.0;
+        v = 0.0 + (omega * (bc - mx)) / d;
+      } else {
+        // m_row order: z-, y-, x-, diag, x+, y+, z+
+        double acc = 0.0;
+        if (D >= 3) acc = acc + -czm * xm;
+        if (D >= 2) acc = acc + -cym * xv_zm<D, P>(x, xc, cnx, cny, xx, yy - 1, z, i - nx);
+        acc = acc + -cxm * xv_zm<D, P>(x, xc, cnx, cny, xx - 1, yy, z, i - 1);
+        acc = acc + d * xcur;
+        acc = acc + -cxc * xv_zm<D, P>(x, xc, cnx, cny, xx + 1, yy, z, i + 1);
+        if (D >= 2) acc = acc + -cyc * xv_zm<D, P>(x, xc, cnx, cny, xx, yy + 1, z, i + nx);
+        if (D >= 3) acc = acc + -czc * xn;
+        v = xcur + (omega * (bc - acc)) / d;
+      }
     }
+    if (ix) out[i] = v;
+    else v = 0.0;
     if (seg) {
-      const double s = tree32(v * bc);
-      if (threadIdx.x == 0) seg[((size_t)z * L.ny + yy) * chunks + blockIdx.x] = s;
+      const double s = tree32(v * (ix ? bc : 0.0));
+      if (threadIdx.x == 0) seg[((long)z * L.ny + yy) * chunks + blockIdx.x] = s;
     }
     // roll
     czm = czc;
     xm = xcur;
     if (MODE == kProlongOnly) {
-      if (ix && z + 1 < z1) xcur = xv_zm<P>(x, xc, cnx, cny, hy, hz, xx, yy, z + 1, i + nxy);
+      if (z + 1 < z1) xcur = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z + 1, i + nxy);
     } else {
       xcur = xn;
       xn = xnn;
@@ -126,6 +133,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
 // dz, dy, dx nested) of r = b - M x.  Fine threads compute r; the (even x, even y) thread
 // of each 2 x 2 patch accumulates the children in the canonical order across the two
 // fine planes of the coarse cell.
+template <int D>
 __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* __restrict__ x,
                                                           const double* __restrict__ b, int cnx, int cny,
                                                           double* __restrict__ bcoarse, const int* gate,
@@ -137,78 +145,79 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
   const int yy = blockIdx.y * 8 + ty;
   const int z0 = blockIdx.z * zc;
   const int z1 = min(L.nz, z0 + zc);
-  const bool hy = L.cy != nullptr, hz = L.cz != nullptr;
-  const size_t nxy = (size_t)L.nx * L.ny;
-  const bool ok = xx < L.nx && yy < L.ny;
+  const int nx = L.nx;
+  const long nxy = (long)nx * L.ny;
+  const bool ok = xx < nx && yy < L.ny;
   const double eps = *L.eps;
-  size_t i = ((size_t)z0 * L.ny + (yy < L.ny ? yy : 0)) * L.nx + (xx < L.nx ? xx : 0);
-  double xm = 0.0, xcur = 0.0, xn = 0.0, czm = 0.0;
-  double bc = 0.0, cxc = 0.0, cyc = 0.0, czc = 0.0;
-  if (ok) {
-    xcur = x[i];
-    if (hz && z0 > 0) {
-      xm = x[i - nxy];
-      czm = L.cz[i - nxy];
-    }
-    if (hz && z0 + 1 < L.nz) xn = x[i + nxy];
-    bc = b[i];
-    cxc = L.cx[i];
-    if (hy) cyc = L.cy[i];
-    if (hz) czc = L.cz[i];
+  const double* __restrict__ cx = L.cx;
+  const double* __restrict__ cy = L.cy;
+  const double* __restrict__ cz = L.cz;
+  long i = ((long)z0 * L.ny + (yy < L.ny ? yy : L.ny - 1)) * nx + (xx < nx ? xx : nx - 1);
+  double xm = 0.0, xcur = x[i], xn = 0.0, czm = 0.0;
+  double bc = b[i], cxc = cx[i], cyc = 0.0, czc = 0.0;
+  if (D >= 2) cyc = cy[i];
+  if (D >= 3) {
+    xm = x[i - nxy];
+    xn = x[i + nxy];
+    czm = cz[i - nxy];
+    czc = cz[i];
   }
-  const bool owner = ok && (tx % 2 == 0) && (!hy || ty % 2 == 0);
+  const bool owner = ok && (tx % 2 == 0) && (D < 2 || ty % 2 == 0);
   double s = 0.0;
   for (int z = z0; z < z1; ++z, i += nxy) {
     double bn = 0.0, cxn = 0.0, cyn = 0.0, czn = 0.0, xnn = 0.0;
-    if (ok && z + 1 < z1) {
+    if (z + 1 < z1) {
       bn = b[i + nxy];
-      cxn = L.cx[i + nxy];
-      if (hy) cyn = L.cy[i + nxy];
-      if (hz) czn = L.cz[i + nxy];
-      if (hz && z + 2 < L.nz) xnn = x[i + 2 * nxy];
-    }
-    double r = 0.0;
-    if (ok) {
-      double d = 0.0;
-      if (xx > 0) d = d + L.cx[i - 1];
-      if (xx + 1 < L.nx) d = d + cxc;
-      if (hy) {
-        if (yy > 0) d = d + L.cy[i - L.nx];
-        if (yy + 1 < L.ny) d = d + cyc;
+      cxn = cx[i + nxy];
+      if (D >= 2) cyn = cy[i + nxy];
+      if (D >= 3) {
+        czn = cz[i + nxy];
+        xnn = x[i + 2 * nxy];
       }
-      if (hz) {
-        if (z > 0) d = d + czm;
-        if (z + 1 < L.nz) d = d + czc;
-      }
-      d = d + eps;
-      double acc = 0.0;
-      if (hz && z > 0) acc = acc + -czm * xm;
-      if (hy && yy > 0) acc = acc + -L.cy[i - L.nx] * x[i - L.nx];
-      if (xx > 0) acc = acc + -L.cx[i - 1] * x[i - 1];
-      acc = acc + d * xcur;
-      if (xx + 1 < L.nx) acc = acc + -cxc * x[i + 1];
-      if (hy && yy + 1 < L.ny) acc = acc + -cyc * x[i + L.nx];
-      if (hz && z + 1 < L.nz) acc = acc + -czc * xn;
-      r = bc - acc;
     }
+    const double cxm = cx[i - 1];
+    double d = 0.0;
+    d = d + cxm;
+    d = d + cxc;
+    double cym = 0.0;
+    if (D >= 2) {
+      cym = cy[i - nx];
+      d = d + cym;
+      d = d + cyc;
+    }
+    if (D >= 3) {
+      d = d + czm;
+      d = d + czc;
+    }
+    d = d + eps;
+    double acc = 0.0;
+    if (D >= 3) acc = acc + -czm * xm;
+    if (D >= 2) acc = acc + -cym * x[i - nx];
+    acc = acc + -cxm * x[i - 1];
+    acc = acc + d * xcur;
+    acc = acc + -cxc * x[i + 1];
+    if (D >= 2) acc = acc + -cyc * x[i + nx];
+    if (D >= 3) acc = acc + -czc * xn;
+    const double r = ok ? bc - acc : 0.0;
     const double rx1 = __shfl_down_sync(kFull, r, 1);
-    rs[ty][tx] = r;
-    __syncthreads();
+    if (D >= 2) {
+      rs[ty][tx] = r;
+      __syncthreads();
+    }
     if (owner) {
-      const bool first = !hz || (z % 2 == 0);
-      if (first) s = 0.0;
+      if (D < 3 || (z % 2 == 0)) s = 0.0;
       s = s + r;
       s = s + rx1;
-      if (hy) {
+      if (D >= 2) {
         s = s + rs[ty + 1][tx];
         s = s + rs[ty + 1][tx + 1];
       }
-      if (!hz || (z % 2 == 1)) {
-        const int Z = hz ? z / 2 : 0, Y = hy ? yy / 2 : 0;
-        bcoarse[((size_t)Z * cny + Y) * cnx + xx / 2] = s;
+      if (D < 3 || (z % 2 == 1)) {
+        const int Z = D >= 3 ? z / 2 : 0, Y = D >= 2 ? yy / 2 : 0;
+        bcoarse[((long)Z * cny + Y) * cnx + xx / 2] = s;
       }
     }
-    __syncthreads();
+    if (D >= 2) __syncthreads();
     czm = czc;
     xm = xcur;
     xcur = xn;
@@ -218,6 +227,20 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
     cyc = cyn;
     czc = czn;
   }
+}
+
+// zero the boundary edges of explicitly supplied coefficients (an edge that leaves the
+// grid does not exist; the branch-free rows rely on its coefficient being exactly 0)
+__global__ void zero_boundary_edges_kernel(Lvl L, double* cx, double* cy, double* cz) {
+  const int rows = L.ny * L.nz;
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int xx = blockIdx.x * 32 + threadIdx.x;
+  if (row >= rows || xx >= L.nx) return;
+  const int yy = row % L.ny, zz = row / L.ny;
+  const long i = (long)row * L.nx + xx;
+  if (xx + 1 == L.nx) cx[i] = 0.0;
+  if (cy && yy + 1 == L.ny) cy[i] = 0.0;
+  if (cz && zz + 1 == L.nz) cz[i] = 0.0;
 }
 
 // z chunk: enough blocks to fill the GPU a few times; even (restriction pairs fine planes)

@@ -256,10 +256,21 @@ static inline dim3 row_grid(int nx, int rows) {
 
 class VCycle final : public Pc {
  public:
+  // device array with a zero guard zone of g elements on both sides (branch-free stencils)
+  struct GBuf {
+    DevBuf<double> raw;
+    double* p = nullptr;
+    void alloc(size_t n, size_t g, cudaStream_t s) {
+      raw.alloc(n + 2 * g);
+      MLSQR_CUDA(cudaMemsetAsync(raw.p, 0, sizeof(double) * (n + 2 * g), s));
+      p = raw.p + g;
+    }
+  };
   struct Level {
     int nx, ny, nz;
     size_t n;
-    DevBuf<double> cx, cy, cz, xa, xb, b;
+    GBuf cx, cy, cz, xa, xb;
+    DevBuf<double> b;
   };
 
   VCycle(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h, int levels, int nu_pre,
@@ -285,18 +296,22 @@ class VCycle final : public Pc {
       L.ny = (int)(dims >= 2 ? ey >> l : 1);
       L.nz = (int)(dims >= 3 ? ez >> l : 1);
       L.n = (size_t)L.nx * L.ny * L.nz;
-      L.cx.alloc(L.n);
-      if (dims >= 2) L.cy.alloc(L.n);
-      if (dims >= 3) L.cz.alloc(L.n);
-      L.xa.alloc(L.n);
-      L.xb.alloc(L.n);
+      // guard: one plane + 64 (x[i +- nxy], and the prefetch of plane z+2 = nz)
+      const size_t g = (size_t)L.nx * L.ny + 64;
+      L.cx.alloc(L.n, g, c->stream);
+      if (dims >= 2) L.cy.alloc(L.n, g, c->stream);
+      if (dims >= 3) L.cz.alloc(L.n, g, c->stream);
+      L.xa.alloc(L.n, g, c->stream);
+      L.xb.alloc(L.n, g, c->stream);
       if (l > 0) L.b.alloc(L.n);
     }
     eps_.alloc((size_t)levels);
     maxd_.alloc(1);
     MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(false)));
     MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(true)));
-    if (const char* e = getenv("MLSQR_NO_FUSED_SWEEPS")) fuse_enabled_ = e[0] == '0';
+    // the smem-tiled two-sweep kernel (sweep2.cuh) is opt-in: on B200 the branch-free
+    // z-marching sweeps are faster (see profiles/README.md)
+    if (const char* e = getenv("MLSQR_FUSED_SWEEPS")) fuse_enabled_ = e[0] == '1';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
   }
 
@@ -335,6 +350,9 @@ class VCycle final : public Pc {
     MLSQR_CUDA(cudaMemcpyAsync(L0.cx.p, cx, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
     if (dims_ >= 2) MLSQR_CUDA(cudaMemcpyAsync(L0.cy.p, cy, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
     if (dims_ >= 3) MLSQR_CUDA(cudaMemcpyAsync(L0.cz.p, cz, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    zero_boundary_edges_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(
+        view(0), L0.cx.p, dims_ >= 2 ? L0.cy.p : nullptr, dims_ >= 3 ? L0.cz.p : nullptr);
+    ctx->count();
     build(eps);
   }
 
@@ -398,8 +416,12 @@ class VCycle final : public Pc {
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
     const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
-    sweep_zm_kernel<MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out,
-                                                               omega_, seg, gate, zc);
+    if (dims_ == 3)
+      sweep_zm_kernel<3, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
+    else if (dims_ == 2)
+      sweep_zm_kernel<2, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
+    else
+      sweep_zm_kernel<1, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
     ctx->count();
   }
 
@@ -408,7 +430,12 @@ class VCycle final : public Pc {
     Level& C = lv_[(size_t)l + 1];
     const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
-    restrict_zm_kernel<<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
+    if (dims_ == 3)
+      restrict_zm_kernel<3><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
+    else if (dims_ == 2)
+      restrict_zm_kernel<2><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
+    else
+      restrict_zm_kernel<1><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
     ctx->count();
   }
 
@@ -488,7 +515,7 @@ class VCycle final : public Pc {
   }
 
  public:
-  bool fuse_enabled_ = true;
+  bool fuse_enabled_ = false;
 
  private:
 
