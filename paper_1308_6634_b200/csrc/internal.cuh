@@ -196,7 +196,12 @@ struct Ctx {
   void release_staging() {
     for (int k = 0; k < 4; ++k)
       if (stage[k]) cudaFree(stage[k]);
+    if (ws_cache) ws_free(ws_cache);
+    ws_cache = nullptr;
   }
+  // last Krylov workspace, reused by repeated solves of the same shape
+  void* ws_cache = nullptr;
+  void (*ws_free)(void*) = nullptr;
 
   void count(int k = 1) { launches += (uint64_t)k; }
   void check_launch() {

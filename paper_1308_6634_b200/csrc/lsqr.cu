@@ -483,11 +483,21 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
   if (pc && pc->row_len())
     require(pc->row_len() == op->sol_shape.len, MLSQR_EDIM,
             "operator solution-space rows (sol_row_len) must match the V-cycle grid x extent");
-  std::unique_ptr<Workspace> own;
   Workspace* ws = ws_in;
-  if (!ws || ws->rows != op->rows || ws->cols != op->cols || ws->max_iters < stop.max_iters) {
-    own.reset(workspace_new(c, op->rows, op->cols, op->data_shape, op->sol_shape, stop.max_iters));
-    ws = own.get();
+  auto fits = [&](Workspace* w) {
+    return w && w->rows == op->rows && w->cols == op->cols && w->max_iters >= stop.max_iters &&
+           w->data.len == op->data_shape.len && w->sol.len == op->sol_shape.len;
+  };
+  if (!fits(ws)) {
+    // reuse the context's cached workspace (no cudaMalloc per solve)
+    ws = static_cast<Workspace*>(c->ws_cache);
+    if (!fits(ws)) {
+      if (ws) workspace_free(ws);
+      c->ws_cache = nullptr;
+      ws = workspace_new(c, op->rows, op->cols, op->data_shape, op->sol_shape, stop.max_iters);
+      c->ws_cache = ws;
+      c->ws_free = [](void* p) { workspace_free(static_cast<Workspace*>(p)); };
+    }
   }
   if (tau != 0.0 && stop.use_s4) ws->tmp_rows.ensure(op->rows);
   // f lives in the caller's buffer
