@@ -85,6 +85,19 @@ int mlsqr_ctx_get_timing(mlsqr_ctx* ctx, int cls, double* ms, uint64_t* launches
 #define MLSQR_TCLASS_ITER 5    /* whole LSQR iteration                          */
 #define MLSQR_TCLASS_COUNT 6
 
+/* ---- z-slab decomposition (multi-GPU) ----------------------
+ * A context can own a slab of a global 3D grid: every grid object created on it with z
+ * extent nz is the plane range [z_offset, z_offset + nz) of a grid with nz_global planes.
+ * Ghost planes travel through the context's communicator: NCCL (one process per GPU) or
+ * a loopback group (P virtual ranks of one process, each on its own thread/context --
+ * used to verify sharded == unsharded bit for bit on a single GPU). */
+int mlsqr_nccl_unique_id(void* out, size_t cap, size_t* len);
+int mlsqr_ctx_set_comm_nccl(mlsqr_ctx* ctx, const void* unique_id, int rank, int size);
+int mlsqr_loop_group_create(int size, void** group);
+int mlsqr_loop_group_destroy(void* group);
+int mlsqr_ctx_set_comm_loopback(mlsqr_ctx* ctx, void* group, int rank);
+int mlsqr_ctx_set_slab(mlsqr_ctx* ctx, size_t nz_global, size_t z_offset);
+
 /* ---- LinearOperator (linop.hpp:21-47) ----------------------------------- */
 /* Separable Gaussian blur with explicit taps (SeparableGaussianBlur2D, linop.hpp:110-126,
  * GaussianConvolution1D, linop.hpp:83-105; 3D = third z pass).  taps: 2*radius+1 host

@@ -109,6 +109,12 @@ SIGNATURES = {
     "mlsqr_ctx_launch_count": (C.c_uint64, [C.c_void_p, C.c_int]),
     "mlsqr_ctx_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "mlsqr_ctx_get_timing": (C.c_int, [C.c_void_p, C.c_int, dp, C.POINTER(C.c_uint64)]),
+    "mlsqr_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "mlsqr_ctx_set_comm_nccl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "mlsqr_loop_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "mlsqr_loop_group_destroy": (C.c_int, [C.c_void_p]),
+    "mlsqr_ctx_set_comm_loopback": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "mlsqr_ctx_set_slab": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
     "mlsqr_blur_create": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, dp,
                                     C.c_int, C.POINTER(C.c_void_p)]),
     "mlsqr_dense_create": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
@@ -228,6 +234,20 @@ class Context:
     def synchronize(self) -> None:
         _check(lib().mlsqr_ctx_synchronize(self.h))
 
+    # ---- z-slab decomposition
+    def set_slab(self, nz_global: int, z_offset: int) -> None:
+        """Objects built on this context with z extent nz are planes [z_offset, z_offset+nz)
+        of a global grid with nz_global planes."""
+        _check(lib().mlsqr_ctx_set_slab(self.h, nz_global, z_offset))
+
+    def set_comm_nccl(self, unique_id: bytes, rank: int, size: int) -> None:
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().mlsqr_ctx_set_comm_nccl(self.h, buf, rank, size))
+
+    def set_comm_loopback(self, group: "LoopGroup", rank: int) -> None:
+        _check(lib().mlsqr_ctx_set_comm_loopback(self.h, group.h, rank))
+        self._group = group  # keep the group alive
+
     def launch_count(self, reset: bool = False) -> int:
         return int(lib().mlsqr_ctx_launch_count(self.h, int(reset)))
 
@@ -243,6 +263,30 @@ class Context:
         try:
             if getattr(self, "h", None):
                 lib().mlsqr_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    """An ncclUniqueId (128 bytes) for Context.set_comm_nccl; broadcast it from rank 0."""
+    buf = C.create_string_buffer(128)
+    n = C.c_size_t()
+    _check(lib().mlsqr_nccl_unique_id(buf, 128, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+class LoopGroup:
+    """P virtual ranks of one process on one GPU (each with its own Context and thread)."""
+
+    def __init__(self, size: int):
+        h = C.c_void_p()
+        _check(lib().mlsqr_loop_group_create(size, C.byref(h)))
+        self.h, self.size = h, size
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().mlsqr_loop_group_destroy(self.h)
         except Exception:
             pass
 

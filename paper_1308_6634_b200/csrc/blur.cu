@@ -164,7 +164,8 @@ struct B3 {
 template <int R, bool VEC>
 __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict__ in,
                                                        double* __restrict__ out, int nx, int ny,
-                                                       int nz, int zchunk, Taps taps, EpiArgs e) {
+                                                       int nz, int zchunk, int zoff, int nzg, Taps taps,
+                                                       EpiArgs e) {
   using C = B3<R>;
   if (e.gate && *e.gate == 0) return;
   extern __shared__ __align__(16) double sm[];
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
 
   auto issue = [&](int zz) {
     const int slot = (zz - zlo) % C::NBUF;
-    if (zz >= 0 && zz < nz && zz <= zhi) {
+    if (zz + zoff >= 0 && zz + zoff < nzg && zz <= zhi) {  // global plane inside the domain
       double* dst = tin + (size_t)slot * C::IN_DOUBLES;
       const double* src = in + (size_t)zz * nxy;
       if (VEC) {
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
         __syncthreads();
         const int slot = (zz - zlo) % C::NBUF;
         double yv0 = 0.0, yv1 = 0.0;
-        if (zz >= 0 && zz < nz) {
+        if (zz + zoff >= 0 && zz + zoff < nzg) {
           if (xtask) {
             const double* row = tin + (size_t)slot * C::IN_DOUBLES + xr * C::P + C::XK * xg;
             double w[C::XK + 2 * R];
@@ -349,7 +350,8 @@ static void launch_b3v(Ctx* c, const double* in, double* out, int nx, int ny, in
   }
   const int zchunk = nz >= 256 ? 64 : (nz >= 64 ? 32 : nz);
   dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
-  blur3d_fused<R, VEC><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, t, a);
+  const int zoff = c->sharded() ? (int)c->zoff : 0, nzg = c->sharded() ? (int)c->nzg : nz;
+  blur3d_fused<R, VEC><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, t, a);
   c->count();
 }
 
@@ -416,14 +418,36 @@ class BlurOp final : public Op {
         ctx->check_launch();
       }
     }
+    if (ctx->sharded()) {
+      // z-slab of a global grid: the fused 3D kernel reads R ghost planes per side
+      require(dims_ == 3 && fused_, MLSQR_EINVAL,
+              "z-sharded blur needs a 3D grid and a symmetric radius in {1..6, 8, 12}");
+      require(nz_ >= (size_t)radius, MLSQR_EDIM, "z slab thinner than the blur radius");
+      const size_t g = (size_t)radius * nx_ * ny_;
+      gin_.alloc(rows + 2 * g);
+      MLSQR_CUDA(cudaMemsetAsync(gin_.p, 0, sizeof(double) * gin_.n, ctx->stream));
+    }
   }
 
   void apply(const double* x, double* y, const Epi& e) override { run(x, y, e); }
   void adjoint(const double* y, double* x, const Epi& e) override { run(y, x, e); }  // A = A^T
+  int halo_planes_needed() const override { return ctx->sharded() && dims_ == 3 ? taps_.R : 0; }
+  size_t plane_size() const override { return nx_ * ny_; }
 
  private:
   void run(const double* in, double* out, const Epi& e) {
     TimedRegion tr(ctx, MLSQR_TCLASS_BLUR);
+    if (ctx->sharded()) {
+      // fill the ghost planes: in place for guarded solver vectors, else via a staging copy
+      const size_t plane = nx_ * ny_, g = (size_t)taps_.R * plane;
+      double* src = const_cast<double*>(in);
+      if (!e.in_guarded) {
+        MLSQR_CUDA(cudaMemcpyAsync(gin_.p + g, in, sizeof(double) * rows, cudaMemcpyDeviceToDevice, ctx->stream));
+        src = gin_.p + g;
+      }
+      halo_planes(ctx, src, plane, (long)nz_, taps_.R);
+      in = src;
+    }
     EpiArgs a = to_args(e);
     const size_t rows_ = ny_ * nz_;
     dim3 blk(32, 8);
@@ -453,6 +477,7 @@ class BlurOp final : public Op {
   }
 
   static constexpr int kTY = 32;
+  DevBuf<double> gin_;  // guarded staging input (z-sharded, unguarded callers)
   int dims_;
   size_t nx_, ny_, nz_;
   size_t smem_ = 0;

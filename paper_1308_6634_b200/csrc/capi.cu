@@ -148,6 +148,8 @@ int mlsqr_ctx_destroy(mlsqr_ctx* ctx) {
     cudaSetDevice(ctx->impl.device);
     cudaStreamSynchronize(ctx->impl.stream);
     ctx->impl.release_staging();
+    delete ctx->impl.comm;
+    ctx->impl.comm = nullptr;
     if (ctx->impl.own_stream) cudaStreamDestroy(ctx->impl.stream);
     delete ctx;
   });
@@ -206,6 +208,52 @@ int mlsqr_ctx_get_timing(mlsqr_ctx* ctx, int cls, double* ms, uint64_t* launches
   });
 }
 
+// ---- z-slab decomposition ----
+int mlsqr_nccl_unique_id(void* out, size_t cap, size_t* len) {
+  return guard([&] {
+    require(cap >= 128, MLSQR_EINVAL, "unique id buffer must hold 128 bytes");
+    const int n = nccl_unique_id(out);
+    if (len) *len = (size_t)n;
+  });
+}
+
+int mlsqr_ctx_set_comm_nccl(mlsqr_ctx* ctx, const void* uid, int rank, int size) {
+  return guard([&] {
+    set_device(&ctx->impl);
+    require(size >= 1 && rank >= 0 && rank < size, MLSQR_EINVAL, "bad rank / size");
+    delete ctx->impl.comm;
+    ctx->impl.comm = nullptr;
+    ctx->impl.comm = make_nccl_comm(uid, rank, size);
+  });
+}
+
+int mlsqr_loop_group_create(int size, void** group) {
+  return guard([&] {
+    require(size >= 1, MLSQR_EINVAL, "group size must be >= 1");
+    *group = make_loop_group(size);
+  });
+}
+
+int mlsqr_loop_group_destroy(void* group) {
+  return guard([&] { free_loop_group(static_cast<LoopGroup*>(group)); });
+}
+
+int mlsqr_ctx_set_comm_loopback(mlsqr_ctx* ctx, void* group, int rank) {
+  return guard([&] {
+    delete ctx->impl.comm;
+    ctx->impl.comm = nullptr;
+    ctx->impl.comm = make_loop_comm(static_cast<LoopGroup*>(group), rank);
+  });
+}
+
+int mlsqr_ctx_set_slab(mlsqr_ctx* ctx, size_t nz_global, size_t z_offset) {
+  return guard([&] {
+    require(z_offset < nz_global, MLSQR_EINVAL, "slab offset outside the global grid");
+    ctx->impl.nzg = (long)nz_global;
+    ctx->impl.zoff = (long)z_offset;
+  });
+}
+
 // ---- operators ----
 int mlsqr_blur_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
                       const double* taps, int radius, mlsqr_op** out) {
@@ -220,6 +268,7 @@ int mlsqr_dense_create(mlsqr_ctx* ctx, size_t rows, size_t cols, const double* a
                        size_t sol_row_len, mlsqr_op** out) {
   return guard([&] {
     set_device(&ctx->impl);
+    require(!ctx->impl.sharded(), MLSQR_EINVAL, "dense operators are not z-sharded (use a plain context)");
     *out = new mlsqr_op{make_dense(&ctx->impl, rows, cols, a, a_kind == MLSQR_DEVICE, sol_row_len)};
   });
 }

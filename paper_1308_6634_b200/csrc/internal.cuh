@@ -140,6 +140,7 @@ struct Epi {
   const double* coef = nullptr;
   double* seg = nullptr;
   const int* gate = nullptr;
+  bool in_guarded = false;  // the input carries halo_planes_needed() zero/ghost planes per side
 };
 
 class Op {
@@ -148,6 +149,9 @@ class Op {
   Ctx* ctx = nullptr;
   size_t rows = 0, cols = 0;
   RowShape data_shape{}, sol_shape{};
+  // ghost planes the operator needs on its input when z-sharded (0: none)
+  virtual int halo_planes_needed() const { return 0; }
+  virtual size_t plane_size() const { return 0; }
   virtual void apply(const double* x, double* y, const Epi& e) = 0;
   virtual void adjoint(const double* y, double* x, const Epi& e) = 0;
   virtual int tclass() const { return MLSQR_TCLASS_BLUR; }
@@ -166,8 +170,33 @@ class Pc {
   virtual size_t row_len() const { return 0; }
 };
 
+// communicator of the z-slab decomposition (comm.cu)
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  int rank = 0, size = 1;
+  virtual bool capturable() const = 0;
+  // recv_lo <- (rank-1).send_hi ; recv_hi <- (rank+1).send_lo ; missing neighbours: untouched
+  virtual void halo(const double* send_lo, const double* send_hi, double* recv_lo, double* recv_hi,
+                    size_t count, cudaStream_t s) = 0;
+  // recv[k*count .. (k+1)*count) <- rank k's send
+  virtual void allgather(const double* send, size_t count, double* recv, cudaStream_t s) = 0;
+  virtual void allreduce_max_u64(unsigned long long* buf, cudaStream_t s) = 0;
+};
+struct LoopGroup;
+Comm* make_nccl_comm(const void* uid, int rank, int size);
+int nccl_unique_id(void* out128);
+LoopGroup* make_loop_group(int p);
+void free_loop_group(LoopGroup* g);
+Comm* make_loop_comm(LoopGroup* g, int rank);
+
 struct Ctx {
   int device = 0;
+  // z-slab decomposition: grids built on this context with z extent nz are the planes
+  // [zoff, zoff + nz) of a global grid with nzg planes (nzg == 0: not sharded)
+  Comm* comm = nullptr;
+  long zoff = 0, nzg = 0;
+  bool sharded() const { return comm != nullptr && comm->size > 1; }
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   uint64_t launches = 0;
@@ -300,6 +329,14 @@ size_t reduce_scratch_size(size_t nseg);
 void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, const int* gate);
 // out = x * sx + coef * (old * so) elementwise (identity operator / copies), with seg of out^2
 void axpby_epi(Ctx* c, const double* x, double* out, RowShape s, const Epi& e);
+// z-slab halo: fill k ghost planes below/above a guarded local vector from the neighbours
+void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k);
+// canonical reduction of this rank's segments of a z-sharded vector: bit-identical to the
+// unsharded reduction (block-aligned tree partials or raw segments are allgathered)
+void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                          double* out, const int* gate);
+// scratch sizes of reduce_segments_dist
+size_t dist_gather_size(Ctx* c, size_t nseg);
 
 // ---------------------------------------------------------------------------
 // operator / map factories (blur.cu, dense.cu, vcycle.cu)
@@ -325,7 +362,7 @@ Pc* vcycle_as_pc(VCycle* v);
 size_t vcycle_sol_len(VCycle* v);
 void penalty_functional_async(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
                               const double* f, int kind, double T, double* seg, double* scratch,
-                              double* out);
+                              double* gathered, double* fguard, double* out);
 Pc* make_callback_map(Ctx* c, size_t n, mlsqr_host_map_fn fn, void* user);
 double penalty_functional_dev(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
                               const double* f, int pen_kind, double T);
@@ -333,7 +370,12 @@ double penalty_functional_dev(Ctx* c, int dims, size_t nx, size_t ny, size_t nz,
 // solvers (lsqr.cu)
 struct Workspace;  // per-solve device buffers, reusable across outer steps
 Workspace* workspace_new(Ctx* c, size_t rows, size_t cols, RowShape data, RowShape sol,
-                         int max_iters);
+                         int max_iters, size_t guard = 0);
+// guard elements per side the Krylov vectors need for an operator's ghost planes
+inline size_t op_guard(const Op* o) {
+  const int k = o->halo_planes_needed();
+  return k > 0 ? (size_t)k * o->plane_size() + 64 : 0;
+}
 void workspace_free(Workspace* w);
 // Runs mlsqr (or lsqr when pc == nullptr) fully on the device.  Outputs to host arrays
 // when non-null.  `sync_out`: copy results back and return status; when false the solve
@@ -362,7 +404,7 @@ class OuterSolver {
   mlsqr_stop inner_{};
   VCycle* vc_ = nullptr;
   Workspace* ws_ = nullptr;
-  DevBuf<double> pseg_, pscr_, pval_;
+  DevBuf<double> pseg_, pscr_, pval_, pgat_, pfg_;
   std::vector<mlsqr_iter_rec> trace_;
 };
 

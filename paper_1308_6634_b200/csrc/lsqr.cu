@@ -39,13 +39,25 @@ struct DevState {
   int iter, iterations, stop_reason, error, error_iter, n_alphas, n_betas, breakdown;
 };
 
+// vector with a zero guard zone on both sides (operator ghost planes when z-sharded)
+struct GVec {
+  DevBuf<double> raw;
+  double* p = nullptr;
+  void alloc(size_t n, size_t g, cudaStream_t s) {
+    raw.alloc(n + 2 * g);
+    if (g) MLSQR_CUDA(cudaMemsetAsync(raw.p, 0, sizeof(double) * raw.n, s));
+    p = raw.p + g;
+  }
+};
+
 struct Workspace {
   Ctx* ctx;
-  size_t rows, cols;
+  size_t rows, cols, guard;
   RowShape data, sol;
   int max_iters;
-  DevBuf<double> u, p, v, w, q, tmp_rows;
-  DevBuf<double> seg_u, seg_p, seg_vp, seg_wq, seg_res, scratch;
+  GVec u, p, v;  // blur inputs (u for A^T, v -- or p in lsqr mode -- for A)
+  DevBuf<double> w, q, tmp_rows;
+  DevBuf<double> seg_u, seg_p, seg_vp, seg_wq, seg_res, scratch, gathered;
   DevBuf<DevState> st;
   DevBuf<mlsqr_iter_rec> trace;
   DevBuf<double> alphas, betas;
@@ -54,17 +66,18 @@ struct Workspace {
 };
 
 Workspace* workspace_new(Ctx* c, size_t rows, size_t cols, RowShape data, RowShape sol,
-                         int max_iters) {
+                         int max_iters, size_t guard) {
   auto* w = new Workspace();
   w->ctx = c;
   w->rows = rows;
   w->cols = cols;
+  w->guard = guard;
   w->data = data;
   w->sol = sol;
   w->max_iters = max_iters;
-  w->u.alloc(rows);
-  w->p.alloc(cols);
-  w->v.alloc(cols);
+  w->u.alloc(rows, guard, c->stream);
+  w->p.alloc(cols, guard, c->stream);
+  w->v.alloc(cols, guard, c->stream);
   w->w.alloc(cols);
   w->q.alloc(cols);
   w->seg_u.alloc(data.segments());
@@ -72,8 +85,10 @@ Workspace* workspace_new(Ctx* c, size_t rows, size_t cols, RowShape data, RowSha
   w->seg_p.alloc(sol.segments());
   w->seg_vp.alloc(sol.segments());
   w->seg_wq.alloc(sol.segments());
-  const size_t sc = reduce_scratch_size(data.segments() > sol.segments() ? data.segments() : sol.segments());
-  w->scratch.alloc(sc);
+  const size_t J = data.segments() > sol.segments() ? data.segments() : sol.segments();
+  const size_t G = dist_gather_size(c, J);
+  w->scratch.alloc(reduce_scratch_size(G > J ? G : J) + J);
+  w->gathered.alloc(G > 0 ? G : 1);
   w->st.alloc(1);
   w->trace.alloc((size_t)max_iters);
   w->alphas.alloc((size_t)max_iters + 1);
@@ -377,7 +392,7 @@ struct Runner {
   const int* gate_active() const { return flag(0); }
 
   void reduce(double* seg, size_t nseg, double* out, const int* gate) {
-    reduce_segments(c, seg, nseg, ws->scratch.p, out, gate);
+    reduce_segments_dist(c, seg, nseg, ws->scratch.p, ws->gathered.p, out, gate);
   }
 
   double* vbuf() const { return pc ? ws->v.p : ws->p.p; }
@@ -406,6 +421,7 @@ struct Runner {
     eb.sx = &st->su;
     eb.seg = ws->seg_p.p;
     eb.gate = gate_active();
+    eb.in_guarded = true;
     op->adjoint(ws->u.p, ws->p.p, eb);
     reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, gate_active());
     fin_p0_kernel<<<1, 1, 0, c->stream>>>(st);
@@ -430,6 +446,7 @@ struct Runner {
     ea.coef = &st->neg_alpha;
     ea.seg = ws->seg_u.p;
     ea.gate = gate_active();
+    ea.in_guarded = true;
     op->apply(vbuf(), ws->u.p, ea);
     reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active());
     fin_beta_kernel<<<1, 1, 0, c->stream>>>(st);
@@ -441,6 +458,7 @@ struct Runner {
     eb.coef = &st->neg_beta;
     eb.seg = ws->seg_p.p;
     eb.gate = flag(1);
+    eb.in_guarded = true;
     op->adjoint(ws->u.p, ws->p.p, eb);
     reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1));
     fin_p_kernel<<<1, 1, 0, c->stream>>>(st);
@@ -486,7 +504,8 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
   Workspace* ws = ws_in;
   auto fits = [&](Workspace* w) {
     return w && w->rows == op->rows && w->cols == op->cols && w->max_iters >= stop.max_iters &&
-           w->data.len == op->data_shape.len && w->sol.len == op->sol_shape.len;
+           w->data.len == op->data_shape.len && w->sol.len == op->sol_shape.len &&
+           w->guard >= op_guard(op);
   };
   if (!fits(ws)) {
     // reuse the context's cached workspace (no cudaMalloc per solve)
@@ -494,7 +513,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
     if (!fits(ws)) {
       if (ws) workspace_free(ws);
       c->ws_cache = nullptr;
-      ws = workspace_new(c, op->rows, op->cols, op->data_shape, op->sol_shape, stop.max_iters);
+      ws = workspace_new(c, op->rows, op->cols, op->data_shape, op->sol_shape, stop.max_iters, op_guard(op));
       c->ws_cache = ws;
       c->ws_free = [](void* p) { workspace_free(static_cast<Workspace*>(p)); };
     }
@@ -512,7 +531,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
 
   Runner r{op, pc, ws, tau, stop, ws->st.p, c};
   const bool host_cb = pc && pc->host_callback();
-  const bool graph = use_graph && !host_cb && !c->timing;
+  const bool graph = use_graph && !host_cb && !c->timing && (!c->comm || c->comm->capturable());
   r.init(g_dev);
   if (graph) {
     cudaGraph_t gr = nullptr;

@@ -42,11 +42,18 @@ OuterSolver::OuterSolver(Op* o, int dims, size_t nx, size_t ny, size_t nz, doubl
   if (cfg.inner_cap < inner_.max_iters) inner_.max_iters = cfg.inner_cap;
   vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, cfg.mg_levels, cfg.nu_pre, cfg.nu_post, cfg.omega,
                     cfg.coarse_sweeps);
-  ws_ = workspace_new(o->ctx, o->rows, o->cols, o->data_shape, o->sol_shape, inner_.max_iters);
+  ws_ = workspace_new(o->ctx, o->rows, o->cols, o->data_shape, o->sol_shape, inner_.max_iters, op_guard(o));
   RowShape s{nx, ey * ez};
-  pseg_.alloc(s.segments());
-  pscr_.alloc(reduce_scratch_size(s.segments()));
+  const size_t J = s.segments(), G = dist_gather_size(o->ctx, J);
+  pseg_.alloc(J);
+  pscr_.alloc(reduce_scratch_size(G > J ? G : J) + J);
+  pgat_.alloc(G > 0 ? G : 1);
   pval_.alloc(1);
+  if (o->ctx->sharded()) {
+    const size_t plane = nx * ey;
+    pfg_.alloc(s.n() + 2 * plane);
+    MLSQR_CUDA(cudaMemsetAsync(pfg_.p, 0, sizeof(double) * pfg_.n, o->ctx->stream));
+  }
   trace_.resize((size_t)inner_.max_iters);
   al_.resize((size_t)inner_.max_iters + 1);
   be_.resize((size_t)inner_.max_iters + 2);
@@ -66,7 +73,8 @@ void OuterSolver::step(const double* g, const double* f_prev, double* f_out, mls
   solve_mlsqr(op, vcycle_as_pc(vc_), g, cfg_.tau, inner_, f_out, trace_.data(), al_.data(),
               be_.data(), &info, ws_);
   penalty_functional_async(c, dims_, nx_, ny_, nz_, h_, f_out, cfg_.pen_kind, cfg_.T, pseg_.p,
-                           pscr_.p, pval_.p);
+                           pscr_.p, pgat_.p, pfg_.p ? pfg_.p + nx_ * (dims_ >= 2 ? ny_ : 1) : nullptr,
+                           pval_.p);
   double pv = 0.0, eps = 0.0;
   MLSQR_CUDA(cudaMemcpyAsync(&pv, pval_.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   MLSQR_CUDA(cudaMemcpyAsync(&eps, vcycle_eps_dev(vc_), sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -18,7 +18,8 @@ __device__ __forceinline__ double xv_zm(const double* __restrict__ x, const doub
                                         int cnx, int cny, int xx, int yy, int zz, long j) {
   double v = x[j];
   if (PROLONG) {
-    const int Z = D >= 3 ? zz / 2 : 0, Y = D >= 2 ? yy / 2 : 0;
+    // floor division: the ghost plane z = -1 of a slab belongs to coarse ghost plane -1
+    const int Z = D >= 3 ? (zz >> 1) : 0, Y = D >= 2 ? yy / 2 : 0;
     v = v + xc[((long)Z * cny + Y) * cnx + xx / 2];
   }
   return v;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
 
 // zero the boundary edges of explicitly supplied coefficients (an edge that leaves the
 // grid does not exist; the branch-free rows rely on its coefficient being exactly 0)
-__global__ void zero_boundary_edges_kernel(Lvl L, double* cx, double* cy, double* cz) {
+__global__ void zero_boundary_edges_kernel(Lvl L, int zoff, int nzg, double* cx, double* cy, double* cz) {
   const int rows = L.ny * L.nz;
   const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int xx = blockIdx.x * 32 + threadIdx.x;
@@ -240,7 +241,7 @@ __global__ void zero_boundary_edges_kernel(Lvl L, double* cx, double* cy, double
   const long i = (long)row * L.nx + xx;
   if (xx + 1 == L.nx) cx[i] = 0.0;
   if (cy && yy + 1 == L.ny) cy[i] = 0.0;
-  if (cz && zz + 1 == L.nz) cz[i] = 0.0;
+  if (cz && zz + zoff + 1 == nzg) cz[i] = 0.0;  // global top plane
 }
 
 // z chunk: enough blocks to fill the GPU a few times; even (restriction pairs fine planes)

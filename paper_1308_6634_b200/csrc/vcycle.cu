@@ -158,8 +158,9 @@ __global__ void __launch_bounds__(256) restrict_kernel(Lvl L, const double* __re
 }
 
 // Galerkin coarse edges (oracle coarsen()): sum of the fine edges crossing each coarse face
-__global__ void coarsen_kernel(Lvl F, int cnx, int cny, int cnz, double* __restrict__ ccx,
-                               double* __restrict__ ccy, double* __restrict__ ccz) {
+__global__ void coarsen_kernel(Lvl F, int cnx, int cny, int cnz, int czoff, int cnzg,
+                               double* __restrict__ ccx, double* __restrict__ ccy,
+                               double* __restrict__ ccz) {
   const int crows = cny * cnz;
   const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int X = blockIdx.x * 32 + threadIdx.x;
@@ -178,7 +179,7 @@ __global__ void coarsen_kernel(Lvl F, int cnx, int cny, int cnz, double* __restr
   if (F.cz)
     for (int dy = 0; dy < 2; ++dy)
       for (int dx = 0; dx < 2; ++dx)
-        if (Z + 1 < cnz) sz = sz + F.cz[(size_t)(2 * Z + 1) * fnxy + (size_t)(2 * Y + dy) * fnx + 2 * X + dx];
+        if (Z + czoff + 1 < cnzg) sz = sz + F.cz[(size_t)(2 * Z + 1) * fnxy + (size_t)(2 * Y + dy) * fnx + 2 * X + dx];
   const size_t I = (size_t)row * cnx + X;
   ccx[I] = sx;
   if (ccy) ccy[I] = sy;
@@ -188,7 +189,7 @@ __global__ void coarsen_kernel(Lvl F, int cnx, int cny, int cnz, double* __restr
 // K_D: edge coefficients from a field, plus the max unshifted diagonal (atomic max on
 // the bit pattern of non-negative doubles: order-independent, deterministic)
 __global__ void edge_coeffs_kernel(const double* __restrict__ f, int nx, int ny, int nz, int dims,
-                                   int kind, double T, double h, double scale,
+                                   int kind, double T, double h, double scale, int zoff, int nzg,
                                    double* __restrict__ cx, double* __restrict__ cy,
                                    double* __restrict__ cz) {
   const int rows = ny * nz;
@@ -200,7 +201,8 @@ __global__ void edge_coeffs_kernel(const double* __restrict__ f, int nx, int ny,
   const double fi = f[i];
   cx[i] = xx + 1 < nx ? diffusivity(kind, T, fabs((f[i + 1] - fi) / h)) * scale : 0.0;
   if (dims >= 2) cy[i] = yy + 1 < ny ? diffusivity(kind, T, fabs((f[i + nx] - fi) / h)) * scale : 0.0;
-  if (dims >= 3) cz[i] = zz + 1 < nz ? diffusivity(kind, T, fabs((f[i + nxy] - fi) / h)) * scale : 0.0;
+  // global top plane has no +z edge; a slab's top plane reads f from the ghost plane above
+  if (dims >= 3) cz[i] = zz + zoff + 1 < nzg ? diffusivity(kind, T, fabs((f[i + nxy] - fi) / h)) * scale : 0.0;
 }
 
 __global__ void max_diag_kernel(Lvl L, unsigned long long* __restrict__ out) {
@@ -229,7 +231,8 @@ __global__ void set_eps_kernel(const unsigned long long* __restrict__ maxd, doub
 
 // R(f): per-node sum of its x/y/z edge terms, canonical segment partials
 __global__ void penalty_kernel(const double* __restrict__ f, int nx, int ny, int nz, int dims,
-                               int kind, double T, double h, double w, double* __restrict__ seg) {
+                               int kind, double T, double h, double w, int zoff, int nzg,
+                               double* __restrict__ seg) {
   const int rows = ny * nz;
   const int row = blockIdx.y * blockDim.y + threadIdx.y;
   if (row >= rows) return;
@@ -241,7 +244,7 @@ __global__ void penalty_kernel(const double* __restrict__ f, int nx, int ny, int
     const double fi = f[i];
     if (xx + 1 < nx) v = v + w * r_value(kind, T, fabs((f[i + 1] - fi) / h));
     if (dims >= 2 && yy + 1 < ny) v = v + w * r_value(kind, T, fabs((f[i + nx] - fi) / h));
-    if (dims >= 3 && zz + 1 < nz) v = v + w * r_value(kind, T, fabs((f[i + nxy] - fi) / h));
+    if (dims >= 3 && zz + zoff + 1 < nzg) v = v + w * r_value(kind, T, fabs((f[i + nxy] - fi) / h));
   }
   const double s = tree32(v);
   if (threadIdx.x == 0) seg[(size_t)row * ((nx + 31) / 32) + blockIdx.x] = s;
@@ -305,6 +308,13 @@ class VCycle final : public Pc {
       L.xb.alloc(L.n, g, c->stream);
       if (l > 0) L.b.alloc(L.n);
     }
+    if (c->sharded()) {
+      // z slabs: every level's local planes must stay even-aligned with the global grid
+      require(dims == 3, MLSQR_EINVAL, "z-slab decomposition needs a 3D grid");
+      require(c->zoff % (long)f == 0 && c->nzg % (long)f == 0 && c->zoff + (long)ez <= c->nzg,
+              MLSQR_EINVAL, "slab offsets and the global z extent must be multiples of 2^(levels-1)");
+      fg_.alloc(n, (size_t)nx * ey + 64, c->stream);
+    }
     eps_.alloc((size_t)levels);
     maxd_.alloc(1);
     MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(false)));
@@ -329,19 +339,29 @@ class VCycle final : public Pc {
   }
 
   // build coarse levels from level 0 (device-resident); eps_cfg < 0 -> auto shift
+  // global z offset / extent of level l (slab decomposition; identity when unsharded)
+  int zoff_l(int l) const { return ctx->sharded() ? (int)(ctx->zoff >> l) : 0; }
+  int nzg_l(int l) const { return ctx->sharded() ? (int)(ctx->nzg >> l) : lv_[(size_t)l].nz; }
+
   void build(double eps_cfg) {
     Level& L0 = lv_[0];
     MLSQR_CUDA(cudaMemsetAsync(maxd_.p, 0, sizeof(unsigned long long), ctx->stream));
     max_diag_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(view(0), maxd_.p);
+    ctx->count();
+    if (ctx->sharded()) ctx->comm->allreduce_max_u64(maxd_.p, ctx->stream);  // order-free max
     set_eps_kernel<<<1, 1, 0, ctx->stream>>>(maxd_.p, eps_cfg, mult(), (int)lv_.size(), eps_.p);
-    ctx->count(2);
+    ctx->count();
     for (size_t l = 1; l < lv_.size(); ++l) {
       Level& C = lv_[l];
       coarsen_kernel<<<row_grid(C.nx, C.ny * C.nz), dim3(32, 8), 0, ctx->stream>>>(
-          view((int)l - 1), C.nx, C.ny, C.nz, C.cx.p, dims_ >= 2 ? C.cy.p : nullptr,
-          dims_ >= 3 ? C.cz.p : nullptr);
+          view((int)l - 1), C.nx, C.ny, C.nz, zoff_l((int)l), nzg_l((int)l), C.cx.p,
+          dims_ >= 2 ? C.cy.p : nullptr, dims_ >= 3 ? C.cz.p : nullptr);
       ctx->count();
     }
+    // the sweeps read cz[z-1] of the plane below a slab: fill its ghost on every level
+    if (ctx->sharded() && dims_ >= 3)
+      for (size_t l = 0; l < lv_.size(); ++l)
+        halo_planes(ctx, lv_[l].cz.p, (size_t)lv_[l].nx * lv_[l].ny, lv_[l].nz, 1);
     ctx->check_launch();
   }
 
@@ -351,21 +371,32 @@ class VCycle final : public Pc {
     if (dims_ >= 2) MLSQR_CUDA(cudaMemcpyAsync(L0.cy.p, cy, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
     if (dims_ >= 3) MLSQR_CUDA(cudaMemcpyAsync(L0.cz.p, cz, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
     zero_boundary_edges_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(
-        view(0), L0.cx.p, dims_ >= 2 ? L0.cy.p : nullptr, dims_ >= 3 ? L0.cz.p : nullptr);
+        view(0), zoff_l(0), nzg_l(0), L0.cx.p, dims_ >= 2 ? L0.cy.p : nullptr, dims_ >= 3 ? L0.cz.p : nullptr);
     ctx->count();
     build(eps);
   }
 
-  double update(const double* f, int kind, double T, double eps_cfg) {
+  // K_D from a field f (device, unguarded): the slab's top plane needs f one plane above
+  void edge_coeffs(const double* f, int kind, double T) {
     Level& L0 = lv_[0];
     const double h = h_;
     double w = h;
     if (dims_ >= 2) w = h * h;
     if (dims_ >= 3) w = h * h * h;
     const double scale = w / (h * h);
+    const double* src = f;
+    if (ctx->sharded()) {
+      MLSQR_CUDA(cudaMemcpyAsync(fg_.p, f, sizeof(double) * L0.n, cudaMemcpyDeviceToDevice, ctx->stream));
+      halo_planes(ctx, fg_.p, (size_t)L0.nx * L0.ny, L0.nz, 1);
+      src = fg_.p;
+    }
     edge_coeffs_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(
-        f, L0.nx, L0.ny, L0.nz, dims_, kind, T, h, scale, L0.cx.p, L0.cy.p, L0.cz.p);
+        src, L0.nx, L0.ny, L0.nz, dims_, kind, T, h, scale, zoff_l(0), nzg_l(0), L0.cx.p, L0.cy.p, L0.cz.p);
     ctx->count();
+  }
+
+  double update(const double* f, int kind, double T, double eps_cfg) {
+    edge_coeffs(f, kind, T);
     build(eps_cfg);
     double e = 0.0;
     MLSQR_CUDA(cudaMemcpyAsync(&e, eps_.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -375,15 +406,7 @@ class VCycle final : public Pc {
 
   // device-resident variant used by the outer loop (no host sync); eps stays on device
   void update_async(const double* f, int kind, double T, double eps_cfg) {
-    Level& L0 = lv_[0];
-    const double h = h_;
-    double w = h;
-    if (dims_ >= 2) w = h * h;
-    if (dims_ >= 3) w = h * h * h;
-    const double scale = w / (h * h);
-    edge_coeffs_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(
-        f, L0.nx, L0.ny, L0.nz, dims_, kind, T, h, scale, L0.cx.p, L0.cy.p, L0.cz.p);
-    ctx->count();
+    edge_coeffs(f, kind, T);
     build(eps_cfg);
   }
   const double* eps_dev() const { return eps_.p; }
@@ -448,7 +471,7 @@ class VCycle final : public Pc {
     int nb = 0;
     // pre-smoothing (or the whole coarse solve) from zero
     const double* cur = nullptr;
-    const bool fuse = fused_ok(l);
+    const bool fuse = fused_ok(l) && !ctx->sharded();
     for (int s = 0; s < pre; ++s) {
       const bool pair = fuse && s == 0 && pre >= 2;  // sweeps 1 + 2 in one kernel
       const bool last_here = coarsest && s + (pair ? 2 : 1) == pre;
@@ -460,6 +483,7 @@ class VCycle final : public Pc {
       } else if (s == 0) {
         sweep<kFirst>(l, nullptr, nullptr, b, dst, sg, gate);
       } else {
+        hx(l, cur);
         sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
       }
       cur = dst;
@@ -467,6 +491,7 @@ class VCycle final : public Pc {
     }
     if (coarsest) return cur;
     Level& C = lv_[(size_t)l + 1];
+    hx(l, cur);
     restrict_to(l, cur, b, gate);
     const double* xc = level(l + 1, C.b.p, nullptr, nullptr, gate);
     if (nu_post_ == 0) {
@@ -483,8 +508,11 @@ class VCycle final : public Pc {
         sweep2<true>(l, cur, xc, b, dst, sg, gate);
         ++s;
       } else if (s == 0) {
+        hx(l, cur);
+        hx(l + 1, xc);
         sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
       } else {
+        hx(l, cur);
         sweep<kNormal>(l, cur, nullptr, b, dst, sg, gate);
       }
       cur = dst;
@@ -526,6 +554,14 @@ class VCycle final : public Pc {
   std::vector<Level> lv_;
   DevBuf<double> eps_;
   DevBuf<unsigned long long> maxd_;
+  GBuf fg_;  // guarded copy of the field for K_D (z-sharded)
+
+  // fill the one-plane ghosts of a level-l iterate (z-sharded)
+  void hx(int l, const double* v) {
+    if (!ctx->sharded()) return;
+    const Level& L = lv_[(size_t)l];
+    halo_planes(ctx, const_cast<double*>(v), (size_t)L.nx * L.ny, L.nz, 1);
+  }
 };
 
 VCycle* make_vcycle(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h, int levels,
@@ -563,36 +599,50 @@ class IdentityMap final : public Pc {
 Pc* make_identity_map(Ctx* c, size_t n) { return new IdentityMap(c, n); }
 
 // R(f) on the device, canonical order; returns to the host (synchronizes)
+// R(f) on the device in canonical order.  z-sharded: f is copied into the guarded
+// buffer fguard (n + 2 planes) so the slab's top plane sees f one plane above, and the
+// segment partials are reduced across ranks.
+void penalty_functional_async(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
+                              const double* f, int kind, double T, double* seg, double* scratch,
+                              double* gathered, double* fguard, double* out) {
+  const size_t ey = dims >= 2 ? ny : 1, ez = dims >= 3 ? nz : 1;
+  RowShape s{nx, ey * ez};
+  double w = h;
+  if (dims >= 2) w = h * h;
+  if (dims >= 3) w = h * h * h;
+  const double* src = f;
+  if (c->sharded()) {
+    require(fguard != nullptr, MLSQR_EINVAL, "sharded R(f) needs a guarded buffer");
+    MLSQR_CUDA(cudaMemcpyAsync(fguard, f, sizeof(double) * s.n(), cudaMemcpyDeviceToDevice, c->stream));
+    halo_planes(c, fguard, nx * ey, (long)ez, 1);
+    src = fguard;
+  }
+  const int zoff = c->sharded() ? (int)c->zoff : 0, nzg = c->sharded() ? (int)c->nzg : (int)ez;
+  penalty_kernel<<<row_grid((int)nx, (int)(ey * ez)), dim3(32, 8), 0, c->stream>>>(
+      src, (int)nx, (int)ey, (int)ez, dims, kind, T, h, w, zoff, nzg, seg);
+  c->count();
+  reduce_segments_dist(c, seg, s.segments(), scratch, gathered, out, nullptr);
+}
+
 double penalty_functional_dev(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
                               const double* f, int kind, double T) {
   const size_t ey = dims >= 2 ? ny : 1, ez = dims >= 3 ? nz : 1;
   RowShape s{nx, ey * ez};
-  DevBuf<double> seg(s.segments()), scratch(reduce_scratch_size(s.segments())), out(1);
-  double w = h;
-  if (dims >= 2) w = h * h;
-  if (dims >= 3) w = h * h * h;
-  penalty_kernel<<<row_grid((int)nx, (int)(ey * ez)), dim3(32, 8), 0, c->stream>>>(
-      f, (int)nx, (int)ey, (int)ez, dims, kind, T, h, w, seg.p);
-  c->count();
-  reduce_segments(c, seg.p, s.segments(), scratch.p, out.p, nullptr);
+  const size_t J = s.segments();
+  const size_t G = dist_gather_size(c, J);
+  DevBuf<double> seg(J), scratch(reduce_scratch_size(G > J ? G : J) + J), gathered(G > 0 ? G : 1), out(1);
+  DevBuf<double> fg;
+  double* fguard = nullptr;
+  if (c->sharded()) {
+    fg.alloc(s.n() + 2 * nx * ey);
+    MLSQR_CUDA(cudaMemsetAsync(fg.p, 0, sizeof(double) * fg.n, c->stream));
+    fguard = fg.p + nx * ey;
+  }
+  penalty_functional_async(c, dims, nx, ny, nz, h, f, kind, T, seg.p, scratch.p, gathered.p, fguard, out.p);
   double r = 0.0;
   MLSQR_CUDA(cudaMemcpyAsync(&r, out.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   MLSQR_CUDA(cudaStreamSynchronize(c->stream));
   return r;
-}
-
-void penalty_functional_async(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
-                              const double* f, int kind, double T, double* seg, double* scratch,
-                              double* out) {
-  const size_t ey = dims >= 2 ? ny : 1, ez = dims >= 3 ? nz : 1;
-  RowShape s{nx, ey * ez};
-  double w = h;
-  if (dims >= 2) w = h * h;
-  if (dims >= 3) w = h * h * h;
-  penalty_kernel<<<row_grid((int)nx, (int)(ey * ez)), dim3(32, 8), 0, c->stream>>>(
-      f, (int)nx, (int)ey, (int)ez, dims, kind, T, h, w, seg);
-  c->count();
-  reduce_segments(c, seg, s.segments(), scratch, out, nullptr);
 }
 
 }  // namespace mlsqr_b200

@@ -106,4 +106,40 @@ void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, do
   c->check_launch();
 }
 
+// ---------------------------------------------------------------------------
+// z-slab decomposition helpers
+// ---------------------------------------------------------------------------
+void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k) {
+  if (!c->sharded() || k <= 0) return;
+  require(nz_loc >= k, MLSQR_EDIM, "z slab thinner than the halo it must provide");
+  const size_t cnt = plane * (size_t)k;
+  c->comm->halo(v, v + (size_t)(nz_loc - k) * plane, v - cnt, v + (size_t)nz_loc * plane, cnt, c->stream);
+}
+
+size_t dist_gather_size(Ctx* c, size_t nseg) {
+  const size_t P = c->comm ? (size_t)c->comm->size : 1;
+  return (nseg % 32768 == 0 ? nseg / 32768 : nseg) * P;
+}
+
+void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                          double* out, const int* gate) {
+  if (!c->sharded()) {
+    reduce_segments(c, seg, nseg, scratch, out, gate);
+    return;
+  }
+  const size_t P = (size_t)c->comm->size;
+  if (nseg % 32768 == 0) {
+    // this rank's segments are whole 32768-blocks of the global list: levels 1-3 locally
+    const size_t K = nseg / 32768;
+    reduce3_kernel<<<(unsigned)K, 1024, 0, c->stream>>>(seg, nseg, scratch, gate);
+    c->count();
+    c->check_launch();
+    c->comm->allgather(scratch, K, gathered, c->stream);
+    reduce_segments(c, gathered, K * P, scratch, out, gate);
+  } else {
+    c->comm->allgather(seg, nseg, gathered, c->stream);
+    reduce_segments(c, gathered, nseg * P, scratch, out, gate);
+  }
+}
+
 }  // namespace mlsqr_b200

@@ -71,23 +71,24 @@ def test_c1_full_config_bit_exact(ctx, dev):
     assert np.linalg.norm(rep.solution - f) < np.linalg.norm(g - f)
 
 
-def test_c2_first_outer_step_bit_exact(ctx, dev):
-    """C2: 1024^2, sigma 3 px / 19 taps, 32 discs/rectangles, smoothed TV T=0.01, tau 5e-3, 30 its."""
+def test_c2_full_config_bit_exact(ctx, dev):
+    """C2: 1024^2, sigma 3 px / 19 taps, 32 discs/rectangles, smoothed TV T=0.01, tau 5e-3, 5 x 30."""
     taps, f, g, o = make_2d(dev, 1024, 3.0, 9, "shapes", 32, 2)
-    rep, orep = run_both(dev, taps, g, o, (1024, 1024), "tv", 0.01, 5e-3, 1, 30, 5)
+    rep, orep = run_both(dev, taps, g, o, (1024, 1024), "tv", 0.01, 5e-3, 5, 30, 5)
     assert_same(rep, orep, 30)
+    assert np.linalg.norm(rep.solution - f) < np.linalg.norm(g - f)
 
 
-def test_c3_first_outer_step_bit_exact(ctx, dev):
-    """C3: 128^3, sigma 1.5 vox / 9 taps, 10 ellipsoids, 2% noise, PM-log T=0.05, tau 1e-2 (20 of 40 its)."""
+def test_c3_full_config_bit_exact(ctx, dev):
+    """C3: 128^3, sigma 1.5 vox / 9 taps, 10 ellipsoids, 2% noise, PM-log T=0.05, tau 1e-2, 5 x 40."""
     n = 128
     taps = dev.taps(n, 1.5 / n, radius=4)
     f = dev.ellipsoids3d(n, n, n, 10, 8.0, 40.0, 0.2, 1.0, 3)
     o = dev.blur(3, (n, n, n), taps)
     af = o.apply(f)
     g = af + dev.gauss(1003, n ** 3, 0.02 * np.abs(af).max())
-    rep, orep = run_both(dev, taps, g, o, (n, n, n), "pm_log", 0.05, 1e-2, 1, 20, 5)
-    assert_same(rep, orep, 20)
+    rep, orep = run_both(dev, taps, g, o, (n, n, n), "pm_log", 0.05, 1e-2, 5, 40, 5)
+    assert_same(rep, orep, 40)
 
 
 def test_c4_reduced_bit_exact(ctx, dev):

@@ -1,0 +1,145 @@
+"""z-slab decomposition on one GPU: P virtual ranks (loopback communicator, one thread and
+one Context per rank) must reproduce the unsharded results BIT FOR BIT -- blur with R-plane
+ghosts, the V-cycle hierarchy with one-plane ghosts on every level and an allreduced max
+diagonal, the canonical reductions (allgathered block partials / raw segments), mlsqr and
+the outer loop.  The NCCL transport runs exactly the same code with ncclSend/Recv and
+ncclAllGather instead of the loopback copies."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1308_6634_b200 as mb
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
+
+
+def run_ranks(P, nz, fn):
+    group = mb.LoopGroup(P)
+    ctxs = []
+    for r in range(P):
+        c = mb.Context(0)
+        c.set_comm_loopback(group, r)
+        c.set_slab(nz, r * nz // P)
+        ctxs.append(c)
+    out, errs = [None] * P, []
+
+    def work(r):
+        try:
+            out[r] = fn(r, ctxs[r], slice(r * nz // P, (r + 1) * nz // P))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=500)
+    assert not any(t.is_alive() for t in th), "a virtual rank hung"
+    assert not errs, errs
+    return out
+
+
+def planes(v, shape):
+    nx, ny, nz = shape
+    return v.reshape(nz, ny * nx)
+
+
+@pytest.fixture(scope="module")
+def problem():
+    shape = (64, 40, 64)
+    nx, ny, nz = shape
+    taps = mb.gaussian_taps(nx, 2.0 / nx, 6)
+    rng = np.random.default_rng(3)
+    f = mb.phantom_ellipsoids3d(nx, ny, nz, 6, 4.0, 16.0, 0.2, 1.0, 9)
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    af = op.apply(f)
+    g = af + 0.01 * np.abs(af).max() * rng.standard_normal(f.size)
+    return shape, taps, f, g
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_blur_and_vcycle_sharded_bit_exact(problem, P):
+    shape, taps, f, g = problem
+    nx, ny, nz = shape
+    h = 1.0 / nx
+    x = np.random.default_rng(P).uniform(-1, 1, f.size)
+    ref_y = mb.SeparableGaussianBlur(shape, taps=taps).apply(x)
+    vc = mb.VCycleMap(shape, h, 4)
+    ref_eps = vc.update(f, mb.PenaltySpec.tv_smoothed(0.05))
+    ref_v = vc.solve(x)
+
+    def fn(r, ctx, sl):
+        loc = (nx, ny, sl.stop - sl.start)
+        op = mb.SeparableGaussianBlur(loc, taps=taps, ctx=ctx)
+        y = op.apply(planes(x, shape)[sl].ravel())
+        m = mb.VCycleMap(loc, h, 4, ctx=ctx)
+        eps = m.update(planes(f, shape)[sl].ravel(), mb.PenaltySpec.tv_smoothed(0.05))
+        v = m.solve(planes(x, shape)[sl].ravel())
+        return y, eps, v
+
+    res = run_ranks(P, nz, fn)
+    assert np.array_equal(np.concatenate([r[0] for r in res]), ref_y)
+    assert all(r[1] == ref_eps for r in res)
+    assert np.array_equal(np.concatenate([r[2] for r in res]), ref_v)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_mlsqr_and_outer_sharded_bit_exact(problem, P):
+    shape, taps, f, g = problem
+    nx, ny, nz = shape
+    h = 1.0 / nx
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    vc = mb.VCycleMap(shape, h, 4)
+    vc.update(f, mb.PenaltySpec.tv_smoothed(0.05))
+    st = mb.StoppingConfig.max_iterations(15)
+    ref = mb.mlsqr(op, vc, g, 5e-3, st)
+    cfg = mb.OuterConfig(tau=5e-3, penalty=mb.PenaltySpec.tv_smoothed(0.05),
+                         inner_stop=mb.StoppingConfig.max_iterations(8), inner_cap=8,
+                         rel_decrease_threshold=0.0, max_outer=2, mg_levels=4)
+    ref_nl = mb.solve_nonlinear(op, g, shape, h, cfg)
+
+    def fn(r, ctx, sl):
+        loc = (nx, ny, sl.stop - sl.start)
+        o = mb.SeparableGaussianBlur(loc, taps=taps, ctx=ctx)
+        m = mb.VCycleMap(loc, h, 4, ctx=ctx)
+        m.update(planes(f, shape)[sl].ravel(), mb.PenaltySpec.tv_smoothed(0.05))
+        gl = planes(g, shape)[sl].ravel()
+        res = mb.mlsqr(o, m, gl, 5e-3, st)
+        nl = mb.solve_nonlinear(o, gl, loc, h, cfg)
+        return res, nl
+
+    out = run_ranks(P, nz, fn)
+    for res, nl in out:
+        assert np.array_equal(res.alphas, ref.alphas) and np.array_equal(res.betas, ref.betas)
+        assert [s.penalty_value for s in nl.steps] == [s.penalty_value for s in ref_nl.steps]
+        assert [s.eps_used for s in nl.steps] == [s.eps_used for s in ref_nl.steps]
+    assert np.array_equal(np.concatenate([o[0].solution for o in out]), ref.solution)
+    assert np.array_equal(np.concatenate([o[1].solution for o in out]), ref_nl.solution)
+
+
+def test_block_aligned_reduction_path_bit_exact():
+    """1024 x 64 x 64 with P = 2: each rank owns 65536 reduction segments (two whole
+    32768-blocks), so the ranks allgather level-3 tree partials instead of raw segments."""
+    shape = (1024, 64, 64)
+    nx, ny, nz = shape
+    h = 1.0 / nx
+    taps = mb.gaussian_taps(nx, 2.0 / nx, 4)
+    rng = np.random.default_rng(7)
+    g = rng.uniform(-1, 1, nx * ny * nz)
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    vc = mb.VCycleMap(shape, h, 3)
+    vc.update(np.zeros(g.size), mb.PenaltySpec.tikhonov())
+    st = mb.StoppingConfig.max_iterations(6)
+    ref = mb.mlsqr(op, vc, g, 1e-2, st)
+
+    def fn(r, ctx, sl):
+        loc = (nx, ny, sl.stop - sl.start)
+        o = mb.SeparableGaussianBlur(loc, taps=taps, ctx=ctx)
+        m = mb.VCycleMap(loc, h, 3, ctx=ctx)
+        m.update(np.zeros(nx * ny * loc[2]), mb.PenaltySpec.tikhonov())
+        return mb.mlsqr(o, m, planes(g, shape)[sl].ravel(), 1e-2, st)
+
+    out = run_ranks(2, nz, fn)
+    assert all(np.array_equal(o.alphas, ref.alphas) for o in out)
+    assert np.array_equal(np.concatenate([o.solution for o in out]), ref.solution)
