@@ -143,3 +143,21 @@ def test_block_aligned_reduction_path_bit_exact():
     out = run_ranks(2, nz, fn)
     assert all(np.array_equal(o.alphas, ref.alphas) for o in out)
     assert np.array_equal(np.concatenate([o.solution for o in out]), ref.solution)
+
+
+def test_nccl_world1_transport_loads_and_solves():
+    """The NCCL transport on one GPU: dlopen + ncclGetUniqueId + ncclCommInitRank through the
+    C-ABI, then a solve on that context (world 1 = unsharded, so results equal the plain
+    context's).  N > 1 needs one GPU per rank; the loopback tests above run the same
+    Comm-interface call sequence bit-exact."""
+    from paper_1308_6634_b200 import dist as pdist
+    uid = mb.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
+    ctx = pdist.sharded_context(0, 0, 1, 32, uid)
+    shape = (32, 32, 32)
+    taps = mb.gaussian_taps(32, 2.0 / 32, 4)
+    g = np.random.default_rng(1).uniform(-1, 1, 32 ** 3)
+    st = mb.StoppingConfig.max_iterations(5)
+    a = mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps, ctx=ctx), mb.IdentityMap(g.size, ctx=ctx), g, 1e-2, st)
+    b = mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), mb.IdentityMap(g.size), g, 1e-2, st)
+    assert np.array_equal(a.solution, b.solution)
