@@ -53,7 +53,8 @@ static Api& api() {
       if (a.h) break;
     }
     if (!a.h) return;
-    auto sym = [](const char* s) { return dlsym(api().h, s); };
+    void* h = a.h;  // (never re-enter api() inside call_once: that deadlocks)
+    auto sym = [h](const char* s) { return dlsym(h, s); };
     a.GetUniqueId = (decltype(a.GetUniqueId))sym("ncclGetUniqueId");
     a.CommInitRank = (decltype(a.CommInitRank))sym("ncclCommInitRank");
     a.CommDestroy = (decltype(a.CommDestroy))sym("ncclCommDestroy");

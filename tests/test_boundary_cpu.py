@@ -85,3 +85,11 @@ def test_python_mirror_validation_matches_reference_contract():
         mb.PenaltySpec.tv_smoothed(0.0).validate()
     assert issubclass(mb.DimensionError, ValueError)
     assert mb.BreakdownError("x", 3).iteration == 3
+
+
+@pytest.mark.timeout(60)
+def test_nccl_unique_id_without_gpu():
+    """ncclGetUniqueId only opens the bootstrap socket: it works here and must not hang
+    (regression: the dlopen'ed symbol table was once resolved re-entrantly under call_once)."""
+    uid = mb.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
