@@ -20,6 +20,10 @@
 // (xpby with the old vector, also staged by cp.async, plus the canonical
 // |out|^2 segment partials) is fused.  HBM traffic: read x once, read old
 // once, write out once.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "internal.cuh"
 #include "vec.cuh"
 
@@ -339,29 +343,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict_
 #undef TAP
 }
 
-template <int R, bool VEC>
-static void launch_b3v(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
-                       const EpiArgs& a) {
-  using C = B3<R>;
-  static bool attr = false;
-  if (!attr) {
-    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_fused<R, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
-  const int zchunk = nz >= 256 ? 64 : (nz >= 64 ? 32 : nz);
-  dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
-  const int zoff = c->sharded() ? (int)c->zoff : 0, nzg = c->sharded() ? (int)c->nzg : nz;
-  blur3d_fused<R, VEC><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, t, a);
-  c->count();
-}
-
-template <int R>
-static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
-                      const EpiArgs& a) {
-  if (R % 2 == 0 && nx % 2 == 0) launch_b3v<R, true>(c, in, out, nx, ny, nz, t, a);
-  else launch_b3v<R, false>(c, in, out, nx, ny, nz, t, a);
-}
-
+#include "blur3d_pipe.cuh"
 // radius dispatch for the fused kernel (BASELINE taps: 9 (R=4) and 13 (R=6))
 static bool fused3d(Ctx* c, int R, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
                     const EpiArgs& a) {

@@ -1,0 +1,347 @@
+// blur3d_pipe.cuh -- the default fused 3D blur (included by blur.cu).
+//
+// Same per-output arithmetic as blur3d_fused (hence bit-identical), scheduled
+// for the issue-bound regime the FP64 stencil lives in:
+//  * TMA: one thread loads each input plane tile (a (32+2R) x P box; the
+//    hardware zero-fills everything outside the grid, so no per-element
+//    predicates) and the old-vector tile into a 4-stage ring completed by
+//    mbarriers.  Falls back to 8-byte cp.async when a tensor map is impossible
+//    (odd nx, misaligned vector);
+//  * phase p runs the x pass of plane p+1 next to the y pass of plane p (x-pass
+//    results double-buffered), so one __syncthreads per plane suffices;
+//  * the z pass keeps 2R+1 running accumulators per column instead of a ring of
+//    raw planes: plane p adds its tap-(p - zo + R) term to every output zo it
+//    touches -- 2R+1 independent DFMAs rather than one 2R+1-long dependent chain.
+//    Each output still receives fma(t[0], y[zo-R], 0), fma(t[1], y[zo-R+1], .),
+//    ... in ascending order;
+//  * |out|^2 goes to shared memory and warp 15 (no x-pass work) forms the
+//    canonical row-segment trees one phase later (tree32_serial == tree32).
+// (included inside namespace mlsqr_b200; blur.cu includes <cudaTypedefs.h> and <mutex>)
+
+template <int R>
+struct B3P {
+  static constexpr int NT = 2 * R + 1;
+  static constexpr int TX = 32, TY = 32;
+  static constexpr int THREADS = 512;
+  static constexpr int W = TX + 2 * R;
+  static constexpr int H = TY + 2 * R;
+  static constexpr int XK = 4;
+  static constexpr int XG = TX / XK;
+  // smem column c holds global x = x0 - R - XOFF + c: the TMA box must start at a
+  // 16-byte aligned x (an odd start coordinate faults), so odd R loads one extra column
+  static constexpr int XOFF = R & 1;
+  static constexpr int WE = (W + XOFF + 1) / 2 * 2;   // even box width
+  static constexpr int P = ((WE / 2) % 2) ? WE : WE + 2;  // row pitch = box width (P/2 odd)
+  static constexpr int WL = (XK + 2 * R + XOFF + 1) / 2 * 2;  // x-window doubles per task
+  static constexpr int XP = 34;
+  static constexpr int SQP = 34;
+  static constexpr int NSTAGE = 4;  // input + old ring (old plane read 3 phases after issue)
+  static constexpr int TREE_WARP = 15;
+  static constexpr int IN_SLOT = (H * P + 15) / 16 * 16;  // 128-byte aligned TMA destinations
+  static constexpr int OLD_DOUBLES = TX * TY;
+  static constexpr int XS_DOUBLES = H * XP;
+  static constexpr int SQ_DOUBLES = TY * SQP;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)NSTAGE * IN_SLOT + (size_t)NSTAGE * OLD_DOUBLES +
+                                                   2 * XS_DOUBLES + 2 * SQ_DOUBLES) +
+                                 NSTAGE * sizeof(unsigned long long);
+  static constexpr unsigned IN_BYTES = H * P * 8u;
+  static constexpr unsigned OLD_BYTES = TX * TY * 8u;
+  static_assert(H * XG <= TREE_WARP * 32, "x-pass tasks must leave the tree warp free");
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load3d(double* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                           unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int R, bool TMA>
+__global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__ in, double* __restrict__ out,
+                                                      int nx, int ny, int nz, int zchunk, int zoff, int nzg,
+                                                      int zshift, Taps taps, EpiArgs e,
+                                                      const __grid_constant__ CUtensorMap map_in,
+                                                      const __grid_constant__ CUtensorMap map_old) {
+  using C = B3P<R>;
+  if (e.gate && *e.gate == 0) return;
+  extern __shared__ __align__(128) double sm[];
+  double* tin = sm;                                       // [NSTAGE][IN_SLOT]  rows of pitch P
+  double* olds = tin + C::NSTAGE * C::IN_SLOT;            // [NSTAGE][TY][TX]
+  double* xs = olds + C::NSTAGE * C::OLD_DOUBLES;         // [2][H][XP]
+  double* sq = xs + 2 * C::XS_DOUBLES;                    // [2][TY][SQP]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sq + 2 * C::SQ_DOUBLES);
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * C::TX, y0 = blockIdx.y * C::TY;
+  const int z0 = blockIdx.z * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int zlo = z0 - R, zhi = z1 + R - 1;
+  const size_t nxy = (size_t)nx * ny;
+  const double sx = e.sx ? *e.sx : 1.0;
+#define TAP(k) taps.t[(k) <= R ? (k) : 2 * R - (k)]
+
+  if (TMA && tid == 0) {
+#pragma unroll
+    for (int s = 0; s < C::NSTAGE; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto inside = [&](int zz) { return zz >= zlo && zz <= zhi && zz + zoff >= 0 && zz + zoff < nzg; };
+  // stage q: input plane q and old plane q - R
+  auto issue = [&](int zz) {
+    const int st = (zz - zlo) & (C::NSTAGE - 1);
+    const int zo = zz - R;
+    const bool lin = inside(zz);
+    const bool lold = e.old && zo >= z0 && zo < z1;
+    if (TMA) {
+      if (tid == 0) {  // always arrive, so every stage's phase advances once per use
+        mbar_arrive_expect(bars + st, (lin ? C::IN_BYTES : 0u) + (lold ? C::OLD_BYTES : 0u));
+        if (lin) tma_load3d(tin + st * C::IN_SLOT, &map_in, x0 - R - C::XOFF, y0 - R, zz + zshift, bars + st);
+        if (lold) tma_load3d(olds + st * C::OLD_DOUBLES, &map_old, x0, y0, zo, bars + st);
+      }
+    } else {
+      if (lin) {
+        double* dst = tin + st * C::IN_SLOT;
+        const double* src = in + (size_t)zz * nxy;
+        for (int k = tid; k < C::H * C::W; k += C::THREADS) {
+          const int ly = k / C::W, lx = k - ly * C::W;
+          const int gx = x0 + lx - R, gy = y0 + ly - R;
+          const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+          cp_async8(dst + ly * C::P + lx + C::XOFF, ok ? src + (size_t)gy * nx + gx : in, ok);
+        }
+      }
+      if (lold) {
+        double* dst = olds + st * C::OLD_DOUBLES;
+        const double* src = e.old + (size_t)zo * nxy;
+        for (int k = tid; k < C::TX * C::TY; k += C::THREADS) {
+          const int ly = k >> 5, lx = k & 31;
+          const int gx = x0 + lx, gy = y0 + ly;
+          const bool ok = gx < nx && gy < ny;
+          cp_async8(dst + k, ok ? src + (size_t)gy * nx + gx : in, ok);
+        }
+      }
+      cp_async_commit();
+    }
+  };
+
+  const int tx = tid & 31, ty = tid >> 5;
+  const int xr = tid % C::H, xg = tid / C::H;
+  const bool xtask = tid < C::H * C::XG;
+  const double so = e.so ? *e.so : 1.0;
+  const double coef = e.old ? *e.coef : 0.0;
+  const size_t chunks = (size_t)(nx + 31) / 32;
+  const int gx = x0 + tx, gy0 = y0 + 2 * ty;
+  const bool ok0 = gx < nx && gy0 < ny, ok1 = gx < nx && gy0 + 1 < ny;
+  double* const obase = out + (size_t)gy0 * nx + gx;
+  double acc[2][C::NT];
+#pragma unroll
+  for (int o = 0; o < 2; ++o)
+#pragma unroll
+    for (int k = 0; k < C::NT; ++k) acc[o][k] = 0.0;
+
+  issue(zlo);
+  issue(zlo + 1);
+  for (int pb = zlo - 1; pb <= zhi + 1; pb += C::NT) {
+#pragma unroll
+    for (int u = 0; u < C::NT; ++u) {
+      const int p = pb + u;
+      if (p <= zhi + 1) {  // block-uniform
+        // stage p+1 (x-pass input of this phase, old plane of the next) has landed
+        if (TMA) mbar_wait(bars + ((p + 1 - zlo) & (C::NSTAGE - 1)), ((p + 1 - zlo) >> 2) & 1);
+        else cp_async_wait<1>();
+        __syncthreads();  // ... for everyone; phase p-1 is done with every buffer
+        issue(p + 3);
+        const int xz = p + 1;
+        if (xtask && inside(xz)) {
+          const double* row = tin + ((xz - zlo) & (C::NSTAGE - 1)) * C::IN_SLOT + xr * C::P + C::XK * xg;
+          double w[C::WL];
+#pragma unroll
+          for (int j = 0; j < C::WL / 2; ++j) {
+            const double2 q = *reinterpret_cast<const double2*>(row + 2 * j);
+            w[2 * j] = q.x;
+            w[2 * j + 1] = q.y;
+          }
+          if (e.sx) {
+#pragma unroll
+            for (int j = C::XOFF; j < C::XK + 2 * R + C::XOFF; ++j) w[j] = w[j] * sx;
+          }
+          double a[C::XK];
+#pragma unroll
+          for (int o = 0; o < C::XK; ++o) {
+            a[o] = 0.0;
+#pragma unroll
+            for (int k = 0; k < C::NT; ++k) a[o] = fma(TAP(k), w[o + k + C::XOFF], a[o]);
+          }
+          double* xw = xs + ((xz - zlo) & 1) * C::XS_DOUBLES + xr * C::XP + C::XK * xg;
+          *reinterpret_cast<double2*>(xw) = make_double2(a[0], a[1]);
+          *reinterpret_cast<double2*>(xw + 2) = make_double2(a[2], a[3]);
+        }
+        if (p >= zlo && p <= zhi) {
+          double yv0 = 0.0, yv1 = 0.0;
+          if (inside(p)) {
+            const double* xb = xs + ((p - zlo) & 1) * C::XS_DOUBLES + 2 * ty * C::XP + tx;
+            double c[2 + 2 * R];
+#pragma unroll
+            for (int j = 0; j < 2 + 2 * R; ++j) c[j] = xb[j * C::XP];
+#pragma unroll
+            for (int k = 0; k < C::NT; ++k) {
+              yv0 = fma(TAP(k), c[k], yv0);
+              yv1 = fma(TAP(k), c[k + 1], yv1);
+            }
+          }
+          // output zo' = p - R + j takes tap 2R - j; j = 2R starts output p + R
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) {
+            const int s = (u + j) % C::NT;
+            acc[0][s] = fma(TAP(2 * R - j), yv0, j == C::NT - 1 ? 0.0 : acc[0][s]);
+            acc[1][s] = fma(TAP(2 * R - j), yv1, j == C::NT - 1 ? 0.0 : acc[1][s]);
+          }
+          const int zo = p - R;  // complete now (slot u)
+          if (zo >= z0 && zo < z1) {
+            const double* po = olds + ((p - zlo) & (C::NSTAGE - 1)) * C::OLD_DOUBLES + 2 * ty * 32 + tx;
+            double* sqb = sq + ((zo - z0) & 1) * C::SQ_DOUBLES + 2 * ty * C::SQP + tx;
+            double* orow = obase + (size_t)zo * nxy;
+            double v0 = ok0 ? acc[0][u] : 0.0, v1 = ok1 ? acc[1][u] : 0.0;
+            if (e.old) {
+              double o0 = po[0], o1 = po[32];
+              if (e.so) {
+                o0 = o0 * so;
+                o1 = o1 * so;
+              }
+              if (ok0) v0 = v0 + coef * o0;
+              if (ok1) v1 = v1 + coef * o1;
+            }
+            if (ok0) orow[0] = v0;
+            if (ok1) orow[nx] = v1;
+            if (e.seg) {
+              sqb[0] = v0 * v0;
+              sqb[C::SQP] = v1 * v1;
+            }
+          }
+        }
+        // canonical segment partials of the plane completed in the previous phase
+        const int zt = p - R - 1;
+        if (e.seg && ty == C::TREE_WARP && zt >= z0 && zt < z1) {
+          const int gy = y0 + tx;
+          if (gy < ny) {
+            const double* r = sq + ((zt - z0) & 1) * C::SQ_DOUBLES + tx * C::SQP;
+            double v[32];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const double2 q = *reinterpret_cast<const double2*>(r + 2 * j);
+              v[2 * j] = q.x;
+              v[2 * j + 1] = q.y;
+            }
+            e.seg[((size_t)zt * ny + gy) * chunks + blockIdx.x] = tree32_serial(v);
+          }
+        }
+      }
+    }
+  }
+#undef TAP
+}
+
+// ---- host side ------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    (void)cudaGetLastError();
+  });
+  return fn;
+}
+
+// fp64 tensor map of an (nx, ny, nz) grid with a (bx, by, 1) box; false if TMA cannot address it
+static bool tensor_map3d(CUtensorMap* m, const double* base, int nx, int ny, int nz, int bx, int by) {
+  auto enc = tensor_map_encoder();
+  if (!enc || (nx & 1) || (reinterpret_cast<uintptr_t>(base) & 15) || bx > 256 || by > 256) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool blur_legacy() {
+  static const bool v = [] {
+    const char* s = getenv("MLSQR_BLUR_LEGACY");
+    return s && s[0] == '1';
+  }();
+  return v;
+}
+
+template <int R, bool VEC>
+static void launch_b3_legacy(Ctx* c, const double* in, double* out, int nx, int ny, int nz, int zchunk,
+                             const Taps& t, const EpiArgs& a) {
+  static bool attr = false;
+  if (!attr) {
+    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_fused<R, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B3<R>::SMEM));
+    attr = true;
+  }
+  dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
+  const int zoff = c->sharded() ? (int)c->zoff : 0, nzg = c->sharded() ? (int)c->nzg : nz;
+  blur3d_fused<R, VEC><<<grd, B3<R>::THREADS, B3<R>::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, t, a);
+}
+
+template <int R>
+static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
+                      const EpiArgs& a) {
+  using C = B3P<R>;
+  const int zchunk = nz >= 256 ? 64 : (nz >= 64 ? 32 : nz);
+  if (blur_legacy()) {
+    if (R % 2 == 0 && nx % 2 == 0) launch_b3_legacy<R, true>(c, in, out, nx, ny, nz, zchunk, t, a);
+    else launch_b3_legacy<R, false>(c, in, out, nx, ny, nz, zchunk, t, a);
+    c->count();
+    return;
+  }
+  static bool attr = false;
+  if (!attr) {
+    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_pipe<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_pipe<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
+  const bool sh = c->sharded();
+  const int zoff = sh ? (int)c->zoff : 0, nzg = sh ? (int)c->nzg : nz;
+  // z-sharded inputs carry R ghost planes on either side (guard zones): map them too
+  const int zshift = sh ? R : 0;
+  CUtensorMap mi{}, mo{};
+  bool tma = tensor_map3d(&mi, in - (size_t)zshift * nx * ny, nx, ny, nz + 2 * zshift, C::P, C::H);
+  if (tma && a.old) tma = tensor_map3d(&mo, a.old, nx, ny, nz, C::TX, C::TY);
+  if (getenv("MLSQR_BLUR_NOTMA")) tma = false;
+  if (getenv("MLSQR_BLUR_DEBUG")) fprintf(stderr, "blur3d_pipe R=%d tma=%d P=%d H=%d smem=%zu\n", R, (int)tma, C::P, C::H, C::SMEM);
+  if (tma)
+    blur3d_pipe<R, true><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, zshift, t,
+                                                                  a, mi, mo);
+  else
+    blur3d_pipe<R, false><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, zshift, t,
+                                                                   a, mi, mo);
+  c->count();
+}
+
