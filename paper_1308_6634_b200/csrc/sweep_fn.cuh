@@ -1,0 +1,163 @@
+// sweep_fn.cuh -- the first two pre-smoothing sweeps of a level fused in one
+// z-marching kernel (3D; included by vcycle.cu).
+//
+//   x1  = 0 + (omega * (b - 0)) / D                     (sweep 1 from zero: pointwise)
+//   out = x1 + (omega * (b - M x1)) / D                 (sweep 2, + optional <out, b> partials)
+//
+// Sweep 1 needs no neighbours, so the intermediate iterate never touches HBM:
+// each thread computes x1 at its own point one plane ahead and publishes it in
+// a 3-plane shared ring (one __syncthreads per plane); two extra warps compute
+// x1 on the y-halo rows and a third on the x-halo columns.  b and the edge
+// coefficients are read once (the neighbour coefficients cx[i-1], cy[i-nx] are
+// L1/L2 hits, cz[i-nxy] stays in a register), so level-0 traffic drops from
+// 5 + 6 words per voxel (two sweeps) to 4 + 1.
+//
+// Bit-exactness: D and both row sums are formed in exactly the order of
+// sweep_zm_kernel (diag_at / m_row, sparse.cpp:65-74).  x1 outside the domain is
+// 0 here where the unfused kernel read some finite in-domain value -- either way
+// it meets an exactly-zero boundary coefficient and acc + (+-0) == acc.
+namespace fn {
+constexpr int TX = 32, TY = 8;
+constexpr int ROWS = TY + 2, COLS = TX + 2;
+constexpr int WARPS = ROWS + 1;  // rows y0-1 .. y0+TY, then the x-halo warp
+constexpr int THREADS = 32 * WARPS;
+constexpr int MINB = 2;  // resident blocks per SM (80 registers)
+}  // namespace fn
+
+struct FnPlane {
+  double b, cx, cxm, cy, cym, cz;
+};
+
+__device__ __forceinline__ FnPlane fn_load(const Lvl& L, const double* __restrict__ b, bool on, long i,
+                                           long nx) {
+  FnPlane s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (on) {
+    s.b = b[i];
+    s.cx = L.cx[i];
+    s.cxm = L.cx[i - 1];
+    s.cy = L.cy[i];
+    s.cym = L.cy[i - nx];
+    s.cz = L.cz[i];
+  }
+  return s;
+}
+
+// diag_at order: x-, x+, y-, y+, z-, z+ ; then + eps
+__device__ __forceinline__ double fn_diag(const FnPlane& s, double czm, double eps) {
+  double d = 0.0;
+  d = d + s.cxm;
+  d = d + s.cx;
+  d = d + s.cym;
+  d = d + s.cy;
+  d = d + czm;
+  d = d + s.cz;
+  return d + eps;
+}
+
+__global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, const double* __restrict__ b,
+                                                                  double* __restrict__ out, double omega,
+                                                                  double* __restrict__ seg, const int* gate,
+                                                                  int zc) {
+  using namespace fn;
+  if (gate && *gate == 0) return;
+  __shared__ double ring[3][ROWS][COLS];
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int nx = L.nx, ny = L.ny, nz = L.nz;
+  const long nxy = (long)nx * ny;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(nz, z0 + zc);
+  // the point this thread computes x1 for, and where it publishes it
+  int px, py, sr, sc;
+  bool act;
+  if (w < ROWS) {
+    px = x0 + lane;
+    py = y0 - 1 + w;
+    sr = w;
+    sc = lane + 1;
+    act = true;
+  } else {
+    const int side = lane / TY, k = lane % TY;
+    px = side ? x0 + TX : x0 - 1;
+    py = y0 + k;
+    sr = k + 1;
+    sc = side ? COLS - 1 : 0;
+    act = lane < 2 * TY;
+  }
+  const bool inxy = act && px >= 0 && px < nx && py >= 0 && py < ny;
+  const bool outw = w >= 1 && w <= TY;  // output rows (whole warps)
+  const bool ix = inxy && outw;
+  const double eps = *L.eps;
+  const long chunks = (nx + 31) / 32;
+  const long col = inxy ? (long)py * nx + px : 0;
+  auto idx = [&](int z) { return (long)z * nxy + col; };
+  auto on = [&](int z) { return inxy && z >= 0 && z < nz; };
+  auto first = [&](const FnPlane& s, double d, bool in) { return in ? 0.0 + (omega * (s.b - 0.0)) / d : 0.0; };
+
+  // prologue: plane z0-1 (own column only), plane z0 (published), plane z0+1 (loaded)
+  double czm = on(z0 - 1) ? L.cz[idx(z0 - 2)] : 0.0;
+  FnPlane m = fn_load(L, b, on(z0 - 1), idx(z0 - 1), nx);
+  double x1m = first(m, fn_diag(m, czm, eps), on(z0 - 1));
+  FnPlane c = fn_load(L, b, on(z0), idx(z0), nx);
+  double czm_c = m.cz;  // cz of plane z0-1
+  double dc = fn_diag(c, czm_c, eps);
+  double x1c = first(c, dc, on(z0));
+  if (act) ring[0][sr][sc] = x1c;
+  FnPlane n = fn_load(L, b, on(z0 + 1), idx(z0 + 1), nx);
+  int slot = 0;  // ring slot of plane z
+  for (int z = z0; z < z1; ++z) {
+    FnPlane f = fn_load(L, b, on(z + 2), idx(z + 2), nx);  // prefetch
+    const double dn = fn_diag(n, c.cz, eps);
+    const double x1n = first(n, dn, on(z + 1));
+    const int ns = slot == 2 ? 0 : slot + 1;
+    if (act) ring[ns][sr][sc] = x1n;
+    __syncthreads();
+    if (outw) {
+      double v = 0.0;
+      if (ix) {
+        // m_row order: z-, y-, x-, diag, x+, y+, z+
+        double acc = 0.0;
+        acc = acc + -czm_c * x1m;
+        acc = acc + -c.cym * ring[slot][sr - 1][sc];
+        acc = acc + -c.cxm * ring[slot][sr][sc - 1];
+        acc = acc + dc * x1c;
+        acc = acc + -c.cx * ring[slot][sr][sc + 1];
+        acc = acc + -c.cy * ring[slot][sr + 1][sc];
+        acc = acc + -c.cz * x1n;
+        v = x1c + (omega * (c.b - acc)) / dc;
+        out[idx(z)] = v;
+      }
+      if (seg) {
+        const double s = tree32(v * (ix ? c.b : 0.0));
+        if (lane == 0) seg[((long)z * ny + py) * chunks + blockIdx.x] = s;
+      }
+    }
+    x1m = x1c;
+    x1c = x1n;
+    czm_c = c.cz;
+    c = n;
+    dc = dn;
+    n = f;
+    slot = ns;
+  }
+}
+
+// z chunk minimising (waves x planes per block), chunks of >= 8 planes
+static inline int fn_chunk(int nx, int ny, int nz, int sms) {
+  const long bxy = (long)((nx + fn::TX - 1) / fn::TX) * ((ny + fn::TY - 1) / fn::TY);
+  const long slots = (long)fn::MINB * sms;
+  int best = nz;
+  double best_cost = 1e30;
+  for (int ch = 1; ch <= nz; ++ch) {
+    const int zc = (nz + ch - 1) / ch;
+    if (zc < 8 && ch > 1) break;
+    const long blocks = bxy * ((nz + zc - 1) / zc);
+    const long waves = (blocks + slots - 1) / slots;
+    // time ~ waves of (zc + 2) planes
+    const double cost = (double)waves * (zc + 2);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = zc;
+    }
+  }
+  return best;
+}

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restr
 
 #include "stencil_zm.cuh"
 #include "sweep2.cuh"
+#include "sweep_fn.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
 __global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
@@ -322,6 +323,7 @@ class VCycle final : public Pc {
     // the smem-tiled two-sweep kernel (sweep2.cuh) is opt-in: on B200 the branch-free
     // z-marching sweeps are faster (see profiles/README.md)
     if (const char* e = getenv("MLSQR_FUSED_SWEEPS")) fuse_enabled_ = e[0] == '1';
+    if (const char* e = getenv("MLSQR_FN_SWEEPS")) fn_enabled_ = e[0] != '0';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
   }
 
@@ -474,11 +476,15 @@ class VCycle final : public Pc {
     const bool fuse = fused_ok(l) && !ctx->sharded();
     for (int s = 0; s < pre; ++s) {
       const bool pair = fuse && s == 0 && pre >= 2;  // sweeps 1 + 2 in one kernel
-      const bool last_here = coarsest && s + (pair ? 2 : 1) == pre;
+      const bool fpair = !pair && fn_ok(l) && s == 0 && pre >= 2;  // same, x1 kept on chip
+      const bool last_here = coarsest && s + ((pair || fpair) ? 2 : 1) == pre;
       double* dst = (last_here && out) ? out : bufs[nb];
       double* sg = (last_here && out) ? seg : nullptr;
       if (pair) {
         sweep2<false>(l, nullptr, nullptr, b, dst, sg, gate);
+        ++s;
+      } else if (fpair) {
+        sweep_fn(l, b, dst, sg, gate);
         ++s;
       } else if (s == 0) {
         sweep<kFirst>(l, nullptr, nullptr, b, dst, sg, gate);
@@ -524,6 +530,19 @@ class VCycle final : public Pc {
   // fused two-sweep kernel: 16-byte plane copies need an even x extent
   bool fused_ok(int l) const { return fuse_enabled_ && lv_[(size_t)l].nx % 2 == 0; }
 
+  // first + second pre-sweep in one kernel (3D, unsharded: x1 halos are computed, not exchanged)
+  bool fn_ok(int) const { return fn_enabled_ && dims_ == 3 && !ctx->sharded(); }
+
+  void sweep_fn(int l, const double* b, double* out, double* seg, const int* gate) {
+    const Level& L = lv_[(size_t)l];
+    TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    const int zc = fn_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
+    dim3 grd((unsigned)((L.nx + fn::TX - 1) / fn::TX), (unsigned)((L.ny + fn::TY - 1) / fn::TY),
+             (unsigned)((L.nz + zc - 1) / zc));
+    sweep_fn_kernel<<<grd, dim3(32, fn::WARPS), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate, zc);
+    ctx->count();
+  }
+
   template <bool PROLONG>
   void sweep2(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
               const int* gate) {
@@ -544,6 +563,7 @@ class VCycle final : public Pc {
 
  public:
   bool fuse_enabled_ = false;
+  bool fn_enabled_ = true;
 
  private:
 
