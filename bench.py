@@ -84,19 +84,34 @@ def canonical_bytes_per_iter(cfg) -> float:
     return 8.0 * (W_A + W_B + W_MG + W_U)
 
 
-def class_bytes(cfg):
+def class_bytes(cfg, world=1):
     """Algorithmic bytes per launch of each timed kernel class (level-0 vectors, 8 B words)."""
     d = cfg["dims"]
     n = float(cfg["n"] ** d)
     r = 2.0 ** -d
-    # four level-0 sweeps per V(2,2): first-from-zero (b, d coefs -> x), normal (x, b, d coefs -> x),
-    # prolong+sweep (x, x_c, b, d coefs -> x), normal (+ <v,p> partials)
-    sweep_words = [(2 + d), (3 + d), (3 + d + r), (3 + d)]
+    if d == 3 and world == 1:
+        # level-0 smoothing launches per V(2,2): fused first+second sweep (b, cx, cy, cz -> x),
+        # prolong+sweep (x, x_c, b, cx, cy, cz -> x), last sweep (x, b, cx, cy, cz -> x)
+        sweep_words = [4 + 1, (3 + d + r), (3 + d)]
+    else:
+        # unfused: first-from-zero, normal, prolong+sweep, normal
+        sweep_words = [(2 + d), (3 + d), (3 + d + r), (3 + d)]
     return {
         "blur": 8.0 * 3 * n,                       # read x, read old, write out (m = n)
-        "smooth": 8.0 * n * sum(sweep_words) / 4,  # average per sweep launch
+        "smooth": 8.0 * n * sum(sweep_words) / len(sweep_words),  # average per level-0 launch
         "update": 8.0 * 8 * n,                     # read f w q v p, write f w q
     }
+
+
+def measured_traffic(kernel_class):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the class's
+    level-0 kernels from the committed `ncu --set full` captures (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        return t["classes"][kernel_class]["bytes_per_launch"], t["source"]
+    except Exception:
+        return None, None
 
 
 def make_problem(mb, cfg):
@@ -329,13 +344,18 @@ def main():
     torch.cuda.synchronize()
     cls_ms = {k: ctx.timing(c) for k, c in mb.TCLASS.items()}
     ctx.set_timing(False)
-    cb = {k: v / world for k, v in class_bytes(cfg).items()}  # this rank's slab
+    cb = {k: v / world for k, v in class_bytes(cfg, world).items()}  # this rank's slab
     peak, peak_src = peaks()
     cands = {"blur": cls_ms["blur"], "smooth": cls_ms["smooth"], "update": cls_ms["update"]}
     dom = max(cands, key=lambda k: cands[k][0])
     dms, dn = cands[dom]
     achieved = cb[dom] * dn / (dms / 1000.0) / 1e9 if dms > 0 else None
     it_ms = cls_ms["iter"][0] / max(1, cls_ms["iter"][1])
+    traffic, traffic_src = measured_traffic(dom) if world == 1 and args.config == "c5" else (None, None)
+    per_class = {k: {"ms_per_launch": v[0] / v[1], "algorithmic_bytes": cb[k],
+                     "achieved_gbs": cb[k] / (v[0] / v[1] / 1e3) / 1e9,
+                     "frac": cb[k] / (v[0] / v[1] / 1e3) / 1e9 / peak}
+                 for k, v in cands.items() if v[1] > 0}
     b_iter = canonical_bytes_per_iter(cfg)
 
     # ---- e2e through the public API with host (pinned) buffers
@@ -386,13 +406,15 @@ def main():
                        f"z-slabs x{world}: NCCL ghost planes + allgathered canonical tree partials",
                        "l2": "no flush needed: every vector (8 B x %d) exceeds the 126 MB L2" % N},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if achieved else None, "traffic": None,
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": cb[dom], "traffic_source": traffic_src,
                          "peak_source": peak_src,
                          "note": "algorithmic bytes per launch / mean CUDA-event launch time, instrumented step"},
             "iteration_roofline": {"bytes_per_iter": b_iter, "model": "SURVEY.md 8d canonical B_iter",
                                    "achieved_gbs": b_iter * value / world / 1e9,
                                    "frac": b_iter * value / world / 1e9 / peak},
             "kernel_classes_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in cls_ms.items()},
+            "class_rooflines": per_class,
             "instrumented_ms_per_iter": it_ms,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -78,5 +78,38 @@ def full(path, out):
     print("\n".join(lines))
 
 
+def traffic(tag, out):
+    """profiles/traffic.json: DRAM bytes per launch of each level-0 hot kernel (one ncu --set full
+    capture each, gpurun_out/<tag>_full_<name>.ncu-rep) and the per-class averages bench.py reads."""
+    import json
+    import os
+    per = {}
+    for name in ("blur", "sweep_fn", "sweep_prolong", "sweep_normal", "restrict", "update"):
+        rep = f"gpurun_out/{tag}_full_{name}.ncu-rep"
+        if not os.path.exists(rep):
+            continue
+        r = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                            "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                           capture_output=True, text=True).stdout
+        rows = list(csv.reader(r.splitlines()))
+        hdr, units, row = rows[0], rows[1], rows[2]
+        g = lambda m: (row[hdr.index(m)], units[hdr.index(m)])
+        per[name] = {"kernel": row[hdr.index("Kernel Name")].split("(")[0].replace("void ", ""),
+                     "dram_bytes": 1e9 * (to_gb(*g("dram__bytes_read.sum")) + to_gb(*g("dram__bytes_write.sum"))),
+                     "ms": to_ms(*g("gpu__time_duration.sum"))}
+    classes = {}
+    if "blur" in per:
+        classes["blur"] = {"bytes_per_launch": per["blur"]["dram_bytes"], "kernels": ["blur"]}
+    sm = [k for k in ("sweep_fn", "sweep_prolong", "sweep_normal") if k in per]
+    if sm:
+        classes["smooth"] = {"bytes_per_launch": sum(per[k]["dram_bytes"] for k in sm) / len(sm), "kernels": sm}
+    if "update" in per:
+        classes["update"] = {"bytes_per_launch": per["update"]["dram_bytes"], "kernels": ["update"]}
+    doc = {"source": f"ncu --set full captures gpurun_out/{tag}_full_*.ncu-rep (512^3 C5 driver, level-0 launches)",
+           "kernels": per, "classes": classes}
+    open(out, "w").write(json.dumps(doc, indent=1) + "\n")
+    print(json.dumps(doc, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](sys.argv[2], sys.argv[3])
