@@ -97,6 +97,14 @@ int mlsqr_loop_group_create(int size, void** group);
 int mlsqr_loop_group_destroy(void* group);
 int mlsqr_ctx_set_comm_loopback(mlsqr_ctx* ctx, void* group, int rank);
 int mlsqr_ctx_set_slab(mlsqr_ctx* ctx, size_t nz_global, size_t z_offset);
+/* Row shards (DenseOperator linop.hpp:59-71 with its rows split over ranks):
+ * rank k holds data rows [row_offset, row_offset + rows_global / P) of every data-space vector
+ * and of the dense operator (mlsqr_dense_create takes the local rows; the fDOT generator forms
+ * them).  The solution space and the preconditioner are replicated.  A x is local; A^T u
+ * allgathers the 8 canonical row-chunk partials and sums them in chunk order, and the data-space
+ * norms allgather their segment partials -- so P in {1, 2, 4, 8} is bit-identical to P = 1.
+ * Needs rows_global % 8 == 0 and whole 32-row segments per rank. */
+int mlsqr_ctx_set_row_shard(mlsqr_ctx* ctx, size_t rows_global, size_t row_offset);
 
 /* ---- LinearOperator (linop.hpp:21-47) ----------------------------------- */
 /* Separable Gaussian blur with explicit taps (SeparableGaussianBlur2D, linop.hpp:110-126,

@@ -115,6 +115,7 @@ SIGNATURES = {
     "mlsqr_loop_group_destroy": (C.c_int, [C.c_void_p]),
     "mlsqr_ctx_set_comm_loopback": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "mlsqr_ctx_set_slab": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
+    "mlsqr_ctx_set_row_shard": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
     "mlsqr_blur_create": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, dp,
                                     C.c_int, C.POINTER(C.c_void_p)]),
     "mlsqr_dense_create": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
@@ -239,6 +240,11 @@ class Context:
         """Objects built on this context with z extent nz are planes [z_offset, z_offset+nz)
         of a global grid with nz_global planes."""
         _check(lib().mlsqr_ctx_set_slab(self.h, nz_global, z_offset))
+
+    def set_row_shard(self, rows_global: int, row_offset: int) -> None:
+        """Dense operators built on this context hold data rows [row_offset, row_offset +
+        rows_global / P); solution-space vectors and preconditioners are replicated."""
+        _check(lib().mlsqr_ctx_set_row_shard(self.h, rows_global, row_offset))
 
     def set_comm_nccl(self, unique_id: bytes, rank: int, size: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)

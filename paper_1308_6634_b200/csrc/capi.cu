@@ -249,8 +249,18 @@ int mlsqr_ctx_set_comm_loopback(mlsqr_ctx* ctx, void* group, int rank) {
 int mlsqr_ctx_set_slab(mlsqr_ctx* ctx, size_t nz_global, size_t z_offset) {
   return guard([&] {
     require(z_offset < nz_global, MLSQR_EINVAL, "slab offset outside the global grid");
+    ctx->impl.row_mode = false;
     ctx->impl.nzg = (long)nz_global;
     ctx->impl.zoff = (long)z_offset;
+  });
+}
+
+int mlsqr_ctx_set_row_shard(mlsqr_ctx* ctx, size_t rows_global, size_t row_offset) {
+  return guard([&] {
+    require(row_offset < rows_global, MLSQR_EINVAL, "row shard offset outside the data space");
+    ctx->impl.row_mode = true;
+    ctx->impl.rows_g = (long)rows_global;
+    ctx->impl.row0 = (long)row_offset;
   });
 }
 
@@ -260,6 +270,7 @@ int mlsqr_blur_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
   return guard([&] {
     set_device(&ctx->impl);
     require(taps != nullptr, MLSQR_EINVAL, "taps must not be null");
+    require(!ctx->impl.row_sharded(), MLSQR_EINVAL, "a blur is z-sharded, not row-sharded (mlsqr_ctx_set_slab)");
     *out = new mlsqr_op{make_blur(&ctx->impl, dims, nx, ny, nz, taps, radius)};
   });
 }
@@ -268,7 +279,7 @@ int mlsqr_dense_create(mlsqr_ctx* ctx, size_t rows, size_t cols, const double* a
                        size_t sol_row_len, mlsqr_op** out) {
   return guard([&] {
     set_device(&ctx->impl);
-    require(!ctx->impl.sharded(), MLSQR_EINVAL, "dense operators are not z-sharded (use a plain context)");
+    require(!ctx->impl.sharded(), MLSQR_EINVAL, "dense operators are row-sharded, not z-sharded (mlsqr_ctx_set_row_shard)");
     *out = new mlsqr_op{make_dense(&ctx->impl, rows, cols, a, a_kind == MLSQR_DEVICE, sol_row_len)};
   });
 }

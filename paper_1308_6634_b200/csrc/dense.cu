@@ -109,6 +109,51 @@ __global__ void __launch_bounds__(256) gemvt_kernel(const double* __restrict__ A
   out[j] = epilogue(tot, e, j);
 }
 
+// row shards: this rank's canonical row chunks of A^T (y*sy), one partial n-vector per chunk
+// (the same per-chunk loop as gemvt_kernel), later allgathered and summed in chunk order
+__global__ void __launch_bounds__(256) gemvt_part_kernel(const double* __restrict__ A,
+                                                         const double* __restrict__ y, size_t rows,
+                                                         size_t cols, double* __restrict__ part,
+                                                         const double* sx, const int* gate, int chunks) {
+  if (gate && *gate == 0) return;
+  const size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const double s = sx ? *sx : 1.0;
+  const size_t ch = rows / (size_t)chunks;
+  for (int c = 0; c < chunks; ++c) {
+    double acc = 0.0;
+    const size_t i0 = (size_t)c * ch, i1 = i0 + ch;
+    size_t i = i0;
+    for (; i + 4 <= i1; i += 4) {
+      const double a0 = A[i * cols + j], a1 = A[(i + 1) * cols + j];
+      const double a2 = A[(i + 2) * cols + j], a3 = A[(i + 3) * cols + j];
+      double y0 = y[i], y1 = y[i + 1], y2 = y[i + 2], y3 = y[i + 3];
+      if (sx) { y0 = y0 * s; y1 = y1 * s; y2 = y2 * s; y3 = y3 * s; }
+      acc = acc + y0 * a0;
+      acc = acc + y1 * a1;
+      acc = acc + y2 * a2;
+      acc = acc + y3 * a3;
+    }
+    for (; i < i1; ++i) {
+      double yi = y[i];
+      if (sx) yi = yi * s;
+      acc = acc + yi * A[i * cols + j];
+    }
+    part[(size_t)c * cols + j] = acc;
+  }
+}
+
+// the 8 gathered chunk partials summed in chunk order (gemvt_kernel's tot), then the epilogue
+__global__ void gemvt_combine_kernel(const double* __restrict__ part, size_t cols, int chunks,
+                                     double* __restrict__ out, EpiArgs e) {
+  if (e.gate && *e.gate == 0) return;
+  const size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double tot = 0.0;
+  for (int c = 0; c < chunks; ++c) tot = chunks == 1 ? part[j] : tot + part[(size_t)c * cols + j];
+  out[j] = epilogue(tot, e, j);
+}
+
 __global__ void epi_vec_kernel(const double* __restrict__ in, double* __restrict__ out, size_t n,
                                EpiArgs e) {
   if (e.gate && *e.gate == 0) return;
@@ -117,11 +162,12 @@ __global__ void epi_vec_kernel(const double* __restrict__ in, double* __restrict
 }
 
 __global__ void fdot_form_kernel(const double* __restrict__ gs, const double* __restrict__ gd,
-                                 size_t nvox, int ndet, size_t rows, double* __restrict__ A) {
+                                 size_t nvox, int ndet, size_t rows, size_t row0,
+                                 double* __restrict__ A) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t row = blockIdx.y + (size_t)gridDim.y * blockIdx.z;
   if (row >= rows || idx >= nvox) return;
-  const size_t s = row / (size_t)ndet, d = row % (size_t)ndet;
+  const size_t s = (row0 + row) / (size_t)ndet, d = (row0 + row) % (size_t)ndet;
   A[row * nvox + idx] = gs[s * nvox + idx] * gd[d * nvox + idx];
 }
 
@@ -132,6 +178,18 @@ class DenseOp final : public Op {
     rows = r;
     cols = cl;
     require(r >= 1 && cl >= 1, MLSQR_EDIM, "operator shape must be at least 1x1");
+    if (c->row_sharded()) {
+      // rank k holds rows [k m/P, (k+1) m/P): whole canonical A^T chunks and whole 32-row
+      // reduction segments, so every result equals the unsharded operator's bit for bit
+      const long P = c->comm->size;
+      require(c->rows_g > 0 && c->rows_g % 8 == 0 && 8 % P == 0, MLSQR_EINVAL,
+              "row shards need m % 8 == 0 and P in {1, 2, 4, 8}");
+      require((long)r * P == c->rows_g, MLSQR_EDIM, "local rows must be m / P");
+      require((r % 32) == 0, MLSQR_EDIM, "local rows must be a multiple of 32 (whole reduction segments)");
+      require(c->row0 == (long)r * c->comm->rank, MLSQR_EINVAL, "row shard offset must be rank * m / P");
+      part_.alloc((size_t)(8 / P) * cl);
+      gath_.alloc((size_t)8 * cl);
+    }
     data_shape = RowShape{rows, 1};
     const size_t L = (sol_row_len && cols % sol_row_len == 0) ? sol_row_len : cols;
     sol_shape = RowShape{L, cols / L};
@@ -166,17 +224,27 @@ class DenseOp final : public Op {
 
   void adjoint(const double* y, double* x, const Epi& e) override {
     TimedRegion tr(ctx, MLSQR_TCLASS_DENSE);
-    const int chunks = rows % 8 == 0 ? 8 : 1;
     EpiArgs a = to_args(e);
     a.seg = nullptr;
-    gemvt_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, ctx->stream>>>(a_.p, y, rows, cols, x, a, chunks);
-    ctx->count();
+    if (ctx->row_sharded()) {
+      const int local = 8 / ctx->comm->size;
+      gemvt_part_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, ctx->stream>>>(a_.p, y, rows, cols, part_.p, e.sx,
+                                                                                 e.gate, local);
+      ctx->comm->allgather(part_.p, (size_t)local * cols, gath_.p, ctx->stream);
+      gemvt_combine_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, ctx->stream>>>(gath_.p, cols, 8, x, a);
+      ctx->count(2);
+    } else {
+      const int chunks = rows % 8 == 0 ? 8 : 1;
+      gemvt_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, ctx->stream>>>(a_.p, y, rows, cols, x, a, chunks);
+      ctx->count();
+    }
     ctx->check_launch();
     if (e.seg) seg_dot(ctx, x, x, sol_shape, e.seg, e.gate);
   }
 
  private:
   DevBuf<double> tmp_;
+  DevBuf<double> part_, gath_;  // row shards: local chunk partials, all 8 gathered
 };
 
 Op* make_dense(Ctx* c, size_t rows, size_t cols, const double* a, bool a_on_device,
@@ -196,7 +264,12 @@ Op* make_dense(Ctx* c, size_t rows, size_t cols, const double* a, bool a_on_devi
 
 Op* make_dense_fdot(Ctx* c, size_t nvox, int nsrc, int ndet, const double* gs, const double* gd,
                     size_t sol_row_len) {
-  const size_t rows = (size_t)nsrc * (size_t)ndet;
+  size_t rows = (size_t)nsrc * (size_t)ndet, row0 = 0;
+  if (c->row_sharded()) {  // this rank forms only its rows of the global (s, d) row space
+    require(c->rows_g == (long)rows, MLSQR_EDIM, "row-shard context rows != nsrc * ndet");
+    rows /= (size_t)c->comm->size;
+    row0 = (size_t)c->row0;
+  }
   auto* op = new DenseOp(c, rows, nvox, sol_row_len);
   try {
     DevBuf<double> dgs((size_t)nsrc * nvox), dgd((size_t)ndet * nvox);
@@ -205,7 +278,7 @@ Op* make_dense_fdot(Ctx* c, size_t nvox, int nsrc, int ndet, const double* gs, c
     const unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
     const unsigned gz = (unsigned)((rows + gy - 1) / gy);
     dim3 grd((unsigned)((nvox + 255) / 256), gy, gz);
-    fdot_form_kernel<<<grd, 256, 0, c->stream>>>(dgs.p, dgd.p, nvox, ndet, rows, op->a_.p);
+    fdot_form_kernel<<<grd, 256, 0, c->stream>>>(dgs.p, dgd.p, nvox, ndet, rows, row0, op->a_.p);
     c->count();
     c->check_launch();
     MLSQR_CUDA(cudaStreamSynchronize(c->stream));

@@ -196,7 +196,15 @@ struct Ctx {
   // [zoff, zoff + nz) of a global grid with nzg planes (nzg == 0: not sharded)
   Comm* comm = nullptr;
   long zoff = 0, nzg = 0;
-  bool sharded() const { return comm != nullptr && comm->size > 1; }
+  // row-shard decomposition (dense operators): data-space vectors hold the rows
+  // [row0, row0 + rows_g / P) of a global data space with rows_g rows; the solution space and any
+  // preconditioner are replicated (so sharded() -- the z-slab predicate -- is false)
+  bool row_mode = false;
+  long row0 = 0, rows_g = 0;
+  bool sharded() const { return comm != nullptr && comm->size > 1 && !row_mode; }
+  bool row_sharded() const { return comm != nullptr && comm->size > 1 && row_mode; }
+  // data-space reductions span ranks in both decompositions
+  bool data_distributed() const { return comm != nullptr && comm->size > 1; }
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   uint64_t launches = 0;
@@ -333,6 +341,9 @@ void axpby_epi(Ctx* c, const double* x, double* out, RowShape s, const Epi& e);
 void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k);
 // canonical reduction of this rank's segments of a z-sharded vector: bit-identical to the
 // unsharded reduction (block-aligned tree partials or raw segments are allgathered)
+// dist: the segments are this rank's share of a distributed vector (else: a local / replicated one)
+void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                          double* out, const int* gate, bool dist);
 void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
                           double* out, const int* gate);
 // scratch sizes of reduce_segments_dist

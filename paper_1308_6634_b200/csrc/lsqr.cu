@@ -391,8 +391,11 @@ struct Runner {
   const int* flag(int k) const { return &st->flags[k]; }
   const int* gate_active() const { return flag(0); }
 
-  void reduce(double* seg, size_t nseg, double* out, const int* gate) {
-    reduce_segments_dist(c, seg, nseg, ws->scratch.p, ws->gathered.p, out, gate);
+  // data-space vectors are distributed under z slabs and row shards; solution-space ones
+  // only under z slabs (row shards replicate the solution space)
+  void reduce(double* seg, size_t nseg, double* out, const int* gate, bool data) {
+    reduce_segments_dist(c, seg, nseg, ws->scratch.p, ws->gathered.p, out, gate,
+                         data ? c->data_distributed() : c->sharded());
   }
 
   double* vbuf() const { return pc ? ws->v.p : ws->p.p; }
@@ -403,7 +406,7 @@ struct Runner {
     } else {
       seg_dot(c, ws->p.p, ws->p.p, ws->sol, ws->seg_vp.p, gate);
     }
-    reduce(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate);
+    reduce(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false);
   }
 
   void init(const double* g) {
@@ -414,7 +417,7 @@ struct Runner {
     Epi e;
     e.seg = ws->seg_u.p;
     axpby_epi(c, g, ws->u.p, ws->data, e);
-    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, nullptr);
+    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, nullptr, true);
     fin_beta1_kernel<<<1, 1, 0, c->stream>>>(st, ws->betas.p);
     // p_s = A^T (u_s * su), |p|^2
     Epi eb;
@@ -423,14 +426,14 @@ struct Runner {
     eb.gate = gate_active();
     eb.in_guarded = true;
     op->adjoint(ws->u.p, ws->p.p, eb);
-    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, gate_active());
+    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, gate_active(), false);
     fin_p0_kernel<<<1, 1, 0, c->stream>>>(st);
     precond(gate_active());
     fin_alpha1_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p);
     dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
     init_wq_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
-    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, gate_active());
+    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, gate_active(), false);
     fin_wq0_kernel<<<1, 1, 0, c->stream>>>(st);
     c->count(6);
     c->check_launch();
@@ -448,7 +451,7 @@ struct Runner {
     ea.gate = gate_active();
     ea.in_guarded = true;
     op->apply(vbuf(), ws->u.p, ea);
-    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active());
+    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true);
     fin_beta_kernel<<<1, 1, 0, c->stream>>>(st);
     // K_B: p_s <- A^T(u_s*su) + (-beta)(p_s*sv)
     Epi eb;
@@ -460,7 +463,7 @@ struct Runner {
     eb.gate = flag(1);
     eb.in_guarded = true;
     op->adjoint(ws->u.p, ws->p.p, eb);
-    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1));
+    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1), false);
     fin_p_kernel<<<1, 1, 0, c->stream>>>(st);
     // M^{-1}
     precond(flag(2));
@@ -472,7 +475,7 @@ struct Runner {
       update_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
                                                 ws->sol.len, ws->sol.rows, ws->seg_wq.p);
     }
-    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3));
+    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false);
     if (tau != 0.0 && stop.use_s4) {
       // exact data residual |g - A f| (krylov.cpp:142-144): (A f - g)^2 partials
       Epi er;
@@ -481,7 +484,7 @@ struct Runner {
       er.seg = ws->seg_res.p;
       er.gate = gate_active();
       op->apply(ws->f.p, ws->tmp_rows.p, er);
-      reduce(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active());
+      reduce(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active(), true);
     }
     fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
     c->count(5);

@@ -123,7 +123,12 @@ size_t dist_gather_size(Ctx* c, size_t nseg) {
 
 void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
                           double* out, const int* gate) {
-  if (!c->sharded()) {
+  reduce_segments_dist(c, seg, nseg, scratch, gathered, out, gate, c->sharded());
+}
+
+void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                          double* out, const int* gate, bool dist) {
+  if (!dist || !c->data_distributed()) {
     reduce_segments(c, seg, nseg, scratch, out, gate);
     return;
   }
