@@ -53,6 +53,9 @@ CONFIGS = {
     "c3": dict(workload="C3 3D Perona-Malik deconvolution 128^3 fp64", dims=3, n=128, sigma_px=1.5,
                R=4, phantom="ellipsoids", count=10, semi=(8.0, 40.0), vals=(0.2, 1.0), noise=0.02,
                pen="pm_log", T=0.05, tau=1e-2, K=5, I=40, levels=5, seed=3),
+    "c4": dict(workload="C4 3D fDOT-like dense reconstruction 64^3 x 4096 rows fp64", dims=3, n=64,
+               kind="fdot", ns=64, nd=64, mu=1.0, phantom="ellipsoids", count=3, semi=(6.0, 6.0),
+               vals=(1.0, 1.0), noise=0.01, pen="tv", T=0.01, tau=1e-3, K=8, I=50, levels=4, seed=4, R=0),
     "c5": dict(workload="C5 3D smoothed-TV deblurring 512^3 fp64 (north-star gate)", dims=3, n=512,
                sigma_px=2.0, R=6, phantom="ellipsoids", count=64, semi=(32.0, 160.0),
                vals=(0.2, 1.0), noise=0.01, pen="tv", T=0.01, tau=5e-3, K=10, I=50, levels=5, seed=5),
@@ -72,13 +75,14 @@ def canonical_bytes_per_iter(cfg) -> float:
     """B_iter = 8 (W_A + W_B + W_MG + W_U), kc = 4 coarse sweeps."""
     d = cfg["dims"]
     n = float(cfg["n"] ** d)
-    m = n
+    dense = cfg.get("kind") == "fdot"
+    m = float(cfg["ns"] * cfg["nd"]) if dense else n
     r = 2.0 ** -d
     L = cfg["levels"]
     kc = 4
     nl = [n * r ** l for l in range(L)]
-    W_A = n + 2 * m
-    W_B = m + 2 * n
+    W_A = n + 2 * m + (m * n if dense else 0.0)
+    W_B = m + 2 * n + (m * n if dense else 0.0)
     W_MG = (15 + 5 * d + 2 * r) * sum(nl[:-1]) + kc * (3 + d) * nl[-1]
     W_U = 8 * n
     return 8.0 * (W_A + W_B + W_MG + W_U)
@@ -96,7 +100,9 @@ def class_bytes(cfg, world=1):
     else:
         # unfused: first-from-zero, normal, prolong+sweep, normal
         sweep_words = [(2 + d), (3 + d), (3 + d + r), (3 + d)]
+    m = float(cfg["ns"] * cfg["nd"]) if cfg.get("kind") == "fdot" else n
     return {
+        "dense": 8.0 * (m * n + n + 2 * m),        # A x (or A^T y): the matrix once + the vectors
         "blur": 8.0 * 3 * n,                       # read x, read old, write out (m = n)
         "smooth": 8.0 * n * sum(sweep_words) / len(sweep_words),  # average per level-0 launch
         "update": 8.0 * 8 * n,                     # read f w q v p, write f w q
@@ -271,27 +277,42 @@ def main():
     ctx = mb.Context(local, stream=stream.cuda_stream)
     n = cfg["n"]
     h = 1.0 / n
+    dense = cfg.get("kind") == "fdot"
     if world > 1:
-        # one global problem, z-slab decomposed: rank k owns planes [k n/P, (k+1) n/P)
         from paper_1308_6634_b200 import dist as pdist
-        require3 = cfg["dims"] == 3
-        if not require3:
-            raise SystemExit("multi-GPU slabs need a 3D config (c3 / c5)")
-        z0, nzl = pdist.slab_plan(n, world, levels=cfg["levels"], radius=cfg["R"])[rank]
         ctx.set_comm_nccl(pdist.broadcast_unique_id(dist, rank), rank, world)
-        ctx.set_slab(n, z0)
-    else:
-        z0, nzl = 0, n if cfg["dims"] == 3 else 1
+        if dense:
+            # row shards: rank k owns data rows [k m/P, (k+1) m/P); solution space replicated
+            m_g = cfg["ns"] * cfg["nd"]
+            ctx.set_row_shard(m_g, rank * m_g // world)
+        else:
+            # one global grid in z slabs: rank k owns planes [k n/P, (k+1) n/P)
+            if cfg["dims"] != 3:
+                raise SystemExit("multi-GPU slabs need a 3D config (c3 / c5)")
+            z0, nzl = pdist.slab_plan(n, world, levels=cfg["levels"], radius=cfg["R"])[rank]
+            ctx.set_slab(n, z0)
 
     # ---- inputs resident in HBM
-    shape, taps, f_true, z = make_problem(mb, cfg)
-    if world > 1:
-        plane = n * n
-        f_true = np.ascontiguousarray(f_true[z0 * plane:(z0 + nzl) * plane])
-        z = np.ascontiguousarray(z[z0 * plane:(z0 + nzl) * plane])
-        shape = (n, n, nzl)
+    if dense:
+        shape = (n, n, n)
+        lo, hi = cfg["semi"]
+        vlo, vhi = cfg["vals"]
+        f_true = mb.phantom_ellipsoids3d(n, n, n, cfg["count"], lo, hi, vlo, vhi, cfg["seed"])
+        op = mb.FdotOperator(n, cfg["ns"], cfg["nd"], mu=cfg["mu"], seed=cfg["seed"], ctx=ctx)
+        m_g = cfg["ns"] * cfg["nd"]
+        z = mb.gaussian_noise(cfg["seed"] + 1000, m_g, 1.0)
+        if world > 1:
+            z = np.ascontiguousarray(z[rank * m_g // world:(rank + 1) * m_g // world])
+        taps = []
+    else:
+        shape, taps, f_true, z = make_problem(mb, cfg)
+        if world > 1:
+            plane = n * n
+            f_true = np.ascontiguousarray(f_true[z0 * plane:(z0 + nzl) * plane])
+            z = np.ascontiguousarray(z[z0 * plane:(z0 + nzl) * plane])
+            shape = (n, n, nzl)
+        op = mb.SeparableGaussianBlur(shape, taps=taps, ctx=ctx)
     N = int(np.prod(shape))
-    op = mb.SeparableGaussianBlur(shape, taps=taps, ctx=ctx)
     f_d = torch.from_numpy(f_true).cuda()
     af = op.apply(f_d)
     amax = af.abs().max().reshape(1)
@@ -344,9 +365,10 @@ def main():
     torch.cuda.synchronize()
     cls_ms = {k: ctx.timing(c) for k, c in mb.TCLASS.items()}
     ctx.set_timing(False)
-    cb = {k: v / world for k, v in class_bytes(cfg, world).items()}  # this rank's slab
+    # this rank's share: z slabs split everything; row shards split only the dense operator
+    cb = {k: v / world if (not dense or k == "dense") else v for k, v in class_bytes(cfg, world).items()}
     peak, peak_src = peaks()
-    cands = {"blur": cls_ms["blur"], "smooth": cls_ms["smooth"], "update": cls_ms["update"]}
+    cands = {k: cls_ms[k] for k in ("dense", "blur", "smooth", "update") if cls_ms[k][1] > 0}
     dom = max(cands, key=lambda k: cands[k][0])
     dms, dn = cands[dom]
     achieved = cb[dom] * dn / (dms / 1000.0) / 1e9 if dms > 0 else None
@@ -361,7 +383,7 @@ def main():
     # ---- e2e through the public API with host (pinned) buffers
     e2e = None
     if not args.no_e2e:
-        gh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        gh = torch.empty(op.n_rows, dtype=torch.float64, pin_memory=True)
         gh.copy_(g_d)
         fph = torch.zeros(N, dtype=torch.float64, pin_memory=True)
         foh = torch.empty(N, dtype=torch.float64, pin_memory=True)
@@ -380,7 +402,7 @@ def main():
             t = torch.tensor([secs], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             secs = float(t.item())
-        e2e = {"value": e_iters / secs, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * N * world,
+        e2e = {"value": e_iters / secs, "unit": UNIT, "h2d_bytes_per_step": 8 * (op.n_rows + N) * world,
                "d2h_bytes_per_step": 8 * N * world, "steps": e_steps,
                "path": "mlsqr_outer_advance(ptr_kind=HOST): pinned g, f_prev -> HBM, f -> host, per step"}
 
@@ -399,12 +421,15 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded phantoms + Gaussian noise with BASELINE.json shapes)",
             "config": {"workload": cfg["workload"], "grid": [n] * cfg["dims"], "slab": list(shape),
-                       "taps": len(taps),
+                       "data_rows_local": op.n_rows, "taps": len(taps),
                        "step": f"one lagged-diffusivity outer step = {cfg['I']} MLSQR iterations "
                                f"(A, A^T, one V(2,2) {cfg['levels']}-level cycle each) + D update + R(f)",
-                       "parallelism": "single GPU" if world == 1 else
-                       f"z-slabs x{world}: NCCL ghost planes + allgathered canonical tree partials",
-                       "l2": "no flush needed: every vector (8 B x %d) exceeds the 126 MB L2" % N},
+                       "parallelism": "single GPU" if world == 1 else (
+                           f"row shards x{world}: local A rows, allgathered A^T chunk partials, replicated V-cycle"
+                           if dense else f"z-slabs x{world}: NCCL ghost planes + allgathered canonical tree partials"),
+                       "l2": ("no flush needed: the %.2f GB matrix streamed by every A / A^T exceeds the 126 MB L2"
+                              % (8.0 * op.n_rows * N / 1e9)) if dense else
+                             "no flush needed: every vector (8 B x %d) exceeds the 126 MB L2" % N},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": cb[dom], "traffic_source": traffic_src,
