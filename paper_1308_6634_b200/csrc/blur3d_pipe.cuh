@@ -75,10 +75,15 @@ __device__ __forceinline__ void tma_load3d(double* dst, const CUtensorMap* map, 
       : "memory");
 }
 
+// Persistent: gridDim.x CTAs (one per SM) split the (column tile, z) output work evenly;
+// CTA b owns work items [b W / G, (b+1) W / G) in tile-major, z-minor order, i.e. one
+// to three z segments of consecutive column tiles.  Each segment pays the 2R + 2 phase
+// pipeline fill once.  The TMA ring position (stage, parity) counts every issued plane
+// across segments, and every issued plane is waited for exactly once.
 template <int R, bool TMA>
 __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__ in, double* __restrict__ out,
-                                                      int nx, int ny, int nz, int zchunk, int zoff, int nzg,
-                                                      int zshift, Taps taps, EpiArgs e,
+                                                      int nx, int ny, int nz, int tiles_x, long work, int zoff,
+                                                      int nzg, int zshift, Taps taps, EpiArgs e,
                                                       const __grid_constant__ CUtensorMap map_in,
                                                       const __grid_constant__ CUtensorMap map_old) {
   using C = B3P<R>;
@@ -90,12 +95,14 @@ __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__
   double* sq = xs + 2 * C::XS_DOUBLES;                    // [2][TY][SQP]
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sq + 2 * C::SQ_DOUBLES);
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * C::TX, y0 = blockIdx.y * C::TY;
-  const int z0 = blockIdx.z * zchunk;
-  const int z1 = min(nz, z0 + zchunk);
-  const int zlo = z0 - R, zhi = z1 + R - 1;
   const size_t nxy = (size_t)nx * ny;
   const double sx = e.sx ? *e.sx : 1.0;
+  const double so = e.so ? *e.so : 1.0;
+  const double coef = e.old ? *e.coef : 0.0;
+  const size_t chunks = (size_t)(nx + 31) / 32;
+  const int tx = tid & 31, ty = tid >> 5;
+  const int xr = tid % C::H, xg = tid / C::H;
+  const bool xtask = tid < C::H * C::XG;
 #define TAP(k) taps.t[(k) <= R ? (k) : 2 * R - (k)]
 
   if (TMA && tid == 0) {
@@ -105,157 +112,165 @@ __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__
   }
   __syncthreads();
 
-  auto inside = [&](int zz) { return zz >= zlo && zz <= zhi && zz + zoff >= 0 && zz + zoff < nzg; };
-  // stage q: input plane q and old plane q - R
-  auto issue = [&](int zz) {
-    const int st = (zz - zlo) & (C::NSTAGE - 1);
-    const int zo = zz - R;
-    const bool lin = inside(zz);
-    const bool lold = e.old && zo >= z0 && zo < z1;
-    if (TMA) {
-      if (tid == 0) {  // always arrive, so every stage's phase advances once per use
-        mbar_arrive_expect(bars + st, (lin ? C::IN_BYTES : 0u) + (lold ? C::OLD_BYTES : 0u));
-        if (lin) tma_load3d(tin + st * C::IN_SLOT, &map_in, x0 - R - C::XOFF, y0 - R, zz + zshift, bars + st);
-        if (lold) tma_load3d(olds + st * C::OLD_DOUBLES, &map_old, x0, y0, zo, bars + st);
-      }
-    } else {
-      if (lin) {
-        double* dst = tin + st * C::IN_SLOT;
-        const double* src = in + (size_t)zz * nxy;
-        for (int k = tid; k < C::H * C::W; k += C::THREADS) {
-          const int ly = k / C::W, lx = k - ly * C::W;
-          const int gx = x0 + lx - R, gy = y0 + ly - R;
-          const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-          cp_async8(dst + ly * C::P + lx + C::XOFF, ok ? src + (size_t)gy * nx + gx : in, ok);
-        }
-      }
-      if (lold) {
-        double* dst = olds + st * C::OLD_DOUBLES;
-        const double* src = e.old + (size_t)zo * nxy;
-        for (int k = tid; k < C::TX * C::TY; k += C::THREADS) {
-          const int ly = k >> 5, lx = k & 31;
-          const int gx = x0 + lx, gy = y0 + ly;
-          const bool ok = gx < nx && gy < ny;
-          cp_async8(dst + k, ok ? src + (size_t)gy * nx + gx : in, ok);
-        }
-      }
-      cp_async_commit();
-    }
-  };
-
-  const int tx = tid & 31, ty = tid >> 5;
-  const int xr = tid % C::H, xg = tid / C::H;
-  const bool xtask = tid < C::H * C::XG;
-  const double so = e.so ? *e.so : 1.0;
-  const double coef = e.old ? *e.coef : 0.0;
-  const size_t chunks = (size_t)(nx + 31) / 32;
-  const int gx = x0 + tx, gy0 = y0 + 2 * ty;
-  const bool ok0 = gx < nx && gy0 < ny, ok1 = gx < nx && gy0 + 1 < ny;
-  double* const obase = out + (size_t)gy0 * nx + gx;
   double acc[2][C::NT];
-#pragma unroll
-  for (int o = 0; o < 2; ++o)
-#pragma unroll
-    for (int k = 0; k < C::NT; ++k) acc[o][k] = 0.0;
+  unsigned qbase = 0;  // planes issued by earlier segments (ring position)
+  const long w0 = (long)blockIdx.x * work / gridDim.x, w1 = ((long)blockIdx.x + 1) * work / gridDim.x;
+  for (long w = w0; w < w1;) {
+    const int t = (int)(w / nz);
+    const int z0 = (int)(w % nz);
+    const int z1 = (int)min((long)nz, (long)z0 + (w1 - w));
+    const int bx = t % tiles_x;
+    const int x0 = bx * C::TX, y0 = (t / tiles_x) * C::TY;
+    const int zlo = z0 - R, zhi = z1 + R - 1;
+    auto inside = [&](int zz) { return zz >= zlo && zz <= zhi && zz + zoff >= 0 && zz + zoff < nzg; };
+    auto stage = [&](int zz) { return (qbase + (unsigned)(zz - zlo)) & (C::NSTAGE - 1); };
+    auto parity = [&](int zz) { return ((qbase + (unsigned)(zz - zlo)) >> 2) & 1u; };
+    // stage of plane q: input plane q and old plane q - R
+    auto issue = [&](int zz) {
+      const int st = stage(zz);
+      const int zo = zz - R;
+      const bool lin = inside(zz);
+      const bool lold = e.old && zo >= z0 && zo < z1;
+      if (TMA) {
+        if (zz > zhi) return;  // only planes of this segment take ring stages
+        if (tid == 0) {  // always arrive, so each stage's phase advances once per plane
+          mbar_arrive_expect(bars + st, (lin ? C::IN_BYTES : 0u) + (lold ? C::OLD_BYTES : 0u));
+          if (lin) tma_load3d(tin + st * C::IN_SLOT, &map_in, x0 - R - C::XOFF, y0 - R, zz + zshift, bars + st);
+          if (lold) tma_load3d(olds + st * C::OLD_DOUBLES, &map_old, x0, y0, zo, bars + st);
+        }
+      } else {
+        if (lin) {
+          double* dst = tin + st * C::IN_SLOT;
+          const double* src = in + (size_t)zz * nxy;
+          for (int k = tid; k < C::H * C::W; k += C::THREADS) {
+            const int ly = k / C::W, lx = k - ly * C::W;
+            const int gx = x0 + lx - R, gy = y0 + ly - R;
+            const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+            cp_async8(dst + ly * C::P + lx + C::XOFF, ok ? src + (size_t)gy * nx + gx : in, ok);
+          }
+        }
+        if (lold) {
+          double* dst = olds + st * C::OLD_DOUBLES;
+          const double* src = e.old + (size_t)zo * nxy;
+          for (int k = tid; k < C::TX * C::TY; k += C::THREADS) {
+            const int ly = k >> 5, lx = k & 31;
+            const int gx = x0 + lx, gy = y0 + ly;
+            const bool ok = gx < nx && gy < ny;
+            cp_async8(dst + k, ok ? src + (size_t)gy * nx + gx : in, ok);
+          }
+        }
+        cp_async_commit();  // one group per plane, empty ones included (wait<1> counts them)
+      }
+    };
 
-  issue(zlo);
-  issue(zlo + 1);
-  for (int pb = zlo - 1; pb <= zhi + 1; pb += C::NT) {
+    const int gx = x0 + tx, gy0 = y0 + 2 * ty;
+    const bool ok0 = gx < nx && gy0 < ny, ok1 = gx < nx && gy0 + 1 < ny;
+    double* const obase = out + (size_t)gy0 * nx + gx;
+    __syncthreads();  // the previous segment is done with every buffer
+    issue(zlo);
+    issue(zlo + 1);
+    for (int pb = zlo - 1; pb <= zhi + 1; pb += C::NT) {
 #pragma unroll
-    for (int u = 0; u < C::NT; ++u) {
-      const int p = pb + u;
-      if (p <= zhi + 1) {  // block-uniform
-        // stage p+1 (x-pass input of this phase, old plane of the next) has landed
-        if (TMA) mbar_wait(bars + ((p + 1 - zlo) & (C::NSTAGE - 1)), ((p + 1 - zlo) >> 2) & 1);
-        else cp_async_wait<1>();
-        __syncthreads();  // ... for everyone; phase p-1 is done with every buffer
-        issue(p + 3);
-        const int xz = p + 1;
-        if (xtask && inside(xz)) {
-          const double* row = tin + ((xz - zlo) & (C::NSTAGE - 1)) * C::IN_SLOT + xr * C::P + C::XK * xg;
-          double w[C::WL];
-#pragma unroll
-          for (int j = 0; j < C::WL / 2; ++j) {
-            const double2 q = *reinterpret_cast<const double2*>(row + 2 * j);
-            w[2 * j] = q.x;
-            w[2 * j + 1] = q.y;
+      for (int u = 0; u < C::NT; ++u) {
+        const int p = pb + u;
+        if (p <= zhi + 1) {  // block-uniform
+          // plane p+1 (x-pass input of this phase, old plane of the next) has landed
+          if (TMA) {
+            if (p + 1 <= zhi) mbar_wait(bars + stage(p + 1), parity(p + 1));
+          } else {
+            cp_async_wait<1>();
           }
-          if (e.sx) {
+          __syncthreads();  // ... for everyone; phase p-1 is done with every buffer
+          issue(p + 3);
+          const int xz = p + 1;
+          if (xtask && inside(xz)) {
+            const double* row = tin + stage(xz) * C::IN_SLOT + xr * C::P + C::XK * xg;
+            double wv[C::WL];
 #pragma unroll
-            for (int j = C::XOFF; j < C::XK + 2 * R + C::XOFF; ++j) w[j] = w[j] * sx;
-          }
-          double a[C::XK];
-#pragma unroll
-          for (int o = 0; o < C::XK; ++o) {
-            a[o] = 0.0;
-#pragma unroll
-            for (int k = 0; k < C::NT; ++k) a[o] = fma(TAP(k), w[o + k + C::XOFF], a[o]);
-          }
-          double* xw = xs + ((xz - zlo) & 1) * C::XS_DOUBLES + xr * C::XP + C::XK * xg;
-          *reinterpret_cast<double2*>(xw) = make_double2(a[0], a[1]);
-          *reinterpret_cast<double2*>(xw + 2) = make_double2(a[2], a[3]);
-        }
-        if (p >= zlo && p <= zhi) {
-          double yv0 = 0.0, yv1 = 0.0;
-          if (inside(p)) {
-            const double* xb = xs + ((p - zlo) & 1) * C::XS_DOUBLES + 2 * ty * C::XP + tx;
-            double c[2 + 2 * R];
-#pragma unroll
-            for (int j = 0; j < 2 + 2 * R; ++j) c[j] = xb[j * C::XP];
-#pragma unroll
-            for (int k = 0; k < C::NT; ++k) {
-              yv0 = fma(TAP(k), c[k], yv0);
-              yv1 = fma(TAP(k), c[k + 1], yv1);
+            for (int j = 0; j < C::WL / 2; ++j) {
+              const double2 q = *reinterpret_cast<const double2*>(row + 2 * j);
+              wv[2 * j] = q.x;
+              wv[2 * j + 1] = q.y;
             }
-          }
-          // output zo' = p - R + j takes tap 2R - j; j = 2R starts output p + R
+            if (e.sx) {
 #pragma unroll
-          for (int j = 0; j < C::NT; ++j) {
-            const int s = (u + j) % C::NT;
-            acc[0][s] = fma(TAP(2 * R - j), yv0, j == C::NT - 1 ? 0.0 : acc[0][s]);
-            acc[1][s] = fma(TAP(2 * R - j), yv1, j == C::NT - 1 ? 0.0 : acc[1][s]);
+              for (int j = C::XOFF; j < C::XK + 2 * R + C::XOFF; ++j) wv[j] = wv[j] * sx;
+            }
+            double a[C::XK];
+#pragma unroll
+            for (int o = 0; o < C::XK; ++o) {
+              a[o] = 0.0;
+#pragma unroll
+              for (int k = 0; k < C::NT; ++k) a[o] = fma(TAP(k), wv[o + k + C::XOFF], a[o]);
+            }
+            double* xw = xs + ((xz - zlo) & 1) * C::XS_DOUBLES + xr * C::XP + C::XK * xg;
+            *reinterpret_cast<double2*>(xw) = make_double2(a[0], a[1]);
+            *reinterpret_cast<double2*>(xw + 2) = make_double2(a[2], a[3]);
           }
-          const int zo = p - R;  // complete now (slot u)
-          if (zo >= z0 && zo < z1) {
-            const double* po = olds + ((p - zlo) & (C::NSTAGE - 1)) * C::OLD_DOUBLES + 2 * ty * 32 + tx;
-            double* sqb = sq + ((zo - z0) & 1) * C::SQ_DOUBLES + 2 * ty * C::SQP + tx;
-            double* orow = obase + (size_t)zo * nxy;
-            double v0 = ok0 ? acc[0][u] : 0.0, v1 = ok1 ? acc[1][u] : 0.0;
-            if (e.old) {
-              double o0 = po[0], o1 = po[32];
-              if (e.so) {
-                o0 = o0 * so;
-                o1 = o1 * so;
+          if (p >= zlo && p <= zhi) {
+            double yv0 = 0.0, yv1 = 0.0;
+            if (inside(p)) {
+              const double* xb = xs + ((p - zlo) & 1) * C::XS_DOUBLES + 2 * ty * C::XP + tx;
+              double c[2 + 2 * R];
+#pragma unroll
+              for (int j = 0; j < 2 + 2 * R; ++j) c[j] = xb[j * C::XP];
+#pragma unroll
+              for (int k = 0; k < C::NT; ++k) {
+                yv0 = fma(TAP(k), c[k], yv0);
+                yv1 = fma(TAP(k), c[k + 1], yv1);
               }
-              if (ok0) v0 = v0 + coef * o0;
-              if (ok1) v1 = v1 + coef * o1;
             }
-            if (ok0) orow[0] = v0;
-            if (ok1) orow[nx] = v1;
-            if (e.seg) {
-              sqb[0] = v0 * v0;
-              sqb[C::SQP] = v1 * v1;
+            // output zo' = p - R + j takes tap 2R - j; j = 2R starts output p + R
+#pragma unroll
+            for (int j = 0; j < C::NT; ++j) {
+              const int s = (u + j) % C::NT;
+              acc[0][s] = fma(TAP(2 * R - j), yv0, j == C::NT - 1 ? 0.0 : acc[0][s]);
+              acc[1][s] = fma(TAP(2 * R - j), yv1, j == C::NT - 1 ? 0.0 : acc[1][s]);
+            }
+            const int zo = p - R;  // complete now (slot u)
+            if (zo >= z0 && zo < z1) {
+              const double* po = olds + stage(p) * C::OLD_DOUBLES + 2 * ty * 32 + tx;
+              double* sqb = sq + ((zo - z0) & 1) * C::SQ_DOUBLES + 2 * ty * C::SQP + tx;
+              double* orow = obase + (size_t)zo * nxy;
+              double v0 = ok0 ? acc[0][u] : 0.0, v1 = ok1 ? acc[1][u] : 0.0;
+              if (e.old) {
+                double o0 = po[0], o1 = po[32];
+                if (e.so) {
+                  o0 = o0 * so;
+                  o1 = o1 * so;
+                }
+                if (ok0) v0 = v0 + coef * o0;
+                if (ok1) v1 = v1 + coef * o1;
+              }
+              if (ok0) orow[0] = v0;
+              if (ok1) orow[nx] = v1;
+              if (e.seg) {
+                sqb[0] = v0 * v0;
+                sqb[C::SQP] = v1 * v1;
+              }
             }
           }
-        }
-        // canonical segment partials of the plane completed in the previous phase
-        const int zt = p - R - 1;
-        if (e.seg && ty == C::TREE_WARP && zt >= z0 && zt < z1) {
-          const int gy = y0 + tx;
-          if (gy < ny) {
-            const double* r = sq + ((zt - z0) & 1) * C::SQ_DOUBLES + tx * C::SQP;
-            double v[32];
+          // canonical segment partials of the plane completed in the previous phase
+          const int zt = p - R - 1;
+          if (e.seg && ty == C::TREE_WARP && zt >= z0 && zt < z1) {
+            const int gy = y0 + tx;
+            if (gy < ny) {
+              const double* r = sq + ((zt - z0) & 1) * C::SQ_DOUBLES + tx * C::SQP;
+              double v[32];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const double2 q = *reinterpret_cast<const double2*>(r + 2 * j);
-              v[2 * j] = q.x;
-              v[2 * j + 1] = q.y;
+              for (int j = 0; j < 16; ++j) {
+                const double2 q = *reinterpret_cast<const double2*>(r + 2 * j);
+                v[2 * j] = q.x;
+                v[2 * j + 1] = q.y;
+              }
+              e.seg[((size_t)zt * ny + gy) * chunks + bx] = tree32_serial(v);
             }
-            e.seg[((size_t)zt * ny + gy) * chunks + blockIdx.x] = tree32_serial(v);
           }
         }
       }
     }
+    qbase += (unsigned)(zhi - zlo + 1);
+    w += z1 - z0;
   }
 #undef TAP
 }
@@ -326,7 +341,9 @@ static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int
     MLSQR_CUDA(cudaFuncSetAttribute(blur3d_pipe<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
+  const int tiles_x = (nx + C::TX - 1) / C::TX, tiles_y = (ny + C::TY - 1) / C::TY;
+  const long work = (long)tiles_x * tiles_y * nz;
+  const unsigned grid = (unsigned)(work < c->sm_count ? work : c->sm_count);  // persistent: one CTA per SM
   const bool sh = c->sharded();
   const int zoff = sh ? (int)c->zoff : 0, nzg = sh ? (int)c->nzg : nz;
   // z-sharded inputs carry R ghost planes on either side (guard zones): map them too
@@ -335,13 +352,12 @@ static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int
   bool tma = tensor_map3d(&mi, in - (size_t)zshift * nx * ny, nx, ny, nz + 2 * zshift, C::P, C::H);
   if (tma && a.old) tma = tensor_map3d(&mo, a.old, nx, ny, nz, C::TX, C::TY);
   if (getenv("MLSQR_BLUR_NOTMA")) tma = false;
-  if (getenv("MLSQR_BLUR_DEBUG")) fprintf(stderr, "blur3d_pipe R=%d tma=%d P=%d H=%d smem=%zu\n", R, (int)tma, C::P, C::H, C::SMEM);
   if (tma)
-    blur3d_pipe<R, true><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, zshift, t,
-                                                                  a, mi, mo);
+    blur3d_pipe<R, true><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, work, zoff, nzg,
+                                                                   zshift, t, a, mi, mo);
   else
-    blur3d_pipe<R, false><<<grd, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, zshift, t,
-                                                                   a, mi, mo);
+    blur3d_pipe<R, false><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, work, zoff, nzg,
+                                                                    zshift, t, a, mi, mo);
   c->count();
 }
 
