@@ -75,15 +75,16 @@ __device__ __forceinline__ void tma_load3d(double* dst, const CUtensorMap* map, 
       : "memory");
 }
 
-// Persistent: gridDim.x CTAs (one per SM) split the (column tile, z) output work evenly;
-// CTA b owns work items [b W / G, (b+1) W / G) in tile-major, z-minor order, i.e. one
-// to three z segments of consecutive column tiles.  Each segment pays the 2R + 2 phase
-// pipeline fill once.  The TMA ring position (stage, parity) counts every issued plane
-// across segments, and every issued plane is waited for exactly once.
+// Persistent: gridDim.x CTAs (one per SM) take work items round-robin; item k is column
+// tile k % T of z chunk k / T (zchunk planes).  CTAs running at the same time therefore
+// work on neighbouring tiles at the same depth, so the x/y halo re-reads hit L2, and each
+// item pays the 2R + 2 phase pipeline fill once (the host picks zchunk to minimise
+// waves x phases).  The TMA ring position (stage, parity) counts every issued plane
+// across items, and every issued plane is waited for exactly once.
 template <int R, bool TMA>
 __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__ in, double* __restrict__ out,
-                                                      int nx, int ny, int nz, int tiles_x, long work, int zoff,
-                                                      int nzg, int zshift, Taps taps, EpiArgs e,
+                                                      int nx, int ny, int nz, int tiles_x, int tiles, int zchunk,
+                                                      int items, int zoff, int nzg, int zshift, Taps taps, EpiArgs e,
                                                       const __grid_constant__ CUtensorMap map_in,
                                                       const __grid_constant__ CUtensorMap map_old) {
   using C = B3P<R>;
@@ -114,11 +115,12 @@ __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__
 
   double acc[2][C::NT];
   unsigned qbase = 0;  // planes issued by earlier segments (ring position)
-  const long w0 = (long)blockIdx.x * work / gridDim.x, w1 = ((long)blockIdx.x + 1) * work / gridDim.x;
-  for (long w = w0; w < w1;) {
-    const int t = (int)(w / nz);
-    const int z0 = (int)(w % nz);
-    const int z1 = (int)min((long)nz, (long)z0 + (w1 - w));
+  // (a contiguous tile-major split needs 8% fewer phases but loses the halo L2 reuse: +50%
+  //  DRAM traffic, more power, lower clocks under the power cap -- 94.5 vs 96.2 it/s at C5)
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int t = item % tiles;
+    const int z0 = (item / tiles) * zchunk;
+    const int z1 = min(nz, z0 + zchunk);
     const int bx = t % tiles_x;
     const int x0 = bx * C::TX, y0 = (t / tiles_x) * C::TY;
     const int zlo = z0 - R, zhi = z1 + R - 1;
@@ -270,7 +272,6 @@ __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__
       }
     }
     qbase += (unsigned)(zhi - zlo + 1);
-    w += z1 - z0;
   }
 #undef TAP
 }
@@ -342,8 +343,21 @@ static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int
     attr = true;
   }
   const int tiles_x = (nx + C::TX - 1) / C::TX, tiles_y = (ny + C::TY - 1) / C::TY;
-  const long work = (long)tiles_x * tiles_y * nz;
-  const unsigned grid = (unsigned)(work < c->sm_count ? work : c->sm_count);  // persistent: one CTA per SM
+  const int tiles = tiles_x * tiles_y;
+  // z chunk minimising (items per CTA) x (phases per item) on one CTA per SM
+  int zck = nz;
+  long best = -1;
+  for (int zc = 1; zc <= nz; ++zc) {
+    const long items = (long)tiles * ((nz + zc - 1) / zc);
+    const long g = items < c->sm_count ? items : c->sm_count;
+    const long cost = (items + g - 1) / g * (zc + 2 * R + 2);
+    if (best < 0 || cost < best) {
+      best = cost;
+      zck = zc;
+    }
+  }
+  const int items = tiles * ((nz + zck - 1) / zck);
+  const unsigned grid = (unsigned)(items < c->sm_count ? items : c->sm_count);  // persistent: one CTA per SM
   const bool sh = c->sharded();
   const int zoff = sh ? (int)c->zoff : 0, nzg = sh ? (int)c->nzg : nz;
   // z-sharded inputs carry R ghost planes on either side (guard zones): map them too
@@ -353,11 +367,11 @@ static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int
   if (tma && a.old) tma = tensor_map3d(&mo, a.old, nx, ny, nz, C::TX, C::TY);
   if (getenv("MLSQR_BLUR_NOTMA")) tma = false;
   if (tma)
-    blur3d_pipe<R, true><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, work, zoff, nzg,
-                                                                   zshift, t, a, mi, mo);
+    blur3d_pipe<R, true><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, tiles, zck,
+                                                                   items, zoff, nzg, zshift, t, a, mi, mo);
   else
-    blur3d_pipe<R, false><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, work, zoff, nzg,
-                                                                    zshift, t, a, mi, mo);
+    blur3d_pipe<R, false><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, tiles, zck,
+                                                                    items, zoff, nzg, zshift, t, a, mi, mo);
   c->count();
 }
 
