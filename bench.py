@@ -143,7 +143,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,enforced.power.limit")
 
     def __init__(self, device: int):
         self.device = device
@@ -164,7 +164,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
+            if len(parts) == 8:
                 self.rows.append(parts)
 
     def __exit__(self, *a):
@@ -182,8 +182,11 @@ class ClockSampler:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        def num(k):
+            v = [float(r[k]) for r in self.rows if r[k].replace(".", "").isdigit()]
+            return statistics.median(v) if v else None
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "power_w": num(6), "power_limit_w": num(7)}
 
 
 def cpu_reference_rate(cfg, iters: int, warm: int, threads_note: str):

@@ -62,6 +62,14 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
     }
   }
   for (int z = z0; z < z1; ++z, i += nxy) {
+    if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
+      const long j = i + 3 * nxy;
+      prefetch_l2(b + j);
+      prefetch_l2(cx + j);
+      prefetch_l2(cy + j);
+      prefetch_l2(cz + j);
+      if (MODE != kFirst) prefetch_l2(x + j + nxy);
+    }
     // prefetch the streams of plane z+1 (plane-uniform condition)
     double bn = 0.0, cxn = 0.0, cyn = 0.0, czn = 0.0, xnn = 0.0;
     if (z + 1 < z1) {
@@ -166,6 +174,14 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
   const bool owner = ok && (tx % 2 == 0) && (D < 2 || ty % 2 == 0);
   double s = 0.0;
   for (int z = z0; z < z1; ++z, i += nxy) {
+    if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
+      const long j = i + 3 * nxy;
+      prefetch_l2(b + j);
+      prefetch_l2(cx + j);
+      prefetch_l2(cy + j);
+      prefetch_l2(cz + j);
+      prefetch_l2(x + j + nxy);
+    }
     double bn = 0.0, cxn = 0.0, cyn = 0.0, czn = 0.0, xnn = 0.0;
     if (z + 1 < z1) {
       bn = b[i + nxy];

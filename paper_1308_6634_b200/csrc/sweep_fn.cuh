@@ -24,6 +24,8 @@ constexpr int THREADS = 32 * WARPS;
 constexpr int MINB = 2;  // resident blocks per SM (80 registers)
 }  // namespace fn
 
+constexpr int kFnL2Ahead = 2;  // L2 prefetch distance beyond the register prefetch (planes)
+
 struct FnPlane {
   double b, cx, cxm, cy, cym, cz;
 };
@@ -106,6 +108,13 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
   int slot = 0;  // ring slot of plane z
   for (int z = z0; z < z1; ++z) {
     FnPlane f = fn_load(L, b, on(z + 2), idx(z + 2), nx);  // prefetch
+    if (on(z + 2 + kFnL2Ahead)) {
+      const long i = idx(z + 2 + kFnL2Ahead);
+      prefetch_l2(b + i);
+      prefetch_l2(L.cx + i);
+      prefetch_l2(L.cy + i);
+      prefetch_l2(L.cz + i);
+    }
     const double dn = fn_diag(n, c.cz, eps);
     const double x1n = first(n, dn, on(z + 1));
     const int ns = slot == 2 ? 0 : slot + 1;
