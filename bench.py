@@ -200,6 +200,32 @@ def cpu_reference_rate(cfg, iters: int, warm: int, threads_note: str):
     n, d = cfg["n"], cfg["dims"]
     shape = (n,) * d
     N = n ** d
+    dense = cfg.get("kind") == "fdot"
+    if dense:
+        # C4: the reference's own DenseOperator (linop.cpp:64-84) over the fDOT-like matrix
+        _, _, a = orc.fdot(n, cfg["ns"], cfg["nd"], cfg["mu"], cfg["seed"])
+        lo, hi = cfg["semi"]
+        vlo, vhi = cfg["vals"]
+        f = orc.ellipsoids3d(n, n, n, cfg["count"], lo, hi, vlo, vhi, cfg["seed"])
+        od = ref.op_dense(a)
+        M = a.shape[0]
+        af = ref.apply(od, f, M)
+        del f
+        g = af + orc.gauss(cfg["seed"] + 1000, M, cfg["noise"] * float(np.abs(af).max()))
+        del af
+        grid = orc.grid(d, shape, 1.0 / n)
+        cx, cy, cz = orc.edge_coeffs(grid, np.zeros(N), cfg["pen"], cfg["T"])
+        eps = 1e-8 * orc.max_diag(grid, cx, cy, cz)
+        mg = orc.vcycle(grid, cfg["levels"])
+        mg.set(cx, cy, cz, eps)
+        md = ref.map_callback(N, orc.solve_cb, mg.h)
+        with pinned_core() as core:
+            secs, done, _ = ref.mlsqr_timed(od, md, g, cfg["tau"], iters, warm, N)
+        timed = done - warm
+        return {"value": timed / secs if secs > 0 else None, "seconds": secs, "iterations": timed,
+                "sample": f"first outer step of {cfg['workload']}: reference mlsqr + reference DenseOperator "
+                          f"(oracle/_ref) iterations {warm + 1}..{done} at full size, V-cycle = oracle restatement; "
+                          f"{threads_note}; {core}"}
     if cfg["phantom"] == "rects":
         f = orc.rects2d(n, n, cfg["count"], cfg["seed"])
     elif cfg["phantom"] == "shapes":
@@ -222,12 +248,43 @@ def cpu_reference_rate(cfg, iters: int, warm: int, threads_note: str):
     del cx, cy, cz
     od = ref.op_callback(N, N, orc.apply_cb, orc.adjoint_cb, op.h)
     md = ref.map_callback(N, orc.solve_cb, mg.h)
-    secs, done, _ = ref.mlsqr_timed(od, md, g, cfg["tau"], iters, warm, N)
+    with pinned_core() as core:
+        secs, done, _ = ref.mlsqr_timed(od, md, g, cfg["tau"], iters, warm, N)
     timed = done - warm
     return {"value": timed / secs if secs > 0 else None, "seconds": secs, "iterations": timed,
             "sample": f"first outer step of {cfg['workload']}: reference mlsqr (oracle/_ref) iterations "
                       f"{warm + 1}..{done} at full size, init + {warm} warm-up iteration(s) excluded; "
-                      f"operators = oracle's restated {d}D blur + V-cycle (the reference has none); {threads_note}"}
+                      f"operators = oracle's restated {d}D blur + V-cycle (the reference has none); {threads_note}; "
+                      f"{core}"}
+
+
+class pinned_core:
+    """Pin this process to one host core for the CPU reference timing (the reference
+    has no threading, so one core is the reference); reports the core, nproc and the CPU model."""
+
+    def __enter__(self):
+        self.old = None
+        core = 0
+        try:
+            self.old = os.sched_getaffinity(0)
+            core = min(self.old)
+            os.sched_setaffinity(0, {core})
+        except Exception:
+            pass
+        model = "unknown CPU"
+        try:
+            with open("/proc/cpuinfo") as fh:
+                model = next(l.split(":", 1)[1].strip() for l in fh if l.startswith("model name"))
+        except Exception:
+            pass
+        return f"pinned to core {core} of nproc={os.cpu_count()} ({model})"
+
+    def __exit__(self, *a):
+        if self.old:
+            try:
+                os.sched_setaffinity(0, self.old)
+            except Exception:
+                pass
 
 
 def reference_arm(args, cfg):
@@ -241,7 +298,7 @@ def reference_arm(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": r["iterations"], "warmup": warm, "ms_per_step": 1000.0 * r["seconds"] / max(1, r["iterations"]),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; BASELINE.json shapes)",
         "config": {"workload": cfg["workload"], "step": "one reference LSQR iteration (A, A^T, one V-cycle)"},
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "reference", "sample": r["sample"]},
