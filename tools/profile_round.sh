@@ -13,7 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   -c 600 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
   > $O/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
 # one full capture per hot kernel, aimed at a level-0 launch of the 512^3 driver:
-#   blur: 5th launch (inside mlsqr, with the xpby/norm epilogue); sweep_fn: 2nd V-cycle's level 0;
+#   blur: 6th launch (mlsqr iteration 1's K_A, with the xpby/norm epilogue); sweep_fn: 2nd V-cycle's level 0;
 #   prolong sweep <3,2>: levels 3,2,1,0 -> 4th; normal sweep <3,1>: coarsest x2, levels 3..0 -> 6th;
 #   restrict: 2nd V-cycle's level 0 (5th); update: first.
 cap() {  # name regex skip
@@ -21,9 +21,9 @@ cap() {  # name regex skip
     -k "regex:$2" -s $3 -c 1 -o $O/${TAG}_full_$1 python profiles/kernel_driver.py --reps 2 --iters 2 \
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
-cap blur 'blur3d_pipe' 4
+cap blur 'blur3d_pipe' 5
 cap sweep_fn 'sweep_fn_kernel' 5
-cap sweep_prolong 'sweep_zm_kernel<3, 2>' 3
-cap sweep_normal 'sweep_zm_kernel<3, 1>' 5
+cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2>' 3
+cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1>' 5
 cap restrict 'restrict_zm_kernel' 4
 cap update 'update_kernel' 0
