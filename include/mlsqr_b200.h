@@ -189,6 +189,15 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
                      double* f, mlsqr_iter_rec* trace, double* alphas, double* betas,
                      mlsqr_solve_info* info, int ptr_kind);
 
+/* cg_normal (krylov.hpp:116-122, krylov.cpp:551-628): CG on (A^T A + tau M) f = A^T g, the
+ * unpriorconditioned baseline of the paper's comparison.  M is the level-0 operator of the
+ * V-cycle map m (as set by mlsqr_vcycle_set_coefficients / _update; m may be NULL when
+ * tau == 0).  Trace rows follow the reference: exact res_data, s2 = |r_k| / |r_0|, NaN
+ * anorm/cond estimates; no bidiagonal entries.  MLSQR_EBREAKDOWN on nonpositive curvature. */
+int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau,
+                          const mlsqr_stop* stop, double* f, mlsqr_iter_rec* trace,
+                          mlsqr_solve_info* info, int ptr_kind);
+
 /* ---- lagged-diffusivity outer loop (outer.hpp:13-62) --------------------- */
 typedef struct {            /* OuterConfig (outer.hpp:13-28) with a V-cycle M^{-1} */
   double tau;

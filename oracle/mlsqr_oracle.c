@@ -1444,3 +1444,97 @@ int orc_map_solve_cb(void* m, const double* p, double* v) {
   orc_map_solve((const orc_map*)m, p, v);
   return 0;
 }
+
+/* ======================================================================== */
+/* cg_normal (krylov.cpp:551-628)                                            */
+/* ======================================================================== */
+int orc_cg_normal(const orc_linop* a, const orc_grid* gr, const double* cx, const double* cy,
+                  const double* cz, double eps, double tau, const double* g, const orc_stop* stop,
+                  double* f_out, orc_iter_rec* trace, orc_solve_info* info) {
+  orc_solve_info dummy;
+  if (!info) info = &dummy;
+  memset(info, 0, sizeof(*info));
+  if (stop_validate(stop)) return ORC_EINVAL;
+  if (!(tau >= 0.0)) return ORC_EINVAL;
+  const size_t n = a->cols, m = a->rows;
+  if (gr->nx * gr->ny * gr->nz != n) return ORC_EDIM;
+  const size_t Ls = a->sol_len, Ld = a->data_len;
+  const double nan = NAN;
+  int status = ORC_OK;
+  double* x = (double*)calloc(n, sizeof(double));
+  double* b = (double*)malloc(sizeof(double) * n);
+  double* r = (double*)malloc(sizeof(double) * n);
+  double* d = (double*)malloc(sizeof(double) * n);
+  double* q = (double*)malloc(sizeof(double) * n);
+  double* mx = (double*)malloc(sizeof(double) * n);
+  double* tr = (double*)malloc(sizeof(double) * m);
+  orc_linop_adjoint(a, g, b); /* b = A^T g */
+  memcpy(r, b, sizeof(double) * n);
+  memcpy(d, r, sizeof(double) * n);
+  double rho = dotL(r, r, n, Ls);
+  const double nres0 = sqrt(rho);
+  info->stop_reason = ORC_STOP_MAX_ITERS;
+  if (nres0 == 0.0) {
+    info->stop_reason = ORC_STOP_BREAKDOWN;
+    goto done;
+  }
+  for (int iter = 1; iter <= stop->max_iters; ++iter) {
+    /* q = (A^T A + tau M) d */
+    orc_linop_apply(a, d, tr);
+    orc_linop_adjoint(a, tr, q);
+    if (tau > 0.0) {
+      orc_m_apply(gr, cx, cy, cz, eps, d, mx);
+      axpy(tau, mx, q, n);
+    }
+    const double curv = dotL(d, q, n, Ls);
+    if (!(curv > 0.0)) {
+      status = ORC_EBREAKDOWN;
+      info->breakdown_iteration = iter;
+      goto done;
+    }
+    const double gamma = rho / curv;
+    axpy(gamma, d, x, n);
+    axpy(-gamma, q, r, n);
+    const double rho_next = dotL(r, r, n, Ls);
+
+    orc_iter_rec row;
+    memset(&row, 0, sizeof(row));
+    row.iteration = iter;
+    /* exact_data_residual: distance(g, A x) (krylov.cpp:110-123) */
+    orc_linop_apply(a, x, tr);
+    for (size_t i = 0; i < m; ++i) tr[i] = g[i] - tr[i];
+    row.res_data = sqrt(dotL(tr, tr, m, Ld));
+    row.res_data_exact = 1;
+    if (tau > 0.0) {
+      orc_m_apply(gr, cx, cy, cz, eps, x, mx); /* SparseSpd::quadratic_form = sum x_i (Mx)_i */
+      row.res_damped = sqrt(row.res_data * row.res_data + tau * dotL(x, mx, n, Ls));
+    } else {
+      row.res_damped = row.res_data;
+    }
+    row.s2_value = sqrt(rho_next) / nres0;
+    row.anorm_est = nan;
+    row.cond_est = nan;
+    row.xnorm_est = nrm2L(x, n, Ls);
+    if (trace) trace[iter - 1] = row;
+    info->iterations = iter;
+    if (stop->use_s4 && row.res_data <= stop->eta * stop->delta) {
+      info->stop_reason = ORC_STOP_S4;
+      break;
+    }
+    if (stop->use_s2 && row.s2_value <= stop->atol) {
+      info->stop_reason = ORC_STOP_S2;
+      break;
+    }
+    if (rho_next == 0.0) {
+      info->stop_reason = ORC_STOP_BREAKDOWN;
+      break;
+    }
+    if (iter >= stop->max_iters) break;
+    xpby(r, rho_next / rho, d, n);
+    rho = rho_next;
+  }
+done:
+  if (f_out) memcpy(f_out, x, sizeof(double) * n);
+  free(x); free(b); free(r); free(d); free(q); free(mx); free(tr);
+  return status;
+}

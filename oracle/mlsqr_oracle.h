@@ -133,6 +133,13 @@ int orc_mlsqr(const orc_linop* a, const orc_map* msolver, const double* g, doubl
 int orc_lsqr(const orc_linop* a, const double* g, double tau, const orc_stop* stop,
              double* f_out, orc_iter_rec* trace, double* alphas, double* betas,
              double* snapshots, orc_solve_info* info);
+/* cg_normal (krylov.cpp:551-628): CG on the normal equation (A^T A + tau M) f = A^T g, the
+ * unpriorconditioned baseline.  M = the edge operator (cx, cy, cz) + eps I on grid gr, applied
+ * in CSR row order (sparse.cpp:65-74); its quadratic form is x . (M x) (sparse.cpp:82-93).
+ * Returns ORC_EBREAKDOWN (info->breakdown_iteration) on nonpositive curvature. */
+int orc_cg_normal(const orc_linop* a, const orc_grid* gr, const double* cx, const double* cy,
+                  const double* cz, double eps, double tau, const double* g, const orc_stop* stop,
+                  double* f_out, orc_iter_rec* trace, orc_solve_info* info);
 
 /* ---- lagged-diffusivity outer loop (outer.cpp:31-100) with a V-cycle M^{-1} ---- */
 typedef struct {

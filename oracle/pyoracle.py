@@ -144,6 +144,8 @@ class Oracle:
         L.orc_map_solve.argtypes = [C.c_void_p, dp, dp]
         L.orc_mlsqr.argtypes = [C.c_void_p, C.c_void_p, dp, C.c_double, C.POINTER(Stop), dp,
                                 C.POINTER(IterRec), dp, dp, dp, C.POINTER(SolveInfo)]
+        L.orc_cg_normal.argtypes = [C.c_void_p, C.POINTER(Grid), dp, dp, dp, C.c_double, C.c_double, dp,
+                                    C.POINTER(Stop), dp, C.POINTER(IterRec), C.POINTER(SolveInfo)]
         L.orc_lsqr.argtypes = [C.c_void_p, dp, C.c_double, C.POINTER(Stop), dp,
                                C.POINTER(IterRec), dp, dp, dp, C.POINTER(SolveInfo)]
         L.orc_nonlinear.argtypes = [C.c_void_p, dp, C.POINTER(Grid), C.POINTER(OuterCfg), dp,
@@ -304,6 +306,21 @@ class Oracle:
                         info.breakdown_iteration,
                         snap.reshape(k, n)[:info.iterations] if snapshots else None)
 
+    def cg_normal(self, op, grid, cx, cy, cz, eps, tau, g, st):
+        """orc_cg_normal (krylov.cpp:551-628); M = edge operator (cx, cy, cz) + eps I."""
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        k = st.max_iters
+        f = np.zeros(op.cols)
+        tr = (IterRec * k)()
+        info = SolveInfo()
+        z = np.zeros(op.cols)
+        cy = z if cy is None else cy
+        cz = z if cz is None else cz
+        status = self.lib.orc_cg_normal(op.h, C.byref(grid), _ptr(cx), _ptr(cy), _ptr(cz), eps, tau, _ptr(g),
+                                        C.byref(st), _ptr(f), tr, C.byref(info))
+        return SolveOut(f, info.iterations, STOP_NAMES[info.stop_reason], np.zeros(0), np.zeros(0),
+                        _trace_list(tr, info.iterations), status, info.breakdown_iteration, None)
+
     def nonlinear(self, op, g, grid, *, tau, pen, T, inner_stop, inner_cap, max_outer,
                   threshold=0.0, epsilon=-1.0, levels=3, nu_pre=2, nu_post=2, coarse_sweeps=4,
                   omega=2.0 / 3.0, keep=False):
@@ -442,6 +459,9 @@ class Reference:
         L.ref_gauss_fill.argtypes = [C.c_uint64, C.c_size_t, C.c_double, dp]
         L.ref_mlsqr.argtypes = [C.POINTER(RefOp), C.POINTER(RefMap), dp, C.c_double, C.POINTER(Stop),
                                 C.c_int, dp, C.POINTER(IterRec), dp, dp, dp, C.POINTER(SolveInfo)]
+        L.ref_cg_normal.argtypes = [C.POINTER(RefOp), C.c_int, C.c_size_t, C.c_size_t, C.c_double, dp, C.c_int,
+                                    C.c_double, C.c_double, C.c_double, dp, C.POINTER(Stop), dp,
+                                    C.POINTER(IterRec), C.POINTER(SolveInfo)]
         L.ref_lsqr.argtypes = [C.POINTER(RefOp), dp, C.c_double, C.POINTER(Stop), C.c_int, dp,
                                C.POINTER(IterRec), dp, dp, dp, C.POINTER(SolveInfo)]
         L.ref_solve_nonlinear.argtypes = [C.POINTER(RefOp), dp, C.c_int, C.c_size_t, C.c_size_t,
@@ -561,6 +581,19 @@ class Reference:
                         be[:info.n_betas].copy(), _trace_list(tr, info.iterations), status,
                         info.breakdown_iteration,
                         snap.reshape(k, cols)[:info.iterations] if snapshots else None)
+
+    def cg_normal(self, od, dims, shape, h, fM, pen, T, eps, tau, g, st, cols):
+        """The reference's own cg_normal with M assembled at fM (eps < 0: auto shift)."""
+        nx, ny = (list(shape) + [1])[:2]
+        k = st.max_iters
+        f = np.zeros(cols)
+        tr = (IterRec * k)()
+        info = SolveInfo()
+        status = self.lib.ref_cg_normal(C.byref(od), dims, nx, ny, h, _ptr(np.ascontiguousarray(fM)),
+                                        PEN.get(pen, pen), T, eps, tau, _ptr(np.ascontiguousarray(g)),
+                                        C.byref(st), _ptr(f), tr, C.byref(info))
+        return SolveOut(f, info.iterations, STOP_NAMES[info.stop_reason], np.zeros(0), np.zeros(0),
+                        _trace_list(tr, info.iterations), status, info.breakdown_iteration, None)
 
     def mlsqr_timed(self, od, md, g, tau, iters, warm, cols):
         """Reference mlsqr for warm+iters iterations; returns (seconds of the last

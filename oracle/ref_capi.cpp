@@ -327,6 +327,25 @@ void ref_gauss_fill(uint64_t seed, size_t n, double stddev, double* out) {
   s.fill(std::span<double>(out, n), stddev);
 }
 
+// The reference's own cg_normal (krylov.cpp:551-628): CG on (A^T A + tau M) f = A^T g, with M
+// assembled at fM (diffusion.cpp:27-87) and shifted by eps (< 0: auto shift).
+int ref_cg_normal(const ref_op_desc* od, int dims, size_t nx, size_t ny, double h, const double* fM,
+                  int pen_kind, double T, double eps, double tau, const double* g, const ref_stop* stop,
+                  double* f, ref_iter_rec* trace, ref_solve_info* info) {
+  if (info) std::memset(info, 0, sizeof(*info));
+  return guarded(
+      [&] {
+        auto op = make_op(od);
+        const Grid grid = make_grid(dims, nx, ny, h);
+        SparseSpd m = assemble_m(grid, std::span<const double>(fM, grid.num_nodes()),
+                                 make_spec(pen_kind, T), 0.0);
+        m = m.with_shift(eps >= 0.0 ? eps : auto_shift(m));
+        const auto r = mlsqr::cg_normal(*op, m, tau, std::span<const double>(g, op->n_rows()), make_stop(stop));
+        export_result(r, op->n_cols(), f, trace, nullptr, nullptr, nullptr, info);
+      },
+      info);
+}
+
 int ref_mlsqr(const ref_op_desc* od, const ref_map_desc* md, const double* g, double tau,
               const ref_stop* stop, int snapshots_on, double* f, ref_iter_rec* trace,
               double* alphas, double* betas, double* snapshots, ref_solve_info* info) {

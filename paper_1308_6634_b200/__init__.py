@@ -146,6 +146,8 @@ SIGNATURES = {
                               C.c_void_p, C.POINTER(_IterRec), dp, dp, C.POINTER(_Info), C.c_int]),
     "mlsqr_lsqr_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop), C.c_void_p,
                                    C.POINTER(_IterRec), dp, dp, C.POINTER(_Info), C.c_int]),
+    "mlsqr_cg_normal_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop),
+                                        C.c_void_p, C.POINTER(_IterRec), C.POINTER(_Info), C.c_int]),
     "mlsqr_nonlinear_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_size_t, C.c_size_t,
                                         C.c_size_t, C.c_double, C.POINTER(_OuterCfg), C.c_void_p,
                                         C.POINTER(_OuterStep), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -588,7 +590,7 @@ class SolveResult:
 
 
 def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: StoppingConfig,
-         f_out=None) -> SolveResult:
+         f_out=None, cgn: bool = False) -> SolveResult:
     stop.validate()
     if not tau >= 0.0:
         raise ValueError("tau must be nonnegative")
@@ -610,7 +612,10 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
         f = np.zeros(op.n_cols) if f_out is None else f_out
         fptr = C.c_void_p(f.ctypes.data)
     sc = stop._c()
-    if pc is None:
+    if cgn:
+        st = lib().mlsqr_cg_normal_solve(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
+                                         C.byref(info), kind)
+    elif pc is None:
         st = lib().mlsqr_lsqr_solve(op.h, gp, tau, C.byref(sc), fptr, tr, _ptr(al), _ptr(be), C.byref(info), kind)
     else:
         st = lib().mlsqr_solve(op.h, pc.h, gp, tau, C.byref(sc), fptr, tr, _ptr(al), _ptr(be), C.byref(info), kind)
@@ -630,6 +635,16 @@ def mlsqr(a: LinearOperator, msolver: SpdMap, g, tau: float, stop: StoppingConfi
 def lsqr(a: LinearOperator, g, tau: float, stop: StoppingConfig, f_out=None) -> SolveResult:
     """Damped LSQR (krylov.hpp:80-87)."""
     return _run(a, None, g, tau, stop, f_out)
+
+
+def cg_normal(a: LinearOperator, m: Optional["VCycleMap"], tau: float, g, stop: StoppingConfig,
+              f_out=None) -> SolveResult:
+    """CG on the normal equation (A^T A + tau M) f = A^T g (krylov.hpp:116-122), the
+    unpriorconditioned baseline.  M is the level-0 operator of the V-cycle map `m` (None when
+    tau == 0).  Argument order follows the reference: (a, m, tau, g, stop)."""
+    if m is not None and not isinstance(m, VCycleMap):
+        raise ValueError("cg_normal's M comes from a VCycleMap (its level-0 edge operator)")
+    return _run(a, m, g, tau, stop, f_out, cgn=True)
 
 
 # ---------------------------------------------------------------------------

@@ -481,6 +481,30 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
   return run_solve(op, nullptr, g, tau, stop, f, trace, alphas, betas, info, ptr_kind, true);
 }
 
+int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau, const mlsqr_stop* stop,
+                          double* f, mlsqr_iter_rec* trace, mlsqr_solve_info* info, int kind) {
+  int bd_iter = 0;
+  if (info) std::memset(info, 0, sizeof(*info));
+  const int st = guard([&] {
+    require(op && stop, MLSQR_EINVAL, "operator and stopping config are required");
+    require(m == nullptr || m->vc != nullptr, MLSQR_EINVAL, "cg_normal's M comes from a V-cycle map");
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    In gin(c, g, o->rows, kind);
+    Out fout(c, f, o->cols, kind);
+    try {
+      solve_cg_normal(o, m ? m->vc : nullptr, gin.d, tau, *stop, fout.d, trace, info);
+    } catch (const Error& e) {
+      if (e.code == MLSQR_EBREAKDOWN) bd_iter = e.iteration;
+      throw;
+    }
+    fout.finish();
+  });
+  if (st == MLSQR_EBREAKDOWN && info) info->breakdown_iteration = bd_iter;
+  return st;
+}
+
 int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, size_t ny,
                           size_t nz, double h, const mlsqr_outer_cfg* cfg, double* f_out,
                           mlsqr_outer_step* steps, int* n_steps, int* stop_reason,

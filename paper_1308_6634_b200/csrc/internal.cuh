@@ -395,6 +395,9 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
                 mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true);
 void validate_stop(const mlsqr_stop& s);
+// cg_normal (krylov.cpp:551-628) on the device; M = the V-cycle's level-0 operator (cgn.cu)
+void solve_cg_normal(Op* op, VCycle* m, const double* g, double tau, const mlsqr_stop& stop,
+                     double* f_dev, mlsqr_iter_rec* trace, mlsqr_solve_info* info);
 // stateful outer step (outer.cu)
 class OuterSolver {
  public:

@@ -147,6 +147,21 @@ def main():
         out[f"{backend}_deblur_eps1_alphas"], out[f"{backend}_deblur_eps1_betas"] = res.alphas, res.betas
         out[f"{backend}_deblur_eps1_f"] = res.f
 
+        # --- cg_normal (krylov.cpp:551-628), the unpriorconditioned baseline
+        for tau in (0.0, 0.1):
+            st = stop(20, s4=True, delta=delta, eta=1.1)
+            res = r.cg_normal(r.op_conv1d(n, 0.03), 1, (n,), 1 / n, ft, "pm_log", 0.005, -1.0, tau, gg, st, n)
+            pre = f"{backend}_cgn_deconv_tau{tau}"
+            out[pre + "_f"] = res.f
+            out[pre + "_iters"] = np.array([res.iterations, res.status])
+            out[pre + "_trace"] = np.array([[t_["res_data"], t_["res_damped"], t_["s2_value"], t_["xnorm_est"]]
+                                            for t_ in res.trace])
+        res = r.cg_normal(r.op_blur2d(nx, nx, 0.04), 2, (nx, nx), 1 / nx, f2, "tv", 0.05, 1.0, 1e-2, g2,
+                          stop(30), nx * nx)
+        out[f"{backend}_cgn_deblur_f"] = res.f
+        out[f"{backend}_cgn_deblur_trace"] = np.array([[t_["res_data"], t_["res_damped"], t_["s2_value"],
+                                                         t_["xnorm_est"]] for t_ in res.trace])
+
         # --- nonlinear (lagged diffusivity) 1D runs, reference outer loop with Cholesky M^-1
         for pen, T in (("pm_log", 0.005), ("tikhonov", 1.0), ("tv", 0.01)):
             st = stop(1000, s4=True, delta=delta, eta=1.1)

@@ -375,3 +375,60 @@ def test_device_resident_torch_tensors(ctx, dev):
     r2 = mb.lsqr(gop, g, 0.01, gstop(20))
     assert np.array_equal(r1.solution.cpu().numpy(), r2.solution)
     assert np.array_equal(gop.apply(gd).cpu().numpy(), gop.apply(g))
+
+
+# ---------------------------------------------------------------------------
+# cg_normal (krylov.cpp:551-628): the unpriorconditioned baseline on the same kernels
+# ---------------------------------------------------------------------------
+CGN_CASES = [  # dims, shape, pen, T, tau, stop
+    (2, (24, 24), "tv", 0.05, 1e-2, mb.StoppingConfig.max_iterations(30)),
+    (2, (40, 24), "pm_log", 0.3, 0.0, mb.StoppingConfig.max_iterations(25)),
+    (3, (16, 12, 10), "tv", 0.1, 5e-3, mb.StoppingConfig.max_iterations(20)),
+    (2, (32, 32), "tikhonov", 1.0, 0.1, mb.StoppingConfig(atol=1e-3, max_iters=200, use_s2=True)),
+]
+
+
+@pytest.mark.parametrize("dims,shape,pen,T,tau,st", CGN_CASES)
+def test_cg_normal_bit_exact(ctx, dev, dims, shape, pen, T, tau, st):
+    n = int(np.prod(shape))
+    h = 1.0 / shape[0]
+    rng = np.random.default_rng(n)
+    f = rng.uniform(0, 1, n)
+    taps = dev.taps(shape[0], 2.5 / shape[0], radius=4)
+    g = dev.blur(dims, shape, taps).apply(f) + 0.01 * rng.standard_normal(n)
+    grid = dev.grid(dims, shape, h)
+    cx, cy, cz = dev.edge_coeffs(grid, f, pen, T)
+    eps = 1e-8 * dev.max_diag(grid, cx, cy, cz)
+    vc = mb.VCycleMap(shape, h, 2)
+    assert vc.update(f, mb.PenaltySpec(pen, T)) == eps
+    res = mb.cg_normal(mb.SeparableGaussianBlur(shape, taps=taps), vc if tau > 0 else None, tau, g, st)
+    ores = dev.cg_normal(dev.blur(dims, shape, taps), grid, cx, cy, cz, eps, tau, g, ostop_from(st))
+    assert res.iterations == ores.iterations and res.stop_reason == ores.stop_reason
+    assert np.array_equal(res.solution, ores.f)
+    for t, o in zip(res.trace, ores.trace):
+        assert (t.res_data, t.res_damped, t.s2_value, t.xnorm_est) == \
+            (o["res_data"], o["res_damped"], o["s2_value"], o["xnorm_est"])
+        assert np.isnan(t.anorm_est) and np.isnan(t.cond_est)
+
+
+def test_cg_normal_dense_and_s4(ctx, dev):
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((64, 48)) / 8
+    x = rng.uniform(-1, 1, 48)
+    g = a @ x + 0.01 * rng.standard_normal(64)
+    st = mb.StoppingConfig(max_iters=40, use_s4=True, delta=0.08, eta=1.1)
+    res = mb.cg_normal(mb.DenseOperator(a), None, 0.0, g, st)
+    o = dev.dense(a).set_row_lengths(64, 48)
+    ores = dev.cg_normal(o, dev.grid(1, (48,), 1 / 48), np.zeros(48), None, None, 0.0, 0.0, g, ostop_from(st))
+    assert res.stop_reason == ores.stop_reason == "S4" and res.iterations == ores.iterations
+    assert np.array_equal(res.solution, ores.f)
+
+
+def test_cg_normal_validation(ctx):
+    op = mb.SeparableGaussianBlur((16, 16), taps=mb.gaussian_taps(16, 0.1, 3))
+    with pytest.raises(ValueError):
+        mb.cg_normal(op, None, 1e-2, np.ones(256), mb.StoppingConfig.max_iterations(5))  # tau > 0 needs M
+    with pytest.raises(ValueError):
+        mb.cg_normal(op, mb.IdentityMap(256), 0.0, np.ones(256), mb.StoppingConfig.max_iterations(5))
+    r = mb.cg_normal(op, None, 0.0, np.zeros(256), mb.StoppingConfig.max_iterations(5))
+    assert r.stop_reason == "breakdown" and r.iterations == 0 and not np.any(r.solution)

@@ -204,3 +204,38 @@ def test_signflip_breakdown(orc, golden):
     res = orc.mlsqr(orc.dense(golden["signflip_A"]), pyoracle.OrcMap(orc, h, 8), golden["signflip_g"],
                     0.0, stop(5))
     assert res.status == pyoracle.C.c_int(3).value and res.breakdown_iteration == 0
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.1])
+def test_cg_normal_deconv_matches_reference(orc, golden, tau):
+    """orc_cg_normal (reference order) against the reference's own cg_normal (krylov.cpp:551-628):
+    bit-exact with the scalar backend, AVX2 within its reassociation floor."""
+    n = 128
+    for backend in ("scalar", "avx2"):
+        ft, g = golden[f"{backend}_deconv_ftrue"], golden[f"{backend}_deconv_g"]
+        grid = orc.grid(1, (n,), 1 / n)
+        cx, cy, cz = orc.edge_coeffs(grid, ft, "pm_log", 0.005)
+        eps = 1e-8 * orc.max_diag(grid, cx, cy, cz)
+        st = stop(20, s4=True, delta=0.01 / np.sqrt(1 / n), eta=1.1)
+        res = orc.cg_normal(orc.blur(1, (n,), orc.taps(n, 0.03)), grid, cx, cy, cz, eps, tau, g, st)
+        pre = f"{backend}_cgn_deconv_tau{tau}"
+        it, status = golden[pre + "_iters"]
+        assert res.iterations == it and res.status == status
+        tr = np.array([[t["res_data"], t["res_damped"], t["s2_value"], t["xnorm_est"]] for t in res.trace])
+        if backend == "scalar":
+            assert np.array_equal(res.f, golden[pre + "_f"]) and np.array_equal(tr, golden[pre + "_trace"])
+        else:
+            assert rel(res.f, golden[pre + "_f"]) < 1e-8 and rel(tr, golden[pre + "_trace"]) < 1e-8
+
+
+def test_cg_normal_deblur2d_matches_reference(orc, golden):
+    nx = 24
+    f2, g2 = golden["scalar_deblur_ftrue"], golden["scalar_deblur_g"]
+    grid = orc.grid(2, (nx, nx), 1 / nx)
+    cx, cy, cz = orc.edge_coeffs(grid, f2, "tv", 0.05)
+    res = orc.cg_normal(orc.blur(2, (nx, nx), orc.taps(nx, 0.04)), grid, cx, cy, cz, 1.0, 1e-2, g2, stop(30))
+    tr = np.array([[t["res_data"], t["res_damped"], t["s2_value"], t["xnorm_est"]] for t in res.trace])
+    assert res.iterations == 30
+    assert np.array_equal(res.f, golden["scalar_cgn_deblur_f"])
+    assert np.array_equal(tr, golden["scalar_cgn_deblur_trace"])
+    assert rel(res.f, golden["avx2_cgn_deblur_f"]) < 1e-6
