@@ -189,6 +189,23 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
                      double* f, mlsqr_iter_rec* trace, double* alphas, double* betas,
                      mlsqr_solve_info* info, int ptr_kind);
 
+/* mlsqr / lsqr with SolveOptions::store_basis (krylov.hpp:77-79): additionally writes the right
+ * basis vtilde_1 .. vtilde_k (the scaled v of krylov.cpp:375-377, 421-423) as the rows of
+ * basis[(max_iters + 1) * n_cols] (ptr_kind memory); info->n_alphas rows are valid.
+ * pc == NULL runs lsqr. */
+int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                      double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
+                      mlsqr_solve_info* info, int ptr_kind);
+/* solve_projected (krylov.hpp:124-127, krylov.cpp:631-678): y[k] minimising
+ * |[B_k; sqrt(tau) I] y - beta1 e1| from k alphas and k+1 betas (host arithmetic; one
+ * bidiagonalization serves every tau).  No device needed. */
+int mlsqr_solve_projected(const double* alphas, size_t k, const double* betas, size_t n_betas,
+                          double beta1, double tau, double* y);
+/* reconstruct_from_basis (krylov.hpp:129-131): f = sum_j y_j basis_j for a basis stored by
+ * mlsqr_solve_basis (rows of length n; ny <= rows).  y is a host array. */
+int mlsqr_reconstruct_from_basis(mlsqr_ctx* ctx, const double* basis, size_t n, const double* y, size_t ny,
+                                 double* f, int ptr_kind);
+
 /* cg_normal (krylov.hpp:116-122, krylov.cpp:551-628): CG on (A^T A + tau M) f = A^T g, the
  * unpriorconditioned baseline of the paper's comparison.  M is the level-0 operator of the
  * V-cycle map m (as set by mlsqr_vcycle_set_coefficients / _update; m may be NULL when

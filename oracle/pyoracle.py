@@ -459,6 +459,7 @@ class Reference:
         L.ref_gauss_fill.argtypes = [C.c_uint64, C.c_size_t, C.c_double, dp]
         L.ref_mlsqr.argtypes = [C.POINTER(RefOp), C.POINTER(RefMap), dp, C.c_double, C.POINTER(Stop),
                                 C.c_int, dp, C.POINTER(IterRec), dp, dp, dp, C.POINTER(SolveInfo)]
+        L.ref_solve_projected.argtypes = [dp, C.c_size_t, dp, C.c_size_t, C.c_double, C.c_double, dp]
         L.ref_cg_normal.argtypes = [C.POINTER(RefOp), C.c_int, C.c_size_t, C.c_size_t, C.c_double, dp, C.c_int,
                                     C.c_double, C.c_double, C.c_double, dp, C.POINTER(Stop), dp,
                                     C.POINTER(IterRec), C.POINTER(SolveInfo)]
@@ -581,6 +582,14 @@ class Reference:
                         be[:info.n_betas].copy(), _trace_list(tr, info.iterations), status,
                         info.breakdown_iteration,
                         snap.reshape(k, cols)[:info.iterations] if snapshots else None)
+
+    def solve_projected(self, alphas, betas, beta1, tau):
+        a = np.ascontiguousarray(alphas, dtype=np.float64)
+        b = np.ascontiguousarray(betas, dtype=np.float64)
+        y = np.zeros(a.size)
+        st = self.lib.ref_solve_projected(_ptr(a), a.size, _ptr(b), b.size, beta1, tau, _ptr(y))
+        assert st == 0, st
+        return y
 
     def cg_normal(self, od, dims, shape, h, fM, pen, T, eps, tau, g, st, cols):
         """The reference's own cg_normal with M assembled at fM (eps < 0: auto shift)."""

@@ -327,6 +327,18 @@ void ref_gauss_fill(uint64_t seed, size_t n, double stddev, double* out) {
   s.fill(std::span<double>(out, n), stddev);
 }
 
+// The reference's own solve_projected (krylov.cpp:631-678)
+int ref_solve_projected(const double* alphas, size_t k, const double* betas, size_t nb, double beta1,
+                        double tau, double* y) {
+  return guarded([&] {
+    BidiagEntries bd;
+    bd.alphas.assign(alphas, alphas + k);
+    bd.betas.assign(betas, betas + nb);
+    const auto v = mlsqr::solve_projected(bd, beta1, tau);
+    std::memcpy(y, v.data(), sizeof(double) * v.size());
+  });
+}
+
 // The reference's own cg_normal (krylov.cpp:551-628): CG on (A^T A + tau M) f = A^T g, with M
 // assembled at fM (diffusion.cpp:27-87) and shifted by eps (< 0: auto shift).
 int ref_cg_normal(const ref_op_desc* od, int dims, size_t nx, size_t ny, double h, const double* fM,

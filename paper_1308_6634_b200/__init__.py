@@ -146,6 +146,11 @@ SIGNATURES = {
                               C.c_void_p, C.POINTER(_IterRec), dp, dp, C.POINTER(_Info), C.c_int]),
     "mlsqr_lsqr_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop), C.c_void_p,
                                    C.POINTER(_IterRec), dp, dp, C.POINTER(_Info), C.c_int]),
+    "mlsqr_solve_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop), C.c_void_p,
+                                    C.POINTER(_IterRec), dp, dp, C.c_void_p, C.POINTER(_Info), C.c_int]),
+    "mlsqr_solve_projected": (C.c_int, [dp, C.c_size_t, dp, C.c_size_t, C.c_double, C.c_double, dp]),
+    "mlsqr_reconstruct_from_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, dp, C.c_size_t, C.c_void_p,
+                                               C.c_int]),
     "mlsqr_cg_normal_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop),
                                         C.c_void_p, C.POINTER(_IterRec), C.POINTER(_Info), C.c_int]),
     "mlsqr_nonlinear_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_size_t, C.c_size_t,
@@ -587,10 +592,11 @@ class SolveResult:
     trace: list
     alphas: np.ndarray
     betas: np.ndarray
+    basis: object = None  # [n_alphas, n] right basis when store_basis was requested
 
 
 def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: StoppingConfig,
-         f_out=None, cgn: bool = False) -> SolveResult:
+         f_out=None, cgn: bool = False, store_basis: bool = False) -> SolveResult:
     stop.validate()
     if not tau >= 0.0:
         raise ValueError("tau must be nonnegative")
@@ -612,7 +618,19 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
         f = np.zeros(op.n_cols) if f_out is None else f_out
         fptr = C.c_void_p(f.ctypes.data)
     sc = stop._c()
-    if cgn:
+    basis = None
+    if store_basis:
+        rows = (k + 1) * op.n_cols
+        if kind == DEVICE:
+            import torch
+            basis = torch.empty(rows, dtype=torch.float64, device=g.device)
+            bptr = C.c_void_p(basis.data_ptr())
+        else:
+            basis = np.zeros(rows)
+            bptr = C.c_void_p(basis.ctypes.data)
+        st = lib().mlsqr_solve_basis(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
+                                     _ptr(al), _ptr(be), bptr, C.byref(info), kind)
+    elif cgn:
         st = lib().mlsqr_cg_normal_solve(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
                                          C.byref(info), kind)
     elif pc is None:
@@ -623,18 +641,56 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
     trace = [IterationRecord(t.iteration, t.res_damped, t.res_data, bool(t.res_data_exact), t.s2_value,
                              t.anorm_est, t.cond_est, t.xnorm_est, t.alpha, t.beta)
              for t in tr[:info.iterations]]
+    if basis is not None:
+        basis = basis[:info.n_alphas * op.n_cols].reshape(info.n_alphas, op.n_cols)
     return SolveResult(f, info.iterations, STOP_NAMES[info.stop_reason], trace,
-                       al[:info.n_alphas].copy(), be[:info.n_betas].copy())
+                       al[:info.n_alphas].copy(), be[:info.n_betas].copy(), basis)
 
 
-def mlsqr(a: LinearOperator, msolver: SpdMap, g, tau: float, stop: StoppingConfig, f_out=None) -> SolveResult:
-    """Factorization-free priorconditioned LSQR (krylov.hpp:89-95)."""
-    return _run(a, msolver, g, tau, stop, f_out)
+def mlsqr(a: LinearOperator, msolver: SpdMap, g, tau: float, stop: StoppingConfig, f_out=None,
+          store_basis: bool = False) -> SolveResult:
+    """Factorization-free priorconditioned LSQR (krylov.hpp:89-95).  store_basis
+    (SolveOptions, krylov.hpp:77-79) also returns the right basis vtilde_1..k as `.basis`."""
+    return _run(a, msolver, g, tau, stop, f_out, store_basis=store_basis)
 
 
-def lsqr(a: LinearOperator, g, tau: float, stop: StoppingConfig, f_out=None) -> SolveResult:
+def lsqr(a: LinearOperator, g, tau: float, stop: StoppingConfig, f_out=None,
+         store_basis: bool = False) -> SolveResult:
     """Damped LSQR (krylov.hpp:80-87)."""
-    return _run(a, None, g, tau, stop, f_out)
+    return _run(a, None, g, tau, stop, f_out, store_basis=store_basis)
+
+
+def solve_projected(alphas, betas, beta1: float, tau: float) -> np.ndarray:
+    """solve_projected (krylov.hpp:124-127): y minimising |[B_k; sqrt(tau) I] y - beta1 e1|
+    from a bidiagonalization's k alphas and k+1 betas -- one solve serves every tau."""
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    b = np.ascontiguousarray(betas, dtype=np.float64)
+    y = np.zeros(max(a.size, 1))
+    _check(lib().mlsqr_solve_projected(_ptr(a), a.size, _ptr(b), b.size, beta1, tau, _ptr(y)))
+    return y[:a.size]
+
+
+def reconstruct_from_basis(basis, y, ctx: Optional[Context] = None, f_out=None):
+    """reconstruct_from_basis (krylov.hpp:129-131): f = sum_j y_j basis[j]."""
+    ctx = ctx or default_context()
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if y.size == 0:
+        raise ValueError("no basis vectors were stored")
+    if y.size > basis.shape[0]:
+        raise DimensionError("more coefficients than basis vectors")
+    n = basis.shape[1]
+    if _is_dev(basis):
+        import torch
+        b = basis[:y.size].contiguous()
+        f = torch.empty(n, dtype=torch.float64, device=basis.device) if f_out is None else f_out
+        _check(lib().mlsqr_reconstruct_from_basis(ctx.h, C.c_void_p(b.data_ptr()), n, _ptr(y), y.size,
+                                                  C.c_void_p(f.data_ptr()), DEVICE))
+    else:
+        b = np.ascontiguousarray(basis[:y.size], dtype=np.float64)
+        f = np.zeros(n) if f_out is None else f_out
+        _check(lib().mlsqr_reconstruct_from_basis(ctx.h, C.c_void_p(b.ctypes.data), n, _ptr(y), y.size,
+                                                  C.c_void_p(f.ctypes.data), HOST))
+    return f
 
 
 def cg_normal(a: LinearOperator, m: Optional["VCycleMap"], tau: float, g, stop: StoppingConfig,

@@ -481,6 +481,68 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
   return run_solve(op, nullptr, g, tau, stop, f, trace, alphas, betas, info, ptr_kind, true);
 }
 
+int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                      double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
+                      mlsqr_solve_info* info, int kind) {
+  int bd_iter = 0;
+  if (info) std::memset(info, 0, sizeof(*info));
+  const int st = guard([&] {
+    require(op && stop && basis, MLSQR_EINVAL, "operator, stopping config and basis are required");
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    In gin(c, g, o->rows, kind);
+    Out fout(c, f, o->cols, kind);
+    const size_t nb = ((size_t)stop->max_iters + 1) * o->cols;
+    DevBuf<double> staged;
+    double* bd = basis;
+    if (kind != MLSQR_DEVICE) {
+      staged.alloc(nb);
+      bd = staged.p;
+    }
+    mlsqr_solve_info inf{};
+    try {
+      solve_mlsqr(o, pc ? pc->impl : nullptr, gin.d, tau, *stop, fout.d, trace, alphas, betas, &inf, nullptr, true, bd);
+    } catch (const Error& e) {
+      if (e.code == MLSQR_EBREAKDOWN) bd_iter = e.iteration;
+      if (info) *info = inf;
+      throw;
+    }
+    if (info) *info = inf;
+    if (kind != MLSQR_DEVICE && inf.n_alphas > 0)
+      MLSQR_CUDA(cudaMemcpyAsync(basis, bd, sizeof(double) * (size_t)inf.n_alphas * o->cols, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    fout.finish();
+  });
+  if (st == MLSQR_EBREAKDOWN && info) info->breakdown_iteration = bd_iter;
+  return st;
+}
+
+int mlsqr_solve_projected(const double* alphas, size_t k, const double* betas, size_t n_betas, double beta1,
+                          double tau, double* y) {
+  return guard([&] {
+    require(alphas && betas && y, MLSQR_EINVAL, "solve_projected: null argument");
+    const std::vector<double> v = solve_projected(alphas, k, betas, n_betas, beta1, tau);
+    std::memcpy(y, v.data(), sizeof(double) * k);
+  });
+}
+
+int mlsqr_reconstruct_from_basis(mlsqr_ctx* ctx, const double* basis, size_t n, const double* y, size_t ny,
+                                 double* f, int kind) {
+  return guard([&] {
+    require(ctx && basis && y && f, MLSQR_EINVAL, "reconstruct_from_basis: null argument");
+    require(ny >= 1, MLSQR_EINVAL, "no basis vectors were stored");
+    Ctx* c = &ctx->impl;
+    set_device(c);
+    In bin(c, basis, ny * n, kind);
+    DevBuf<double> yd(ny);
+    MLSQR_CUDA(cudaMemcpyAsync(yd.p, y, sizeof(double) * ny, cudaMemcpyHostToDevice, c->stream));
+    Out fout(c, f, n, kind);
+    reconstruct_from_basis(c, bin.d, n, yd.p, ny, fout.d);
+    fout.finish();
+  });
+}
+
 int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau, const mlsqr_stop* stop,
                           double* f, mlsqr_iter_rec* trace, mlsqr_solve_info* info, int kind) {
   int bd_iter = 0;

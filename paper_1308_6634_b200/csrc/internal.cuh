@@ -393,7 +393,12 @@ void workspace_free(Workspace* w);
 // stays queued (outer loop) and results must be fetched with solve_fetch().
 int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
-                mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true);
+                mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true,
+                double* basis_dev = nullptr);
+// solve_projected (krylov.cpp:631-678), host arithmetic (projected.cu)
+std::vector<double> solve_projected(const double* alphas, size_t k, const double* betas, size_t nb,
+                                    double beta1, double tau);
+void reconstruct_from_basis(Ctx* c, const double* basis, size_t n, const double* y, size_t ny, double* f);
 void validate_stop(const mlsqr_stop& s);
 // cg_normal (krylov.cpp:551-628) on the device; M = the V-cycle's level-0 operator (cgn.cu)
 void solve_cg_normal(Op* op, VCycle* m, const double* g, double tau, const mlsqr_stop& stop,

@@ -232,6 +232,17 @@ __global__ void fin_p_kernel(DevState* s) {
   s->flags[2] = sqrt(s->red_p) > 0.0 ? 1 : 0;
 }
 
+// SolveOptions::store_basis (krylov.cpp:375-377, 421-423): row n_alphas-1 of the basis is the
+// scaled vtilde (v * (1/alpha), the reference's scal), written when this step produced an alpha
+__global__ void basis_kernel(const DevState* __restrict__ s, const double* __restrict__ v,
+                             double* __restrict__ basis, size_t n, int in_loop) {
+  if (!s->flags[0] || (in_loop && !s->flags[3])) return;
+  double* row = basis + (size_t)(s->n_alphas - 1) * n;
+  const double sv = s->sv;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    row[i] = v[i] * sv;
+}
+
 // F_a (krylov.cpp:399-431)
 __global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) {
   if (!s->flags[0]) return;
@@ -387,8 +398,16 @@ struct Runner {
   mlsqr_stop stop;
   DevState* st;
   Ctx* c;
+  double* basis = nullptr;  // [(max_iters + 1) x cols] when the basis is stored
 
   const int* flag(int k) const { return &st->flags[k]; }
+  void store_basis(int in_loop) {
+    if (!basis) return;
+    const size_t n = op->cols;
+    const unsigned g = (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    basis_kernel<<<g, 256, 0, c->stream>>>(st, vbuf(), basis, n, in_loop);
+    c->count();
+  }
   const int* gate_active() const { return flag(0); }
 
   // data-space vectors are distributed under z slabs and row shards; solution-space ones
@@ -430,6 +449,7 @@ struct Runner {
     fin_p0_kernel<<<1, 1, 0, c->stream>>>(st);
     precond(gate_active());
     fin_alpha1_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p);
+    store_basis(0);
     dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
     init_wq_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
@@ -468,6 +488,7 @@ struct Runner {
     // M^{-1}
     precond(flag(2));
     fin_alpha_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p, ws->betas.p);
+    store_basis(1);
     // K_U
     {
       TimedRegion tr(c, MLSQR_TCLASS_UPDATE);
@@ -496,7 +517,7 @@ struct Runner {
 
 int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
-                mlsqr_solve_info* info, Workspace* ws_in, bool use_graph) {
+                mlsqr_solve_info* info, Workspace* ws_in, bool use_graph, double* basis_dev) {
   Ctx* c = op->ctx;
   validate_stop(stop);
   require(tau >= 0.0, MLSQR_EINVAL, "tau must be nonnegative");
@@ -532,7 +553,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
   ws->f.p = f_dev;
   ws->f.n = op->cols;
 
-  Runner r{op, pc, ws, tau, stop, ws->st.p, c};
+  Runner r{op, pc, ws, tau, stop, ws->st.p, c, basis_dev};
   const bool host_cb = pc && pc->host_callback();
   const bool graph = use_graph && !host_cb && !c->timing && (!c->comm || c->comm->capturable());
   r.init(g_dev);

@@ -147,6 +147,13 @@ def main():
         out[f"{backend}_deblur_eps1_alphas"], out[f"{backend}_deblur_eps1_betas"] = res.alphas, res.betas
         out[f"{backend}_deblur_eps1_f"] = res.f
 
+        # --- solve_projected (krylov.cpp:631-678) over this backend's stored bidiagonalizations
+        for src in ("mlsqr_dense_tau0.0", "deblur_eps1"):
+            al, be = out[f"{backend}_{src}_alphas"], out[f"{backend}_{src}_betas"]
+            k = min(al.size, be.size - 1)
+            for tau in (0.0, 1e-3, 0.1, 10.0):
+                out[f"{backend}_proj_{src}_tau{tau}"] = r.solve_projected(al[:k], be[:k + 1], be[0], tau)
+
         # --- cg_normal (krylov.cpp:551-628), the unpriorconditioned baseline
         for tau in (0.0, 0.1):
             st = stop(20, s4=True, delta=delta, eta=1.1)

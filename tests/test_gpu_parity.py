@@ -432,3 +432,52 @@ def test_cg_normal_validation(ctx):
         mb.cg_normal(op, mb.IdentityMap(256), 0.0, np.ones(256), mb.StoppingConfig.max_iterations(5))
     r = mb.cg_normal(op, None, 0.0, np.zeros(256), mb.StoppingConfig.max_iterations(5))
     assert r.stop_reason == "breakdown" and r.iterations == 0 and not np.any(r.solution)
+
+
+# ---------------------------------------------------------------------------
+# stored basis + solve_projected: one bidiagonalization serves every tau (krylov.cpp:631-689)
+# ---------------------------------------------------------------------------
+def test_store_basis_and_multi_tau(ctx, dev):
+    """SolveOptions::store_basis on the device: for every tau the
+    projected solve re-expanded through the stored basis reproduces a fresh mlsqr at that tau
+    (the reference's stored-basis re-solve property, test_krylov.cpp:237-259, 1e-8).  The
+    bidiagonalization does not depend on tau, so alphas/betas are bit-identical across taus."""
+    shape = (32, 24)
+    n = 32 * 24
+    rng = np.random.default_rng(4)
+    f = rng.uniform(0, 1, n)
+    taps = dev.taps(32, 2.0 / 32, radius=5)
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    g = op.apply(f) + 0.01 * rng.standard_normal(n)
+    vc = mb.VCycleMap(shape, 1.0 / 32, 3)
+    vc.update(f, mb.PenaltySpec.tv_smoothed(0.1))
+    st = mb.StoppingConfig.max_iterations(12)
+    res = mb.mlsqr(op, vc, g, 1e-2, st, store_basis=True)
+    k = res.alphas.size
+    assert res.basis.shape == (k, n) and k == 12
+    # (the basis is orthonormal in the inverse of the V-cycle map B ~ M^-1, which is not formed)
+    assert np.all(np.isfinite(res.basis)) and np.all(np.linalg.norm(res.basis, axis=1) > 0)
+    beta1 = res.betas[0]
+    for tau in (1e-2, 1e-4, 1e-1):
+        y = mb.solve_projected(res.alphas, res.betas[:k + 1], beta1, tau)
+        fr = mb.reconstruct_from_basis(res.basis, y)
+        fresh = res if tau == 1e-2 else mb.mlsqr(op, vc, g, tau, st)
+        assert np.array_equal(fresh.alphas, res.alphas) and np.array_equal(fresh.betas, res.betas)
+        assert np.linalg.norm(fr - fresh.solution) <= 1e-8 * np.linalg.norm(fresh.solution)
+    # the stored solve itself is unchanged by storing the basis
+    assert np.array_equal(res.solution, mb.mlsqr(op, vc, g, 1e-2, st).solution)
+
+
+def test_store_basis_lsqr_device_tensors(ctx):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(6)
+    a = rng.standard_normal((60, 40))
+    op = mb.DenseOperator(a)
+    g = torch.from_numpy(rng.standard_normal(60)).cuda()
+    res = mb.lsqr(op, g, 0.0, mb.StoppingConfig.max_iterations(10), store_basis=True)
+    V = res.basis.cpu().numpy()
+    assert np.abs(V @ V.T - np.eye(V.shape[0])).max() < 1e-10  # plain LSQR: orthonormal
+    y = mb.solve_projected(res.alphas, res.betas[:res.alphas.size + 1], res.betas[0], 0.0)
+    fr = mb.reconstruct_from_basis(res.basis, y)
+    assert torch.is_tensor(fr)
+    assert float((fr - res.solution).norm()) <= 1e-8 * float(res.solution.norm())

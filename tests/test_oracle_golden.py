@@ -239,3 +239,26 @@ def test_cg_normal_deblur2d_matches_reference(orc, golden):
     assert np.array_equal(res.f, golden["scalar_cgn_deblur_f"])
     assert np.array_equal(tr, golden["scalar_cgn_deblur_trace"])
     assert rel(res.f, golden["avx2_cgn_deblur_f"]) < 1e-6
+
+
+@pytest.mark.parametrize("src", ["mlsqr_dense_tau0.0", "deblur_eps1"])
+@pytest.mark.parametrize("tau", [0.0, 1e-3, 0.1, 10.0])
+def test_solve_projected_matches_reference(golden, src, tau):
+    """The library's solve_projected (host code behind the C-ABI, no GPU needed) equals the
+    reference's solve_projected (krylov.cpp:631-678) bit for bit on stored bidiagonalizations."""
+    import paper_1308_6634_b200 as mb
+    for backend in ("scalar", "avx2"):
+        al, be = golden[f"{backend}_{src}_alphas"], golden[f"{backend}_{src}_betas"]
+        k = min(al.size, be.size - 1)
+        y = mb.solve_projected(al[:k], be[:k + 1], be[0], tau)
+        assert np.array_equal(y, golden[f"{backend}_proj_{src}_tau{tau}"])
+
+
+def test_solve_projected_validation():
+    import paper_1308_6634_b200 as mb
+    with pytest.raises(ValueError):
+        mb.solve_projected([], [1.0], 1.0, 0.0)  # empty bidiagonalization
+    with pytest.raises(ValueError):
+        mb.solve_projected([1.0, 2.0], [1.0, 0.5], 1.0, 0.0)  # needs k+1 betas
+    with pytest.raises(ValueError):
+        mb.solve_projected([1.0], [1.0, 0.5], 1.0, -1.0)
