@@ -11,15 +11,10 @@
 // 3D (no reference implementation) uses fma chains -- the canonical
 // DEVICE order the oracle restates with C fma().
 //
-// 3D main kernel (blur3d_fused): one CTA owns a 32 x 32 column tile and a
-// z chunk.  Input planes stream through a 3-deep cp.async ring in shared
-// memory (stored x-major so the x pass reads conflict-free register
-// windows), the x and y passes run out of shared memory with register
-// blocking (8 x outputs / 4 y outputs per thread), the z pass runs from a
-// register ring of the last 2R+1 xy-blurred planes, and the epilogue
-// (xpby with the old vector, also staged by cp.async, plus the canonical
-// |out|^2 segment partials) is fused.  HBM traffic: read x once, read old
-// once, write out once.
+// 3D main kernel: blur3d_pipe (blur3d_pipe.cuh) -- TMA plane ring, one barrier per
+// plane, z accumulators, persistent round-robin (z chunk, column tile) items; the
+// xpby epilogue with the old vector and the canonical |out|^2 segment partials are
+// fused.  HBM traffic: read x once, read old once, write out once.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -139,208 +134,6 @@ __global__ void blur_pass_kernel(const double* __restrict__ in, double* __restri
     const double s = tree32(v * v);
     if (threadIdx.x == 0) e.seg[row * ((nx + 31) / 32) + blockIdx.x] = s;
   }
-}
-
-// ---------------------------------------------------------------------------
-// fused 3D kernel
-// ---------------------------------------------------------------------------
-
-template <int R>
-struct B3 {
-  static constexpr int NT = 2 * R + 1;        // taps
-  static constexpr int TX = 32, TY = 32;      // output tile (x, y)
-  static constexpr int THREADS = 512;         // 32 x 16: two y-columns per thread
-  static constexpr int W = TX + 2 * R;        // input x extent (even)
-  static constexpr int H = TY + 2 * R;        // input y extent (rows)
-  static constexpr int P = ((W / 2) % 2) ? W : W + 2;  // row pitch: P/2 odd -> LDS.128 conflict-free
-  static constexpr int XK = 4;                // x outputs per x-pass task
-  static constexpr int XG = TX / XK;          // x groups per row
-  static constexpr int XP = 34;               // x-pass buffer pitch (XP/2 odd)
-  static constexpr int NBUF = 3;              // cp.async ring depth
-  static constexpr int IN_DOUBLES = H * P;
-  static constexpr int XS_DOUBLES = H * XP;
-  static constexpr int OLD_DOUBLES = TX * TY;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)NBUF * IN_DOUBLES + XS_DOUBLES + (size_t)NBUF * OLD_DOUBLES);
-};
-
-// VEC: 16-byte copies (needs R even and nx even so every pair is aligned and either fully
-// inside or fully outside the domain); otherwise 8-byte copies.
-template <int R, bool VEC>
-__global__ void __launch_bounds__(512, 1) blur3d_fused(const double* __restrict__ in,
-                                                       double* __restrict__ out, int nx, int ny,
-                                                       int nz, int zchunk, int zoff, int nzg, Taps taps,
-                                                       EpiArgs e) {
-  using C = B3<R>;
-  if (e.gate && *e.gate == 0) return;
-  extern __shared__ __align__(16) double sm[];
-  double* tin = sm;                              // [NBUF][H][P]   input planes (row-major)
-  double* xs = sm + C::NBUF * C::IN_DOUBLES;     // [H][XP]        x-pass results
-  double* olds = xs + C::XS_DOUBLES;             // [NBUF][TY][TX] old-vector planes
-  const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * C::TX, y0 = blockIdx.y * C::TY;
-  const int z0 = blockIdx.z * zchunk;
-  const int z1 = min(nz, z0 + zchunk);
-  const int zlo = z0 - R, zhi = z1 + R - 1;  // planes touched
-  const size_t nxy = (size_t)nx * ny;
-  const double sx = e.sx ? *e.sx : 1.0;
-  // the taps are bitwise symmetric (t[k] == t[2R-k], checked on the host): only R+1
-  // distinct constants feed the DFMAs, which keeps them in uniform registers
-#define TAP(k) taps.t[(k) <= R ? (k) : 2 * R - (k)]
-
-  // per-thread 16-byte copy descriptors of the input tile, computed once (VEC path)
-  constexpr int PAIRS = C::W / 2;
-  constexpr int NPAIR = C::H * PAIRS;
-  constexpr int PER = (NPAIR + C::THREADS - 1) / C::THREADS;
-  int c_soff[PER];
-  long c_goff[PER];
-  bool c_ok[PER];
-  if (VEC) {
-#pragma unroll
-    for (int m = 0; m < PER; ++m) {
-      const int k = tid + m * C::THREADS;
-      const int ly = k / PAIRS, q = k - ly * PAIRS;
-      const int gx = x0 - R + 2 * q, gy = y0 + ly - R;
-      c_ok[m] = k < NPAIR && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-      c_soff[m] = k < NPAIR ? ly * C::P + 2 * q : -1;
-      c_goff[m] = c_ok[m] ? (long)gy * nx + gx : 0;
-    }
-  }
-
-  auto issue = [&](int zz) {
-    const int slot = (zz - zlo) % C::NBUF;
-    if (zz + zoff >= 0 && zz + zoff < nzg && zz <= zhi) {  // global plane inside the domain
-      double* dst = tin + (size_t)slot * C::IN_DOUBLES;
-      const double* src = in + (size_t)zz * nxy;
-      if (VEC) {
-#pragma unroll
-        for (int m = 0; m < PER; ++m)
-          if (c_soff[m] >= 0) cp_async16(dst + c_soff[m], c_ok[m] ? src + c_goff[m] : in, c_ok[m]);
-      } else {
-        for (int k = tid; k < C::H * C::W; k += C::THREADS) {
-          const int ly = k / C::W, lx = k - ly * C::W;
-          const int gx = x0 + lx - R, gy = y0 + ly - R;
-          const bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-          cp_async8(dst + ly * C::P + lx, ok ? src + (size_t)gy * nx + gx : in, ok);
-        }
-      }
-    }
-    const int zo = zz - R;
-    if (e.old && zo >= z0 && zo < z1) {
-      double* dst = olds + (size_t)slot * C::OLD_DOUBLES;
-      const double* src = e.old + (size_t)zo * nxy;
-      if (VEC) {
-        for (int k = tid; k < C::TX * C::TY / 2; k += C::THREADS) {
-          const int ly = k >> 4, q = k & 15;
-          const int gx = x0 + 2 * q, gy = y0 + ly;
-          const bool ok = gx < nx && gy < ny;
-          cp_async16(dst + ly * 32 + 2 * q, ok ? src + (size_t)gy * nx + gx : in, ok);
-        }
-      } else {
-        for (int k = tid; k < C::TX * C::TY; k += C::THREADS) {
-          const int ly = k >> 5, lx = k & 31;
-          const int gx = x0 + lx, gy = y0 + ly;
-          const bool ok = gx < nx && gy < ny;
-          cp_async8(dst + k, ok ? src + (size_t)gy * nx + gx : in, ok);
-        }
-      }
-    }
-    cp_async_commit();
-  };
-
-  const int tx = tid & 31, ty = tid >> 5;  // y / z pass + epilogue: y = 2ty, 2ty + 1
-  double ring[2][C::NT];
-#pragma unroll
-  for (int o = 0; o < 2; ++o)
-#pragma unroll
-    for (int k = 0; k < C::NT; ++k) ring[o][k] = 0.0;
-
-  issue(zlo);
-  issue(zlo + 1);
-  const double so = e.so ? *e.so : 1.0;
-  const double coef = e.old ? *e.coef : 0.0;
-  const size_t chunks = (size_t)(nx + 31) / 32;
-  // x-pass task of this thread: row xr (lanes = consecutive rows), x group xg
-  const int xr = tid % C::H, xg = tid / C::H;
-  const bool xtask = tid < C::H * C::XG;
-
-  for (int base = zlo; base <= zhi; base += C::NT) {
-#pragma unroll
-    for (int u = 0; u < C::NT; ++u) {
-      const int zz = base + u;
-      if (zz <= zhi) {  // block-uniform
-        issue(zz + 2);
-        cp_async_wait<2>();
-        __syncthreads();
-        const int slot = (zz - zlo) % C::NBUF;
-        double yv0 = 0.0, yv1 = 0.0;
-        if (zz + zoff >= 0 && zz + zoff < nzg) {
-          if (xtask) {
-            const double* row = tin + (size_t)slot * C::IN_DOUBLES + xr * C::P + C::XK * xg;
-            double w[C::XK + 2 * R];
-#pragma unroll
-            for (int j = 0; j < (C::XK + 2 * R) / 2; ++j) {
-              const double2 p = *reinterpret_cast<const double2*>(row + 2 * j);
-              w[2 * j] = p.x;
-              w[2 * j + 1] = p.y;
-            }
-            if (e.sx) {
-#pragma unroll
-              for (int j = 0; j < C::XK + 2 * R; ++j) w[j] = w[j] * sx;
-            }
-            double acc[C::XK];
-#pragma unroll
-            for (int o = 0; o < C::XK; ++o) {
-              acc[o] = 0.0;
-#pragma unroll
-              for (int k = 0; k < C::NT; ++k) acc[o] = fma(TAP(k), w[o + k], acc[o]);
-            }
-            double* xw = xs + xr * C::XP + C::XK * xg;
-            *reinterpret_cast<double2*>(xw) = make_double2(acc[0], acc[1]);
-            *reinterpret_cast<double2*>(xw + 2) = make_double2(acc[2], acc[3]);
-          }
-          __syncthreads();
-          double c[2 + 2 * R];
-#pragma unroll
-          for (int j = 0; j < 2 + 2 * R; ++j) c[j] = xs[(2 * ty + j) * C::XP + tx];
-#pragma unroll
-          for (int k = 0; k < C::NT; ++k) {
-            yv0 = fma(TAP(k), c[k], yv0);
-            yv1 = fma(TAP(k), c[k + 1], yv1);
-          }
-        }
-        ring[0][u] = yv0;
-        ring[1][u] = yv1;
-        // z pass for output plane zo = zz - R: planes zo-R .. zz sit in ring slots u+1+k (mod NT)
-        const int zo = zz - R;
-        if (zo >= z0 && zo < z1) {
-          const double* po = olds + (size_t)slot * C::OLD_DOUBLES;
-#pragma unroll
-          for (int o = 0; o < 2; ++o) {
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < C::NT; ++k) acc = fma(TAP(k), ring[o][(u + 1 + k) % C::NT], acc);
-            const int gy = y0 + 2 * ty + o, gx = x0 + tx;
-            double v = 0.0;
-            if (gx < nx && gy < ny) {
-              v = acc;
-              if (e.old) {
-                double ov = po[(2 * ty + o) * 32 + tx];
-                if (e.so) ov = ov * so;
-                v = acc + coef * ov;
-              }
-              out[(size_t)zo * nxy + (size_t)gy * nx + gx] = v;
-            }
-            if (e.seg && gy < ny) {
-              const double s = tree32(v * v);
-              if (tx == 0) e.seg[((size_t)zo * ny + gy) * chunks + blockIdx.x] = s;
-            }
-          }
-        }
-        __syncthreads();  // xs and the input slot are reused by the next plane
-      }
-    }
-  }
-#undef TAP
 }
 
 #include "blur3d_pipe.cuh"

@@ -1,7 +1,7 @@
 // blur3d_pipe.cuh -- the default fused 3D blur (included by blur.cu).
 //
-// Same per-output arithmetic as blur3d_fused (hence bit-identical), scheduled
-// for the issue-bound regime the FP64 stencil lives in:
+// Per output: fma(t[0], x[i-R], 0), fma(t[1], x[i-R+1], .) ... along x, then y, then z
+// (the oracle's DEVICE order), scheduled for the issue-bound regime of the FP64 stencil:
 //  * TMA: one thread loads each input plane tile (a (32+2R) x P box; the
 //    hardware zero-fills everything outside the grid, so no per-element
 //    predicates) and the old-vector tile into a 4-stage ring completed by
@@ -304,38 +304,10 @@ static bool tensor_map3d(CUtensorMap* m, const double* base, int nx, int ny, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool blur_legacy() {
-  static const bool v = [] {
-    const char* s = getenv("MLSQR_BLUR_LEGACY");
-    return s && s[0] == '1';
-  }();
-  return v;
-}
-
-template <int R, bool VEC>
-static void launch_b3_legacy(Ctx* c, const double* in, double* out, int nx, int ny, int nz, int zchunk,
-                             const Taps& t, const EpiArgs& a) {
-  static bool attr = false;
-  if (!attr) {
-    MLSQR_CUDA(cudaFuncSetAttribute(blur3d_fused<R, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B3<R>::SMEM));
-    attr = true;
-  }
-  dim3 grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)((nz + zchunk - 1) / zchunk));
-  const int zoff = c->sharded() ? (int)c->zoff : 0, nzg = c->sharded() ? (int)c->nzg : nz;
-  blur3d_fused<R, VEC><<<grd, B3<R>::THREADS, B3<R>::SMEM, c->stream>>>(in, out, nx, ny, nz, zchunk, zoff, nzg, t, a);
-}
-
 template <int R>
 static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
                       const EpiArgs& a) {
   using C = B3P<R>;
-  const int zchunk = nz >= 256 ? 64 : (nz >= 64 ? 32 : nz);
-  if (blur_legacy()) {
-    if (R % 2 == 0 && nx % 2 == 0) launch_b3_legacy<R, true>(c, in, out, nx, ny, nz, zchunk, t, a);
-    else launch_b3_legacy<R, false>(c, in, out, nx, ny, nz, zchunk, t, a);
-    c->count();
-    return;
-  }
   static bool attr = false;
   if (!attr) {
     MLSQR_CUDA(cudaFuncSetAttribute(blur3d_pipe<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -365,7 +337,6 @@ static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int
   CUtensorMap mi{}, mo{};
   bool tma = tensor_map3d(&mi, in - (size_t)zshift * nx * ny, nx, ny, nz + 2 * zshift, C::P, C::H);
   if (tma && a.old) tma = tensor_map3d(&mo, a.old, nx, ny, nz, C::TX, C::TY);
-  if (getenv("MLSQR_BLUR_NOTMA")) tma = false;
   if (tma)
     blur3d_pipe<R, true><<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, tiles, zck,
                                                                    items, zoff, nzg, zshift, t, a, mi, mo);

@@ -118,7 +118,6 @@ __global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restr
 }
 
 #include "stencil_zm.cuh"
-#include "sweep2.cuh"
 #include "sweep_fn.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
@@ -318,11 +317,6 @@ class VCycle final : public Pc {
     }
     eps_.alloc((size_t)levels);
     maxd_.alloc(1);
-    MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(false)));
-    MLSQR_CUDA(cudaFuncSetAttribute(sweep2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep2_smem(true)));
-    // the smem-tiled two-sweep kernel (sweep2.cuh) is opt-in: on B200 the branch-free
-    // z-marching sweeps are faster (see profiles/README.md)
-    if (const char* e = getenv("MLSQR_FUSED_SWEEPS")) fuse_enabled_ = e[0] == '1';
     if (const char* e = getenv("MLSQR_FN_SWEEPS")) fn_enabled_ = e[0] != '0';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
   }
@@ -473,17 +467,12 @@ class VCycle final : public Pc {
     int nb = 0;
     // pre-smoothing (or the whole coarse solve) from zero
     const double* cur = nullptr;
-    const bool fuse = fused_ok(l) && !ctx->sharded();
     for (int s = 0; s < pre; ++s) {
-      const bool pair = fuse && s == 0 && pre >= 2;  // sweeps 1 + 2 in one kernel
-      const bool fpair = !pair && fn_ok(l) && s == 0 && pre >= 2;  // same, x1 kept on chip
-      const bool last_here = coarsest && s + ((pair || fpair) ? 2 : 1) == pre;
+      const bool fpair = fn_ok(l) && s == 0 && pre >= 2;  // sweeps 1 + 2 in one kernel, x1 on chip
+      const bool last_here = coarsest && s + (fpair ? 2 : 1) == pre;
       double* dst = (last_here && out) ? out : bufs[nb];
       double* sg = (last_here && out) ? seg : nullptr;
-      if (pair) {
-        sweep2<false>(l, nullptr, nullptr, b, dst, sg, gate);
-        ++s;
-      } else if (fpair) {
+      if (fpair) {
         sweep_fn(l, b, dst, sg, gate);
         ++s;
       } else if (s == 0) {
@@ -506,14 +495,10 @@ class VCycle final : public Pc {
       return dst;
     }
     for (int s = 0; s < nu_post_; ++s) {
-      const bool pair = fuse && s == 0 && nu_post_ >= 2;  // prolong + sweeps 3 + 4 in one kernel
-      const bool last = s + (pair ? 2 : 1) == nu_post_;
+      const bool last = s + 1 == nu_post_;
       double* dst = (last && out) ? out : bufs[nb];
       double* sg = (last && out) ? seg : nullptr;
-      if (pair) {
-        sweep2<true>(l, cur, xc, b, dst, sg, gate);
-        ++s;
-      } else if (s == 0) {
+      if (s == 0) {
         hx(l, cur);
         hx(l + 1, xc);
         sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
@@ -526,9 +511,6 @@ class VCycle final : public Pc {
     }
     return cur;
   }
-
-  // fused two-sweep kernel: 16-byte plane copies need an even x extent
-  bool fused_ok(int l) const { return fuse_enabled_ && lv_[(size_t)l].nx % 2 == 0; }
 
   // first + second pre-sweep in one kernel (3D, unsharded: x1 halos are computed, not exchanged)
   bool fn_ok(int) const { return fn_enabled_ && dims_ == 3 && !ctx->sharded(); }
@@ -543,26 +525,7 @@ class VCycle final : public Pc {
     ctx->count();
   }
 
-  template <bool PROLONG>
-  void sweep2(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
-              const int* gate) {
-    const Level& L = lv_[(size_t)l];
-    int cnx = 0, cny = 0;
-    if (l + 1 < (int)lv_.size()) {
-      cnx = lv_[(size_t)l + 1].nx;
-      cny = lv_[(size_t)l + 1].ny;
-    }
-    TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
-    const int zc = sweep2_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
-    dim3 grd((unsigned)((L.nx + s2::TX - 1) / s2::TX), (unsigned)((L.ny + s2::TY - 1) / s2::TY),
-             (unsigned)((L.nz + zc - 1) / zc));
-    sweep2_kernel<PROLONG><<<grd, s2::THREADS, sweep2_smem(PROLONG), ctx->stream>>>(
-        view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
-    ctx->count();
-  }
-
  public:
-  bool fuse_enabled_ = false;
   bool fn_enabled_ = true;
 
  private:
