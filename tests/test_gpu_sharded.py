@@ -261,3 +261,41 @@ def test_row_shard_validation():
         mb.DenseOperator(np.zeros((48, 64)), ctx=c)
     with pytest.raises(ValueError):
         mb.SeparableGaussianBlur((16, 16, 16), taps=mb.gaussian_taps(16, 0.1, 2), ctx=c)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_outer_solver_steps_sharded_bit_exact(problem, P):
+    """The bench's path: OuterSolver.step (mlsqr_outer_advance, resident hierarchy and
+    workspace) on device tensors, three steps -- every rank's slab of f after each step and
+    every step's R(f) / eps equal the single-rank run."""
+    torch = pytest.importorskip("torch")
+    shape, taps, f, g = problem
+    nx, ny, nz = shape
+    h = 1.0 / nx
+    cfg = mb.OuterConfig(tau=5e-3, penalty=mb.PenaltySpec.tv_smoothed(0.05),
+                         inner_stop=mb.StoppingConfig.max_iterations(6), inner_cap=6,
+                         rel_decrease_threshold=0.0, max_outer=3, mg_levels=4)
+
+    def run(op, shp, gl, ctx_dev=None):
+        s = mb.OuterSolver(op, shp, h, cfg)
+        gd = torch.from_numpy(gl).cuda()
+        fa = torch.zeros(gl.size, dtype=torch.float64, device="cuda")
+        fb = torch.empty_like(fa)
+        out = []
+        for _ in range(3):
+            st = s.step(gd, fa, fb)
+            torch.cuda.synchronize()
+            out.append((st.penalty_value, st.eps_used, st.inner_iterations, fb.cpu().numpy().copy()))
+            fa, fb = fb, fa
+        return out
+
+    ref = run(mb.SeparableGaussianBlur(shape, taps=taps), shape, g)
+
+    def fn(r, ctx, sl):
+        loc = (nx, ny, sl.stop - sl.start)
+        return run(mb.SeparableGaussianBlur(loc, taps=taps, ctx=ctx), loc, planes(g, shape)[sl].ravel())
+
+    out = run_ranks(P, nz, fn)
+    for k in range(3):
+        assert all(o[k][:3] == ref[k][:3] for o in out)
+        assert np.array_equal(np.concatenate([o[k][3] for o in out]), ref[k][3])
