@@ -1,9 +1,9 @@
 // dense.cu -- K_A' / K_B': the dense (fDOT-like) sensitivity operator and the
 // identity operator (DenseOperator / IdentityOperator, linop.cpp:56-84).
 //
-// A x : one CTA (32 warps) per NR rows.  Each row dot is the canonical
-//       reduction over 32-column segments (tree32 per segment, then tree-32
-//       levels), so y_i is bit-identical to the oracle's DEVICE-order dot.
+// A x : a warp per (row, column part); each row dot is the canonical reduction
+//       over 32-column segments (tree32 per segment, then tree-32 levels), so y_i
+//       is bit-identical to the oracle's DEVICE-order dot.
 // A^T y: one thread per column, rows in 8 fixed chunks, sequential inside a
 //       chunk (the reference's per-row axpy order, linop.cpp:78-84), chunk
 //       partials added in order -- deterministic and row-shardable.
@@ -13,63 +13,106 @@
 namespace mlsqr_b200 {
 
 // ---------------------------------------------------------------------------
-// y = A (x*sx) for NR rows per CTA; level-1 partials staged in smem.
+// y = A (x*sx) in the canonical order with ~5 instructions per element instead of ~20:
+// a CTA owns 8 rows x one column part and walks its 1024-column groups in lockstep.
+// Per group the x slice and each warp's row slice are loaded coalesced (16-byte loads)
+// into shared memory laid out as 32 segments of 34 doubles; lane l then reads segment l
+// with conflict-free 16-byte loads, forms its 32 products and reduces them with
+// tree32_serial (the same pairing as a 32-lane shuffle tree), and the warp trees the 32
+// segment partials (level 1) into a global [rows x G1] buffer.  gemv_top_kernel runs the
+// remaining tree-32 levels of each row.
 // ---------------------------------------------------------------------------
-template <int NR>
-__global__ void __launch_bounds__(1024) gemv_kernel(const double* __restrict__ A,
-                                                    const double* __restrict__ x, size_t rows,
-                                                    size_t cols, double* __restrict__ y,
-                                                    const double* sx, const int* gate) {
+constexpr int kGemvWarps = 8;
+constexpr int kSegPitch = 34;                  // padded segment pitch (doubles)
+constexpr int kGrpDoubles = 32 * kSegPitch;    // one 1024-column group
+
+__global__ void __launch_bounds__(256, 2) gemv_l1_kernel(const double* __restrict__ A,
+                                                         const double* __restrict__ x, size_t rows,
+                                                         size_t cols, int parts, double* __restrict__ l1,
+                                                         const double* sx, const int* gate) {
   if (gate && *gate == 0) return;
-  extern __shared__ double l1[];  // NR x G1 level-1 partials
-  const size_t r0 = (size_t)blockIdx.x * NR;
+  extern __shared__ __align__(16) double gsm[];
+  double* xs = gsm;                       // [kGrpDoubles]
+  double* as = gsm + kGrpDoubles;         // [kGemvWarps][kGrpDoubles]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const size_t nseg = (cols + 31) / 32;
-  const size_t G1 = (nseg + 31) / 32;
+  const size_t rg = blockIdx.x / (size_t)parts, part = blockIdx.x % (size_t)parts;
+  const size_t row = rg * kGemvWarps + w;
+  const bool live = row < rows;
+  const size_t nseg = (cols + 31) / 32, G1 = (nseg + 31) / 32;
+  const size_t gp = (G1 + parts - 1) / parts;
+  const size_t g0 = part * gp, g1 = g0 + gp < G1 ? g0 + gp : G1;
   const double s = sx ? *sx : 1.0;
-  for (size_t g = w; g < G1; g += 32) {
-    double keep[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) keep[r] = 0.0;
-    for (int k = 0; k < 32; ++k) {
-      const size_t col = (g * 32 + k) * 32 + lane;
-      double xv = 0.0;
-      if (col < cols) {
-        xv = x[col];
-        if (sx) xv = xv * s;
+  const double* __restrict__ Ar = A + (live ? row : 0) * cols;
+  const bool vec = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  // element e (0..1023) of a group sits at segment e / 32, slot e % 32
+  auto sidx = [](int e) { return (e >> 5) * kSegPitch + (e & 31); };
+  for (size_t g = g0; g < g1; ++g) {
+    const size_t base = g * 1024;
+    const bool full = vec && base + 1024 <= cols;
+    __syncthreads();  // the previous group's readers are done
+    if (full) {
+      {  // x slice: 512 pairs over 256 threads
+        const int e = 2 * (int)threadIdx.x;
+        const double2 v0 = __ldg(reinterpret_cast<const double2*>(x + base + e));
+        const double2 v1 = __ldg(reinterpret_cast<const double2*>(x + base + 512 + e));
+        *reinterpret_cast<double2*>(xs + sidx(e)) = v0;
+        *reinterpret_cast<double2*>(xs + sidx(512 + e)) = v1;
       }
+      if (live) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        double v = 0.0;
-        if (col < cols && r0 + r < rows) v = A[(r0 + r) * cols + col] * xv;
-        v = tree32(v);
-        v = __shfl_sync(kFull, v, 0);
-        if (lane == k) keep[r] = v;
+        for (int b = 0; b < 16; ++b) {
+          const int e = 64 * b + 2 * lane;
+          *reinterpret_cast<double2*>(as + w * kGrpDoubles + sidx(e)) = *reinterpret_cast<const double2*>(Ar + base + e);
+        }
       }
+    } else {
+      for (int e = threadIdx.x; e < 1024; e += 32 * kGemvWarps) xs[sidx(e)] = base + e < cols ? x[base + e] : 0.0;
+      if (live)
+        for (int e = lane; e < 1024; e += 32) as[w * kGrpDoubles + sidx(e)] = base + e < cols ? Ar[base + e] : 0.0;
     }
+    __syncthreads();
+    if (live) {
+      const double* ap = as + w * kGrpDoubles + lane * kSegPitch;
+      const double* xp = xs + lane * kSegPitch;
+      double p[32];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const double t = tree32(keep[r]);
-      if (lane == 0) l1[r * G1 + g] = t;
+      for (int j = 0; j < 32; j += 2) {
+        const double2 av = *reinterpret_cast<const double2*>(ap + j);
+        double2 xv = *reinterpret_cast<const double2*>(xp + j);
+        if (sx) {
+          xv.x = xv.x * s;
+          xv.y = xv.y * s;
+        }
+        p[j] = av.x * xv.x;
+        p[j + 1] = av.y * xv.y;
+      }
+      // zero extension past cols: those products are 0 * 0 = +0 (staged zeros)
+      const double t = tree32(tree32_serial(p));  // segment partial, then level 1 across the group
+      if (lane == 0) l1[row * G1 + g] = t;
     }
   }
-  __syncthreads();
-  // remaining levels over the G1 level-1 partials of each row (serial trees)
-  if (threadIdx.x < NR && r0 + threadIdx.x < rows) {
-    double* L = l1 + threadIdx.x * G1;
-    size_t J = G1;  // level 1 is done; continue while more than one value remains
-    while (J > 1) {
-      const size_t G = (J + 31) / 32;
-      for (size_t q = 0; q < G; ++q) {
-        double v[32];
+}
+
+// levels >= 2 of each row's canonical tree over its G1 level-1 partials
+__global__ void gemv_top_kernel(double* __restrict__ l1, size_t rows, size_t G1, double* __restrict__ y,
+                                const int* gate) {
+  if (gate && *gate == 0) return;
+  const size_t row = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  double* L = l1 + row * G1;
+  size_t J = G1;
+  while (J > 1) {
+    const size_t G = (J + 31) / 32;
+    for (size_t q = 0; q < G; ++q) {
+      double v[32];
 #pragma unroll
-        for (int l = 0; l < 32; ++l) v[l] = (q * 32 + l < J) ? L[q * 32 + l] : 0.0;
-        L[q] = tree32_serial(v);
-      }
-      J = G;
+      for (int l = 0; l < 32; ++l) v[l] = (q * 32 + l < J) ? L[q * 32 + l] : 0.0;
+      L[q] = tree32_serial(v);
     }
-    y[r0 + threadIdx.x] = L[0];
+    J = G;
   }
+  y[row] = L[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -195,25 +238,30 @@ class DenseOp final : public Op {
     sol_shape = RowShape{L, cols / L};
     a_.alloc(rows * cols);
     tmp_.alloc(rows > cols ? rows : cols);
-    const size_t nseg = (cols + 31) / 32, G1 = (nseg + 31) / 32;
-    smem_ = sizeof(double) * kNR * (G1 < 1 ? 1 : G1);
-    if (smem_ > 48 * 1024)
-      MLSQR_CUDA(cudaFuncSetAttribute(gemv_kernel<kNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
+    l1_.alloc(rows * (((cols + 31) / 32 + 31) / 32));
+    // set outside any graph capture (the first A x may run inside the captured LSQR iteration)
+    MLSQR_CUDA(cudaFuncSetAttribute(gemv_l1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
   }
-  static constexpr int kNR = 4;
-  size_t smem_ = 0;
+  static constexpr int kSmem = sizeof(double) * kGrpDoubles * (1 + kGemvWarps);
   DevBuf<double> a_;
 
   int tclass() const override { return MLSQR_TCLASS_DENSE; }
 
   void apply(const double* x, double* y, const Epi& e) override {
     TimedRegion tr(ctx, MLSQR_TCLASS_DENSE);
-    constexpr int NR = kNR;
-    const size_t smem = smem_;
     double* dst = e.old ? tmp_.p : y;
-    gemv_kernel<NR><<<(unsigned)((rows + NR - 1) / NR), 1024, smem, ctx->stream>>>(
-        a_.p, x, rows, cols, dst, e.sx, e.gate);
-    ctx->count();
+    const size_t nseg = (cols + 31) / 32, G1 = (nseg + 31) / 32;
+    // column parts per 8-row group: enough CTAs for ~7 waves of 2 CTAs per SM
+    const size_t groups = (rows + kGemvWarps - 1) / kGemvWarps;
+    const size_t want = (size_t)ctx->sm_count * 2 * 7;
+    size_t parts = (want + groups - 1) / groups;
+    if (parts < 1) parts = 1;
+    if (parts > G1) parts = G1;
+    const size_t ctas = (rows + kGemvWarps - 1) / kGemvWarps * parts;
+    gemv_l1_kernel<<<(unsigned)ctas, 32 * kGemvWarps, kSmem, ctx->stream>>>(a_.p, x, rows, cols, (int)parts, l1_.p, e.sx,
+                                                                       e.gate);
+    gemv_top_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, ctx->stream>>>(l1_.p, rows, G1, dst, e.gate);
+    ctx->count(2);
     ctx->check_launch();
     if (e.old || e.seg) {
       Epi e2 = e;
@@ -245,6 +293,8 @@ class DenseOp final : public Op {
  private:
   DevBuf<double> tmp_;
   DevBuf<double> part_, gath_;  // row shards: local chunk partials, all 8 gathered
+ public:
+  DevBuf<double> l1_;           // [rows x G1] level-1 partials of A x
 };
 
 Op* make_dense(Ctx* c, size_t rows, size_t cols, const double* a, bool a_on_device,
