@@ -130,22 +130,12 @@ class GpuSpdMap final : public mlsqr::SpdMap {
   mlsqr_pc* pc_;
 };
 
-// Device-resident mlsqr with the reference's signature semantics (krylov.hpp:94-95).
-inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap& m,
-                                    std::span<const double> g, double tau,
-                                    const mlsqr::StoppingConfig& stop) {
-  stop.validate();
-  if (g.size() != a.n_rows()) throw mlsqr::DimensionError("right-hand side length mismatch");
-  mlsqr_stop s{stop.atol, stop.btol, stop.conlim, stop.delta, stop.eta, stop.max_iters,
-               stop.use_s1, stop.use_s2, stop.use_s3, stop.use_s4};
-  mlsqr::SolveResult r;
-  r.solution.assign(a.n_cols(), 0.0);
-  std::vector<mlsqr_iter_rec> tr(static_cast<std::size_t>(stop.max_iters));
-  std::vector<double> al(static_cast<std::size_t>(stop.max_iters) + 1), be(static_cast<std::size_t>(stop.max_iters) + 2);
-  mlsqr_solve_info info{};
-  check(mlsqr_solve(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
-                    be.data(), &info, MLSQR_HOST),
-        info.breakdown_iteration);
+namespace detail {
+inline mlsqr_stop to_c(const mlsqr::StoppingConfig& stop) {
+  return {stop.atol, stop.btol, stop.conlim, stop.delta, stop.eta, stop.max_iters,
+          stop.use_s1, stop.use_s2, stop.use_s3, stop.use_s4};
+}
+inline void fill_trace(mlsqr::SolveResult& r, const std::vector<mlsqr_iter_rec>& tr, const mlsqr_solve_info& info) {
   r.iterations = info.iterations;
   static const mlsqr::StopReason kReasons[] = {mlsqr::StopReason::s1, mlsqr::StopReason::s2,
                                                mlsqr::StopReason::s3, mlsqr::StopReason::s4,
@@ -166,9 +156,65 @@ inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap&
     rec.beta = t.beta;
     r.trace.iterations.push_back(rec);
   }
+}
+}  // namespace detail
+
+// Device-resident mlsqr with the reference's signature semantics (krylov.hpp:94-95);
+// opts.store_basis also returns the right basis (SolveOptions, krylov.hpp:77-79).
+inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap& m,
+                                    std::span<const double> g, double tau,
+                                    const mlsqr::StoppingConfig& stop, const mlsqr::SolveOptions& opts = {}) {
+  stop.validate();
+  if (g.size() != a.n_rows()) throw mlsqr::DimensionError("right-hand side length mismatch");
+  const mlsqr_stop s = detail::to_c(stop);
+  mlsqr::SolveResult r;
+  const std::size_t n = a.n_cols(), k = static_cast<std::size_t>(stop.max_iters);
+  r.solution.assign(n, 0.0);
+  std::vector<mlsqr_iter_rec> tr(k);
+  std::vector<double> al(k + 1), be(k + 2), basis;
+  mlsqr_solve_info info{};
+  if (opts.store_basis) {
+    basis.assign((k + 1) * n, 0.0);
+    check(mlsqr_solve_basis(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
+                            be.data(), basis.data(), &info, MLSQR_HOST),
+          info.breakdown_iteration);
+  } else {
+    check(mlsqr_solve(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
+                      be.data(), &info, MLSQR_HOST),
+          info.breakdown_iteration);
+  }
+  detail::fill_trace(r, tr, info);
   r.bidiag.alphas.assign(al.begin(), al.begin() + info.n_alphas);
   r.bidiag.betas.assign(be.begin(), be.begin() + info.n_betas);
+  for (int j = 0; opts.store_basis && j < info.n_alphas; ++j)
+    r.bidiag.basis.emplace_back(basis.begin() + j * n, basis.begin() + (j + 1) * n);
   return r;
+}
+
+// cg_normal (krylov.hpp:116-122) on the device; M is the V-cycle map's level-0 operator
+// (its update() state), m may be null when tau == 0.
+inline mlsqr::SolveResult gpu_cg_normal(const GpuLinearOperator& a, const GpuSpdMap* m, double tau,
+                                        std::span<const double> g, const mlsqr::StoppingConfig& stop) {
+  stop.validate();
+  if (g.size() != a.n_rows()) throw mlsqr::DimensionError("right-hand side length mismatch");
+  const mlsqr_stop s = detail::to_c(stop);
+  mlsqr::SolveResult r;
+  r.solution.assign(a.n_cols(), 0.0);
+  std::vector<mlsqr_iter_rec> tr(static_cast<std::size_t>(stop.max_iters));
+  mlsqr_solve_info info{};
+  check(mlsqr_cg_normal_solve(a.handle(), m ? m->handle() : nullptr, g.data(), tau, &s, r.solution.data(),
+                              tr.data(), &info, MLSQR_HOST),
+        info.breakdown_iteration);
+  detail::fill_trace(r, tr, info);
+  return r;
+}
+
+// solve_projected (krylov.hpp:124-127) through the library (bit-identical to the reference)
+inline std::vector<double> gpu_solve_projected(const mlsqr::BidiagEntries& bd, double beta1, double tau) {
+  std::vector<double> y(bd.alphas.size());
+  check(mlsqr_solve_projected(bd.alphas.data(), bd.alphas.size(), bd.betas.data(), bd.betas.size(), beta1, tau,
+                              y.data()));
+  return y;
 }
 
 #endif  // MLSQR_B200_WITH_REFERENCE_API

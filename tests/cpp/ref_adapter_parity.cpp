@@ -93,6 +93,47 @@ int main() {
   EXPECT(worst_a < 1e-9);
   EXPECT(relf < 1e-6);
 
+  // multi-tau: the library's solve_projected equals the reference's bit for bit, and the
+  // device basis re-expands to the device solve
+  for (double tau : {0.0, 1e-3, 1e-2, 0.5}) {
+    const auto y_ref = mlsqr::solve_projected(r_cpu.bidiag, r_cpu.bidiag.betas[0], tau);
+    EXPECT(mlsqr_b200::gpu_solve_projected(r_cpu.bidiag, r_cpu.bidiag.betas[0], tau) == y_ref);
+  }
+  SolveOptions so;
+  so.store_basis = true;
+  const auto r_basis = mlsqr_b200::gpu_mlsqr(gpu_op, vc, bundle.g, 1e-2, stop, so);
+  EXPECT(r_basis.solution == r_dev.solution);
+  EXPECT(r_basis.bidiag.basis.size() == r_basis.bidiag.alphas.size());
+  {
+    const auto y = mlsqr_b200::gpu_solve_projected(r_basis.bidiag, r_basis.bidiag.betas[0], 1e-2);
+    const auto f = mlsqr::reconstruct_from_basis(r_basis.bidiag, y);
+    double n2 = 0.0, d2 = 0.0;
+    for (std::size_t i = 0; i < f.size(); ++i) {
+      n2 += (f[i] - r_basis.solution[i]) * (f[i] - r_basis.solution[i]);
+      d2 += r_basis.solution[i] * r_basis.solution[i];
+    }
+    std::printf("stored-basis re-solve: rel %.3e\n", std::sqrt(n2 / d2));
+    EXPECT(std::sqrt(n2 / d2) < 1e-8);
+  }
+
+  // cg_normal: device vs the reference's own cg_normal with the same M (assembled at the
+  // truth with the V-cycle's shift); canonical vs sequential reductions -> rounding level
+  {
+    const double eps = vc.update(bundle.f_true, MLSQR_PEN_TV, 0.05);
+    SparseSpd m2 = assemble_m(bundle.grid, bundle.f_true, PenaltySpec::tv_smoothed(0.05), 0.0).with_shift(eps);
+    const auto st10 = StoppingConfig::max_iterations(10);
+    const auto c_ref = mlsqr::cg_normal(cpu_op, m2, 1e-2, bundle.g, st10);
+    const auto c_dev = mlsqr_b200::gpu_cg_normal(gpu_op, &vc, 1e-2, bundle.g, st10);
+    double n2 = 0.0, d2 = 0.0;
+    for (std::size_t i = 0; i < c_ref.solution.size(); ++i) {
+      n2 += (c_dev.solution[i] - c_ref.solution[i]) * (c_dev.solution[i] - c_ref.solution[i]);
+      d2 += c_ref.solution[i] * c_ref.solution[i];
+    }
+    std::printf("cg_normal device vs reference: rel f %.3e\n", std::sqrt(n2 / d2));
+    EXPECT(c_dev.iterations == c_ref.iterations);
+    EXPECT(std::sqrt(n2 / d2) < 1e-9);
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -481,3 +481,17 @@ def test_store_basis_lsqr_device_tensors(ctx):
     fr = mb.reconstruct_from_basis(res.basis, y)
     assert torch.is_tensor(fr)
     assert float((fr - res.solution).norm()) <= 1e-8 * float(res.solution.norm())
+
+
+def test_reference_adapter_parity_binary(ctx):
+    """tests/cpp/ref_adapter_parity.cpp (built by `make -C oracle adapter` where the reference
+    sources exist): the unmodified reference mlsqr driving the B200 blur / V-cycle through the
+    C++ adapters, gpu_mlsqr / gpu_cg_normal / gpu_solve_projected against the reference."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "ref_adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("adapter driver not built (needs the reference sources: make -C oracle adapter)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK (0 failures)" in r.stdout, r.stdout + r.stderr
