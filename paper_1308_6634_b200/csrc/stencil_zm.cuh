@@ -13,19 +13,21 @@
 // can never reach -0).  Results are bit-identical to the oracle.
 
 // iterate value at fine index j (plus the prolongated coarse correction)
-template <int D, bool PROLONG>
+// I: element index type -- int where the level (with guards) fits 2^31 elements: every
+// access is then one IMAD.WIDE instead of a 64-bit add chain (same loads, same bits)
+template <int D, bool PROLONG, typename I = long>
 __device__ __forceinline__ double xv_zm(const double* __restrict__ x, const double* __restrict__ xc,
-                                        int cnx, int cny, int xx, int yy, int zz, long j) {
+                                        int cnx, int cny, int xx, int yy, int zz, I j) {
   double v = x[j];
   if (PROLONG) {
     // floor division: the ghost plane z = -1 of a slab belongs to coarse ghost plane -1
     const int Z = D >= 3 ? (zz >> 1) : 0, Y = D >= 2 ? yy / 2 : 0;
-    v = v + xc[((long)Z * cny + Y) * cnx + xx / 2];
+    v = v + xc[((I)Z * cny + Y) * cnx + xx / 2];
   }
   return v;
 }
 
-template <int D, int MODE>
+template <int D, int MODE, typename I = long>
 __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __restrict__ x,
                                                        const double* __restrict__ xc, int cnx, int cny,
                                                        const double* __restrict__ b,
@@ -39,14 +41,14 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
   const int z0 = blockIdx.z * zc;
   const int z1 = min(L.nz, z0 + zc);
   const int nx = L.nx;
-  const long nxy = (long)nx * L.ny;
+  const I nxy = (I)nx * L.ny;
   const bool ix = xx < nx;
   const double eps = *L.eps;
   const double* __restrict__ cx = L.cx;
   const double* __restrict__ cy = L.cy;
   const double* __restrict__ cz = L.cz;
   const long chunks = (nx + 31) / 32;
-  long i = ((long)z0 * L.ny + yy) * nx + (ix ? xx : nx - 1);
+  I i = ((I)z0 * L.ny + yy) * nx + (ix ? xx : nx - 1);
   double xm = 0.0, xcur = 0.0, xn = 0.0, czm = 0.0;
   double bc = b[i], cxc = cx[i], cyc = 0.0, czc = 0.0;
   if (D >= 2) cyc = cy[i];
@@ -55,15 +57,15 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
     czm = cz[i - nxy];  // guard zone below plane 0
   }
   if (MODE != kFirst) {
-    xcur = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z0, i);
+    xcur = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z0, i);
     if (D >= 3) {
-      xm = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z0 - 1, i - nxy);
-      xn = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z0 + 1, i + nxy);
+      xm = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z0 - 1, i - nxy);
+      xn = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z0 + 1, i + nxy);
     }
   }
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
-      const long j = i + 3 * nxy;
+      const I j = i + 3 * nxy;
       prefetch_l2(b + j);
       prefetch_l2(cx + j);
       prefetch_l2(cy + j);
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
       if (D >= 2) cyn = cy[i + nxy];
       if (D >= 3) czn = cz[i + nxy];
       if (D >= 3 && MODE != kFirst && MODE != kProlongOnly)
-        xnn = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z + 2, i + 2 * nxy);  // guard covers z+2 = nz
+        xnn = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z + 2, i + 2 * nxy);  // guard covers z+2 = nz
     }
     double v;
     if (MODE == kProlongOnly) {
@@ -107,11 +109,11 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
         // m_row order: z-, y-, x-, diag, x+, y+, z+
         double acc = 0.0;
         if (D >= 3) acc = acc + -czm * xm;
-        if (D >= 2) acc = acc + -cym * xv_zm<D, P>(x, xc, cnx, cny, xx, yy - 1, z, i - nx);
-        acc = acc + -cxm * xv_zm<D, P>(x, xc, cnx, cny, xx - 1, yy, z, i - 1);
+        if (D >= 2) acc = acc + -cym * xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy - 1, z, i - nx);
+        acc = acc + -cxm * xv_zm<D, P, I>(x, xc, cnx, cny, xx - 1, yy, z, i - 1);
         acc = acc + d * xcur;
-        acc = acc + -cxc * xv_zm<D, P>(x, xc, cnx, cny, xx + 1, yy, z, i + 1);
-        if (D >= 2) acc = acc + -cyc * xv_zm<D, P>(x, xc, cnx, cny, xx, yy + 1, z, i + nx);
+        acc = acc + -cxc * xv_zm<D, P, I>(x, xc, cnx, cny, xx + 1, yy, z, i + 1);
+        if (D >= 2) acc = acc + -cyc * xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy + 1, z, i + nx);
         if (D >= 3) acc = acc + -czc * xn;
         v = xcur + (omega * (bc - acc)) / d;
       }
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
     czm = czc;
     xm = xcur;
     if (MODE == kProlongOnly) {
-      if (z + 1 < z1) xcur = xv_zm<D, P>(x, xc, cnx, cny, xx, yy, z + 1, i + nxy);
+      if (z + 1 < z1) xcur = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z + 1, i + nxy);
     } else {
       xcur = xn;
       xn = xnn;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
 // dz, dy, dx nested) of r = b - M x.  Fine threads compute r; the (even x, even y) thread
 // of each 2 x 2 patch accumulates the children in the canonical order across the two
 // fine planes of the coarse cell.
-template <int D>
+template <int D, typename I = long>
 __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* __restrict__ x,
                                                           const double* __restrict__ b, int cnx, int cny,
                                                           double* __restrict__ bcoarse, const int* gate,
@@ -155,13 +157,13 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
   const int z0 = blockIdx.z * zc;
   const int z1 = min(L.nz, z0 + zc);
   const int nx = L.nx;
-  const long nxy = (long)nx * L.ny;
+  const I nxy = (I)nx * L.ny;
   const bool ok = xx < nx && yy < L.ny;
   const double eps = *L.eps;
   const double* __restrict__ cx = L.cx;
   const double* __restrict__ cy = L.cy;
   const double* __restrict__ cz = L.cz;
-  long i = ((long)z0 * L.ny + (yy < L.ny ? yy : L.ny - 1)) * nx + (xx < nx ? xx : nx - 1);
+  I i = ((I)z0 * L.ny + (yy < L.ny ? yy : L.ny - 1)) * nx + (xx < nx ? xx : nx - 1);
   double xm = 0.0, xcur = x[i], xn = 0.0, czm = 0.0;
   double bc = b[i], cxc = cx[i], cyc = 0.0, czc = 0.0;
   if (D >= 2) cyc = cy[i];
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
   double s = 0.0;
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
-      const long j = i + 3 * nxy;
+      const I j = i + 3 * nxy;
       prefetch_l2(b + j);
       prefetch_l2(cx + j);
       prefetch_l2(cy + j);
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
       }
       if (D < 3 || (z % 2 == 1)) {
         const int Z = D >= 3 ? z / 2 : 0, Y = D >= 2 ? yy / 2 : 0;
-        bcoarse[((long)Z * cny + Y) * cnx + xx / 2] = s;
+        bcoarse[((I)Z * cny + Y) * cnx + xx / 2] = s;
       }
     }
     if (D >= 2) __syncthreads();

@@ -423,6 +423,9 @@ class VCycle final : public Pc {
   }
 
  private:
+  // 32-bit element indices when the level, its guard planes and the kernels' look-ahead fit
+  static bool fits_i32(const Level& L) { return ((long)L.nz + 4) * L.nx * L.ny + 1024 < 2147483647L; }
+
   template <int MODE>
   void sweep(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
              const int* gate) {
@@ -435,7 +438,9 @@ class VCycle final : public Pc {
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
     const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
-    if (dims_ == 3)
+    if (dims_ == 3 && fits_i32(L))
+      sweep_zm_kernel<3, MODE, int><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
+    else if (dims_ == 3)
       sweep_zm_kernel<3, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
     else if (dims_ == 2)
       sweep_zm_kernel<2, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
@@ -449,7 +454,9 @@ class VCycle final : public Pc {
     Level& C = lv_[(size_t)l + 1];
     const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
-    if (dims_ == 3)
+    if (dims_ == 3 && fits_i32(L))
+      restrict_zm_kernel<3, int><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
+    else if (dims_ == 3)
       restrict_zm_kernel<3><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
     else if (dims_ == 2)
       restrict_zm_kernel<2><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
