@@ -308,12 +308,11 @@ template <int R>
 static void launch_b3(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
                       const EpiArgs& a) {
   using C = B3P<R>;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr;  // operators may be built on several threads (loopback ranks)
+  std::call_once(attr, [] {
     MLSQR_CUDA(cudaFuncSetAttribute(blur3d_pipe<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     MLSQR_CUDA(cudaFuncSetAttribute(blur3d_pipe<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  });
   const int tiles_x = (nx + C::TX - 1) / C::TX, tiles_y = (ny + C::TY - 1) / C::TY;
   const int tiles = tiles_x * tiles_y;
   // z chunk minimising (items per CTA) x (phases per item) on one CTA per SM
