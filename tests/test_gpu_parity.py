@@ -495,3 +495,57 @@ def test_reference_adapter_parity_binary(ctx):
         pytest.skip("adapter driver not built (needs the reference sources: make -C oracle adapter)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "OK (0 failures)" in r.stdout, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------------------
+# the reference's Krylov property tests (test_krylov.cpp), on the device solvers
+# ---------------------------------------------------------------------------
+def _small_problem(dev, shape=(16, 16), eps_rel=1e-8):
+    n = int(np.prod(shape))
+    rng = np.random.default_rng(21)
+    f = rng.uniform(0, 1, n)
+    taps = dev.taps(shape[0], 2.0 / shape[0], radius=4)
+    A = np.stack([dev.blur(2, shape, taps).apply(e) for e in np.eye(n)], 1)
+    g = A @ f + 0.01 * rng.standard_normal(n)
+    grid = dev.grid(2, shape, 1.0 / shape[0])
+    cx, cy, cz = dev.edge_coeffs(grid, f, "tv", 0.05)
+    eps = eps_rel * dev.max_diag(grid, cx, cy, cz)
+    M = np.stack([dev.m_apply(grid, cx, cy, cz, eps, e) for e in np.eye(n)], 1)
+    return shape, n, taps, A, g, f, M, eps
+
+
+def test_three_solvers_match_dense_solution(ctx, dev):
+    """test_krylov.cpp:366-386: mlsqr (exact M^-1 plug-in), cg_normal and the dense direct
+    solution of (A^T A + tau M) f = A^T g agree to 1e-6; lsqr equals the dense normal solve
+    with M = I (test_krylov.cpp:39-47, 1e-8)."""
+    shape, n, taps, A, g, f, M, eps = _small_problem(dev)
+    tau = 1e-2
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    f_direct = np.linalg.solve(A.T @ A + tau * M, A.T @ g)
+    Minv = np.linalg.inv(M)
+    exact = mb.CallbackMap(n, lambda p: Minv @ p)
+    r_m = mb.mlsqr(op, exact, g, tau, mb.StoppingConfig.max_iterations(3 * n))
+    vc = mb.VCycleMap(shape, 1.0 / shape[0], 2)
+    assert vc.update(f, mb.PenaltySpec.tv_smoothed(0.05)) == eps  # the same M, matrix-free
+    r_c = mb.cg_normal(op, vc, tau, g, mb.StoppingConfig(atol=1e-14, max_iters=6 * n, use_s2=True))
+    for r in (r_m, r_c):
+        assert np.linalg.norm(r.solution - f_direct) <= 1e-6 * np.linalg.norm(f_direct)
+    f_lsqr = np.linalg.solve(A.T @ A + tau * np.eye(n), A.T @ g)
+    r_l = mb.lsqr(op, g, tau, mb.StoppingConfig.max_iterations(3 * n))
+    assert np.linalg.norm(r_l.solution - f_lsqr) <= 1e-8 * np.linalg.norm(f_lsqr)
+
+
+def test_mlsqr_basis_orthogonality_and_monotone_residual(ctx, dev):
+    """test_krylov.cpp:332-364 (drift of the M-orthonormal basis <= 1e-4; 12 iterations, before
+    the Lanczos process re-finds converged directions on this small blur)
+    and :210-223 (the damped residual never increases), with the exact M^-1 plug-in and a
+    well-conditioned M (the auto shift's 1e8 conditioning destroys any M-orthogonality)."""
+    shape, n, taps, A, g, f, M, eps = _small_problem(dev, shape=(24, 24), eps_rel=0.1)
+    Minv = np.linalg.inv(M)
+    r = mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), mb.CallbackMap(n, lambda p: Minv @ p), g, 1e-2,
+                 mb.StoppingConfig.max_iterations(12), store_basis=True)
+    V = r.basis
+    G = V @ M @ V.T
+    assert np.abs(G - np.eye(V.shape[0])).max() <= 1e-4
+    res = [t.res_damped for t in r.trace]
+    assert all(res[i + 1] <= res[i] * (1 + 1e-12) for i in range(len(res) - 1))

@@ -161,3 +161,27 @@ def test_phantoms_and_generators(orc):
     gs, gd, a = orc.fdot(4, 3, 2, 1.0, 7)
     assert a.shape == (6, 64) and (a > 0).all()
     assert np.array_equal(a[1 * 2 + 1], gs[64:128] * gd[64:128])
+
+
+def test_algorithm1_equals_algorithm2(orc):
+    """test_krylov.cpp:75-97: explicit-factor preconditioned LSQR (Algorithm 1: plain LSQR on
+    A R^-1 with M = R^T R, f = R^-1 x) and the factorization-free mlsqr (Algorithm 2) agree to
+    1e-8 over 15 iterations -- here with the oracle's own lsqr and Cholesky map."""
+    rng = np.random.default_rng(12)
+    n, m = 40, 60
+    A = rng.standard_normal((m, n)) / 8
+    g = A @ rng.uniform(-1, 1, n) + 0.01 * rng.standard_normal(m)
+    grid = orc.grid(1, (n,), 1.0 / n)
+    cx, cy, cz = orc.edge_coeffs(grid, rng.uniform(0, 1, n), "tv", 0.1)
+    eps = 0.1 * orc.max_diag(grid, cx, cy, cz)      # a well-conditioned M (the comparison is
+    M = np.stack([orc.m_apply(grid, cx, cy, cz, eps, e) for e in np.eye(n)], 1)  # of two algorithms)
+    R = np.linalg.cholesky(M).T                       # M = R^T R
+    from scipy.linalg import solve_triangular
+    Abar = solve_triangular(R, A.T, trans="T").T      # A R^-1
+    st = stop(15)
+    for tau in (0.0, 1e-2):
+        r2 = orc.mlsqr(orc.dense(A), orc.chol_map(M), g, tau, st)
+        r1 = orc.mlsqr(orc.dense(Abar), None, g, tau, st, lsqr=True)
+        f1 = solve_triangular(R, r1.f)
+        assert np.linalg.norm(f1 - r2.f) <= 1e-8 * np.linalg.norm(r2.f)
+        assert np.max(np.abs(r1.alphas - r2.alphas) / r2.alphas) < 1e-8
