@@ -176,6 +176,7 @@ typedef struct {
   int stop_reason;          /* MLSQR_STOP_* */
   int n_alphas, n_betas;    /* BidiagEntries sizes after trim (krylov.cpp:182-186) */
   int breakdown_iteration;  /* BreakdownError::iteration() when MLSQR_EBREAKDOWN */
+  int n_left_basis;         /* left basis vectors stored by mlsqr_solve_basis (else 0) */
 } mlsqr_solve_info;
 
 /* mlsqr (krylov.hpp:94-95, krylov.cpp:335-440): device-resident loop.
@@ -191,11 +192,12 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
 
 /* mlsqr / lsqr with SolveOptions::store_basis (krylov.hpp:77-79): additionally writes the right
  * basis vtilde_1 .. vtilde_k (the scaled v of krylov.cpp:375-377, 421-423) as the rows of
- * basis[(max_iters + 1) * n_cols] (ptr_kind memory); info->n_alphas rows are valid.
- * pc == NULL runs lsqr. */
+ * basis[(max_iters + 1) * n_cols] and, when left_basis is non-NULL, the left basis u_1 .. u_{k+1}
+ * (krylov.cpp:375-377, 421-425) as the rows of left_basis[(max_iters + 1) * n_rows]
+ * (ptr_kind memory); info->n_alphas / info->n_left_basis rows are valid.  pc == NULL runs lsqr. */
 int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
                       double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
-                      mlsqr_solve_info* info, int ptr_kind);
+                      double* left_basis, mlsqr_solve_info* info, int ptr_kind);
 /* solve_projected (krylov.hpp:124-127, krylov.cpp:631-678): y[k] minimising
  * |[B_k; sqrt(tau) I] y - beta1 e1| from k alphas and k+1 betas (host arithmetic; one
  * bidiagonalization serves every tau).  No device needed. */

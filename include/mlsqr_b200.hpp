@@ -171,12 +171,13 @@ inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap&
   const std::size_t n = a.n_cols(), k = static_cast<std::size_t>(stop.max_iters);
   r.solution.assign(n, 0.0);
   std::vector<mlsqr_iter_rec> tr(k);
-  std::vector<double> al(k + 1), be(k + 2), basis;
+  std::vector<double> al(k + 1), be(k + 2), basis, left;
   mlsqr_solve_info info{};
   if (opts.store_basis) {
     basis.assign((k + 1) * n, 0.0);
+    left.assign((k + 1) * a.n_rows(), 0.0);
     check(mlsqr_solve_basis(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
-                            be.data(), basis.data(), &info, MLSQR_HOST),
+                            be.data(), basis.data(), left.data(), &info, MLSQR_HOST),
           info.breakdown_iteration);
   } else {
     check(mlsqr_solve(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
@@ -188,6 +189,9 @@ inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap&
   r.bidiag.betas.assign(be.begin(), be.begin() + info.n_betas);
   for (int j = 0; opts.store_basis && j < info.n_alphas; ++j)
     r.bidiag.basis.emplace_back(basis.begin() + j * n, basis.begin() + (j + 1) * n);
+  const std::size_t mr = a.n_rows();
+  for (int j = 0; opts.store_basis && j < info.n_left_basis; ++j)
+    r.bidiag.left_basis.emplace_back(left.begin() + j * mr, left.begin() + (j + 1) * mr);
   return r;
 }
 

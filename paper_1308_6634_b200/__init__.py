@@ -81,7 +81,7 @@ class _IterRec(C.Structure):
 
 class _Info(C.Structure):
     _fields_ = [("iterations", C.c_int), ("stop_reason", C.c_int), ("n_alphas", C.c_int),
-                ("n_betas", C.c_int), ("breakdown_iteration", C.c_int)]
+                ("n_betas", C.c_int), ("breakdown_iteration", C.c_int), ("n_left_basis", C.c_int)]
 
 
 class _OuterCfg(C.Structure):
@@ -147,7 +147,8 @@ SIGNATURES = {
     "mlsqr_lsqr_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop), C.c_void_p,
                                    C.POINTER(_IterRec), dp, dp, C.POINTER(_Info), C.c_int]),
     "mlsqr_solve_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop), C.c_void_p,
-                                    C.POINTER(_IterRec), dp, dp, C.c_void_p, C.POINTER(_Info), C.c_int]),
+                                    C.POINTER(_IterRec), dp, dp, C.c_void_p, C.c_void_p, C.POINTER(_Info),
+                                    C.c_int]),
     "mlsqr_solve_projected": (C.c_int, [dp, C.c_size_t, dp, C.c_size_t, C.c_double, C.c_double, dp]),
     "mlsqr_reconstruct_from_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, dp, C.c_size_t, C.c_void_p,
                                                C.c_int]),
@@ -592,7 +593,8 @@ class SolveResult:
     trace: list
     alphas: np.ndarray
     betas: np.ndarray
-    basis: object = None  # [n_alphas, n] right basis when store_basis was requested
+    basis: object = None       # [n_alphas, n] right basis when store_basis was requested
+    left_basis: object = None  # [n_left, m] left basis u_1 .. u_{k+1}
 
 
 def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: StoppingConfig,
@@ -620,16 +622,17 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
     sc = stop._c()
     basis = None
     if store_basis:
-        rows = (k + 1) * op.n_cols
+        rows, lrows = (k + 1) * op.n_cols, (k + 1) * op.n_rows
         if kind == DEVICE:
             import torch
             basis = torch.empty(rows, dtype=torch.float64, device=g.device)
-            bptr = C.c_void_p(basis.data_ptr())
+            left = torch.empty(lrows, dtype=torch.float64, device=g.device)
+            bptr, lptr = C.c_void_p(basis.data_ptr()), C.c_void_p(left.data_ptr())
         else:
-            basis = np.zeros(rows)
-            bptr = C.c_void_p(basis.ctypes.data)
+            basis, left = np.zeros(rows), np.zeros(lrows)
+            bptr, lptr = C.c_void_p(basis.ctypes.data), C.c_void_p(left.ctypes.data)
         st = lib().mlsqr_solve_basis(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
-                                     _ptr(al), _ptr(be), bptr, C.byref(info), kind)
+                                     _ptr(al), _ptr(be), bptr, lptr, C.byref(info), kind)
     elif cgn:
         st = lib().mlsqr_cg_normal_solve(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
                                          C.byref(info), kind)
@@ -641,10 +644,12 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
     trace = [IterationRecord(t.iteration, t.res_damped, t.res_data, bool(t.res_data_exact), t.s2_value,
                              t.anorm_est, t.cond_est, t.xnorm_est, t.alpha, t.beta)
              for t in tr[:info.iterations]]
+    left_basis = None
     if basis is not None:
         basis = basis[:info.n_alphas * op.n_cols].reshape(info.n_alphas, op.n_cols)
+        left_basis = left[:info.n_left_basis * op.n_rows].reshape(info.n_left_basis, op.n_rows)
     return SolveResult(f, info.iterations, STOP_NAMES[info.stop_reason], trace,
-                       al[:info.n_alphas].copy(), be[:info.n_betas].copy(), basis)
+                       al[:info.n_alphas].copy(), be[:info.n_betas].copy(), basis, left_basis)
 
 
 def mlsqr(a: LinearOperator, msolver: SpdMap, g, tau: float, stop: StoppingConfig, f_out=None,

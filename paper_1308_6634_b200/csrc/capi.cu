@@ -483,7 +483,7 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
 
 int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
                       double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
-                      mlsqr_solve_info* info, int kind) {
+                      double* left_basis, mlsqr_solve_info* info, int kind) {
   int bd_iter = 0;
   if (info) std::memset(info, 0, sizeof(*info));
   const int st = guard([&] {
@@ -494,15 +494,22 @@ int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, c
     In gin(c, g, o->rows, kind);
     Out fout(c, f, o->cols, kind);
     const size_t nb = ((size_t)stop->max_iters + 1) * o->cols;
-    DevBuf<double> staged;
+    DevBuf<double> staged, staged_l;
     double* bd = basis;
+    double* ld = left_basis;
+    const size_t nl = ((size_t)stop->max_iters + 1) * o->rows;
     if (kind != MLSQR_DEVICE) {
       staged.alloc(nb);
       bd = staged.p;
+      if (left_basis) {
+        staged_l.alloc(nl);
+        ld = staged_l.p;
+      }
     }
     mlsqr_solve_info inf{};
     try {
-      solve_mlsqr(o, pc ? pc->impl : nullptr, gin.d, tau, *stop, fout.d, trace, alphas, betas, &inf, nullptr, true, bd);
+      solve_mlsqr(o, pc ? pc->impl : nullptr, gin.d, tau, *stop, fout.d, trace, alphas, betas, &inf, nullptr, true, bd,
+                  ld);
     } catch (const Error& e) {
       if (e.code == MLSQR_EBREAKDOWN) bd_iter = e.iteration;
       if (info) *info = inf;
@@ -512,6 +519,9 @@ int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, c
     if (kind != MLSQR_DEVICE && inf.n_alphas > 0)
       MLSQR_CUDA(cudaMemcpyAsync(basis, bd, sizeof(double) * (size_t)inf.n_alphas * o->cols, cudaMemcpyDeviceToHost,
                                  c->stream));
+    if (kind != MLSQR_DEVICE && left_basis && inf.n_left_basis > 0)
+      MLSQR_CUDA(cudaMemcpyAsync(left_basis, ld, sizeof(double) * (size_t)inf.n_left_basis * o->rows,
+                                 cudaMemcpyDeviceToHost, c->stream));
     fout.finish();
   });
   if (st == MLSQR_EBREAKDOWN && info) info->breakdown_iteration = bd_iter;

@@ -394,7 +394,7 @@ void workspace_free(Workspace* w);
 int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
                 mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true,
-                double* basis_dev = nullptr);
+                double* basis_dev = nullptr, double* left_dev = nullptr);
 // solve_projected (krylov.cpp:631-678), host arithmetic (projected.cu)
 std::vector<double> solve_projected(const double* alphas, size_t k, const double* betas, size_t nb,
                                     double beta1, double tau);

@@ -37,6 +37,7 @@ struct DevState {
   // flags: 0 active, 1 beta > 0, 2 p != 0 (run M^-1), 3 no breakdown (update w, q)
   int flags[4];
   int iter, iterations, stop_reason, error, error_iter, n_alphas, n_betas, breakdown;
+  int n_left;  // left basis vectors stored (store_basis)
 };
 
 // vector with a zero guard zone on both sides (operator ghost planes when z-sharded)
@@ -243,6 +244,22 @@ __global__ void basis_kernel(const DevState* __restrict__ s, const double* __res
     row[i] = v[i] * sv;
 }
 
+// left basis (krylov.cpp:375-377, 421-425): u_1 once alpha_1 exists, then u_{i+1} whenever
+// beta_{i+1} > 0 -- the scaled u (u * (1/beta), the reference's scal)
+__global__ void left_basis_kernel(DevState* __restrict__ s, const double* __restrict__ u,
+                                  double* __restrict__ basis, size_t m, int in_loop) {
+  if (!s->flags[0] || (in_loop && !s->flags[1])) return;
+  const int row = in_loop ? s->n_left : 0;
+  double* out = basis + (size_t)row * m;
+  const double su = s->su;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = u[i] * su;
+}
+__global__ void left_count_kernel(DevState* s, int in_loop) {
+  if (!s->flags[0] || (in_loop && !s->flags[1])) return;
+  s->n_left = in_loop ? s->n_left + 1 : 1;
+}
+
 // F_a (krylov.cpp:399-431)
 __global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) {
   if (!s->flags[0]) return;
@@ -399,6 +416,15 @@ struct Runner {
   DevState* st;
   Ctx* c;
   double* basis = nullptr;  // [(max_iters + 1) x cols] when the basis is stored
+  double* lbasis = nullptr; // [(max_iters + 1) x rows] left basis
+  void store_left(int in_loop) {
+    if (!lbasis) return;
+    const size_t m = op->rows;
+    const unsigned g = (unsigned)((m + 255) / 256 < 4096 ? (m + 255) / 256 : 4096);
+    left_basis_kernel<<<g, 256, 0, c->stream>>>(st, ws->u.p, lbasis, m, in_loop);
+    left_count_kernel<<<1, 1, 0, c->stream>>>(st, in_loop);
+    c->count(2);
+  }
 
   const int* flag(int k) const { return &st->flags[k]; }
   void store_basis(int in_loop) {
@@ -450,6 +476,7 @@ struct Runner {
     precond(gate_active());
     fin_alpha1_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p);
     store_basis(0);
+    store_left(0);
     dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
     init_wq_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
@@ -473,6 +500,7 @@ struct Runner {
     op->apply(vbuf(), ws->u.p, ea);
     reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true);
     fin_beta_kernel<<<1, 1, 0, c->stream>>>(st);
+    store_left(1);
     // K_B: p_s <- A^T(u_s*su) + (-beta)(p_s*sv)
     Epi eb;
     eb.sx = &st->su;
@@ -517,7 +545,8 @@ struct Runner {
 
 int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
-                mlsqr_solve_info* info, Workspace* ws_in, bool use_graph, double* basis_dev) {
+                mlsqr_solve_info* info, Workspace* ws_in, bool use_graph, double* basis_dev,
+                double* left_dev) {
   Ctx* c = op->ctx;
   validate_stop(stop);
   require(tau >= 0.0, MLSQR_EINVAL, "tau must be nonnegative");
@@ -553,7 +582,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
   ws->f.p = f_dev;
   ws->f.n = op->cols;
 
-  Runner r{op, pc, ws, tau, stop, ws->st.p, c, basis_dev};
+  Runner r{op, pc, ws, tau, stop, ws->st.p, c, basis_dev, left_dev};
   const bool host_cb = pc && pc->host_callback();
   const bool graph = use_graph && !host_cb && !c->timing && (!c->comm || c->comm->capturable());
   r.init(g_dev);
@@ -606,6 +635,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
     info->n_alphas = hs.error ? hs.n_alphas : na;
     info->n_betas = hs.n_betas;
     info->breakdown_iteration = hs.error_iter;
+    info->n_left_basis = left_dev ? hs.n_left : 0;
   }
   if (hs.error) {
     throw Error(MLSQR_EBREAKDOWN,

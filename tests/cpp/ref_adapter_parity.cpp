@@ -104,6 +104,7 @@ int main() {
   const auto r_basis = mlsqr_b200::gpu_mlsqr(gpu_op, vc, bundle.g, 1e-2, stop, so);
   EXPECT(r_basis.solution == r_dev.solution);
   EXPECT(r_basis.bidiag.basis.size() == r_basis.bidiag.alphas.size());
+  EXPECT(r_basis.bidiag.left_basis.size() == r_basis.bidiag.alphas.size() + 1);
   {
     const auto y = mlsqr_b200::gpu_solve_projected(r_basis.bidiag, r_basis.bidiag.betas[0], 1e-2);
     const auto f = mlsqr::reconstruct_from_basis(r_basis.bidiag, y);

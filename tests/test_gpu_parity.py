@@ -549,3 +549,24 @@ def test_mlsqr_basis_orthogonality_and_monotone_residual(ctx, dev):
     assert np.abs(G - np.eye(V.shape[0])).max() <= 1e-4
     res = [t.res_damped for t in r.trace]
     assert all(res[i + 1] <= res[i] * (1 + 1e-12) for i in range(len(res) - 1))
+
+
+def test_bidiagonal_relation_with_stored_bases(ctx):
+    """test_krylov.cpp:277-306: with an exact SPD map, A V = U B_k to 1e-8 ||B||_F, where V and
+    U are the stored right / left bases (u_1 .. u_{k+1}) of the device solve."""
+    rng = np.random.default_rng(12)
+    m, n = 55, 40
+    A = rng.standard_normal((m, n)) / np.sqrt(n)
+    g = rng.standard_normal(m)
+    Q = rng.standard_normal((n, n))
+    M = Q @ Q.T / n + 2.0 * np.eye(n)
+    Minv = np.linalg.inv(M)
+    iters = 20
+    r = mb.mlsqr(mb.DenseOperator(A), mb.CallbackMap(n, lambda p: Minv @ p), g, 0.0,
+                 mb.StoppingConfig.max_iterations(iters), store_basis=True)
+    assert r.iterations == iters and r.left_basis.shape == (iters + 1, m) and r.basis.shape == (iters, n)
+    V, U, al, be = r.basis, r.left_basis, r.alphas, r.betas
+    num2 = sum(np.sum((A @ V[j] - (al[j] * U[j] + be[j + 1] * U[j + 1])) ** 2) for j in range(iters))
+    bnorm2 = sum(al[j] ** 2 + be[j + 1] ** 2 for j in range(iters))
+    assert np.sqrt(num2) <= 1e-8 * np.sqrt(bnorm2)
+    assert np.abs(U @ U.T - np.eye(iters + 1)).max() < 1e-6  # left basis orthonormal
