@@ -206,17 +206,20 @@ __global__ void edge_coeffs_kernel(const double* __restrict__ f, int nx, int ny,
 }
 
 __global__ void max_diag_kernel(Lvl L, unsigned long long* __restrict__ out) {
+  __shared__ double wmax[8];
   const int rows = L.ny * L.nz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int xx = blockIdx.x * 32 + threadIdx.x;
   double d = 0.0;
-  if (row < rows && xx < L.nx) {
-    const size_t i = (size_t)row * L.nx + xx;
-    d = diag_at(L, xx, row % L.ny, row / L.ny, i);
-  }
-  // warp max (exact), then one atomic per warp
+  // grid-stride over rows; the max is exact in any order
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += gridDim.y * blockDim.y)
+    if (xx < L.nx) d = fmax(d, diag_at(L, xx, row % L.ny, row / L.ny, (size_t)row * L.nx + xx));
   for (int off = 16; off >= 1; off >>= 1) d = fmax(d, __shfl_down_sync(kFull, d, off));
-  if ((threadIdx.x & 31) == 0 && d > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(d));
+  if (threadIdx.x == 0) wmax[threadIdx.y] = d;
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    for (int w = 1; w < (int)blockDim.y; ++w) d = fmax(d, wmax[w]);
+    if (d > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(d));  // one atomic per block
+  }
 }
 
 // eps_0 = given (>= 0) or 1e-8 * max diag; eps_l = eps_{l-1} * 2^d (exact)
@@ -342,7 +345,12 @@ class VCycle final : public Pc {
   void build(double eps_cfg) {
     Level& L0 = lv_[0];
     MLSQR_CUDA(cudaMemsetAsync(maxd_.p, 0, sizeof(unsigned long long), ctx->stream));
-    max_diag_kernel<<<row_grid(L0.nx, L0.ny * L0.nz), dim3(32, 8), 0, ctx->stream>>>(view(0), maxd_.p);
+    {
+      dim3 grd = row_grid(L0.nx, L0.ny * L0.nz);
+      const unsigned cap = (unsigned)(ctx->sm_count * 16 / (grd.x ? grd.x : 1) + 1);
+      if (grd.y > cap) grd.y = cap;
+      max_diag_kernel<<<grd, dim3(32, 8), 0, ctx->stream>>>(view(0), maxd_.p);
+    }
     ctx->count();
     if (ctx->sharded()) ctx->comm->allreduce_max_u64(maxd_.p, ctx->stream);  // order-free max
     set_eps_kernel<<<1, 1, 0, ctx->stream>>>(maxd_.p, eps_cfg, mult(), (int)lv_.size(), eps_.p);
