@@ -255,6 +255,7 @@ class Context:
         _check(lib().mlsqr_ctx_set_row_shard(self.h, rows_global, row_offset))
 
     def set_comm_nccl(self, unique_id: bytes, rank: int, size: int) -> None:
+        _nccl_first()
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _check(lib().mlsqr_ctx_set_comm_nccl(self.h, buf, rank, size))
 
@@ -281,8 +282,18 @@ class Context:
             pass
 
 
+def _nccl_first():
+    """Load torch's bundled NCCL before the library dlopens libnccl.so.2: torch binds to the
+    first libnccl.so.2 in the process, so a system NCCL loaded first would break `import torch`."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """An ncclUniqueId (128 bytes) for Context.set_comm_nccl; broadcast it from rank 0."""
+    _nccl_first()
     buf = C.create_string_buffer(128)
     n = C.c_size_t()
     _check(lib().mlsqr_nccl_unique_id(buf, 128, C.byref(n)))

@@ -212,7 +212,7 @@ class BlurOp final : public Op {
  private:
   void run(const double* in, double* out, const Epi& e) {
     TimedRegion tr(ctx, MLSQR_TCLASS_BLUR);
-    if (ctx->sharded()) {
+    if (ctx->sharded() && !(e.in_guarded && e.ghosts_ready)) {
       // fill the ghost planes: in place for guarded solver vectors, else via a staging copy
       const size_t plane = nx_ * ny_, g = (size_t)taps_.R * plane;
       double* src = const_cast<double*>(in);

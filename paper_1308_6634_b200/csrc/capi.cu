@@ -148,6 +148,8 @@ int mlsqr_ctx_destroy(mlsqr_ctx* ctx) {
     cudaSetDevice(ctx->impl.device);
     cudaStreamSynchronize(ctx->impl.stream);
     ctx->impl.release_staging();
+    if (ctx->impl.side) cudaStreamSynchronize(ctx->impl.side);
+    ctx->impl.release_side();
     delete ctx->impl.comm;
     ctx->impl.comm = nullptr;
     if (ctx->impl.own_stream) cudaStreamDestroy(ctx->impl.stream);

@@ -47,10 +47,19 @@ static Api& api() {
   static Api a;
   static std::once_flag once;
   std::call_once(once, [] {
+    // an explicit path wins; else whatever libnccl.so.2 the process already has (torch's
+    // bundled NCCL once torch is imported -- loading a different one first would break torch,
+    // which binds to the first libnccl.so.2 in the process), else the system one
+    const char* env = getenv("MLSQR_NCCL_LIB");
+    if (env && *env) a.h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
-      a.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
       if (a.h) break;
+      a.h = dlopen(n, RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
+    }
+    for (const char* n : names) {
+      if (a.h) break;
+      a.h = dlopen(n, RTLD_NOW | RTLD_LOCAL);
     }
     if (!a.h) return;
     void* h = a.h;  // (never re-enter api() inside call_once: that deadlocks)

@@ -141,6 +141,7 @@ struct Epi {
   double* seg = nullptr;
   const int* gate = nullptr;
   bool in_guarded = false;  // the input carries halo_planes_needed() zero/ghost planes per side
+  bool ghosts_ready = false; // (z-sharded) the caller already filled the input's ghost planes
 };
 
 class Op {
@@ -196,6 +197,25 @@ struct Ctx {
   // [zoff, zoff + nz) of a global grid with nzg planes (nzg == 0: not sharded)
   Comm* comm = nullptr;
   long zoff = 0, nzg = 0;
+  // side stream + fork/join events for exchanges overlapped with main-stream work
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side_stream() {
+    if (!side) {
+      MLSQR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      MLSQR_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      MLSQR_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    return side;
+  }
+  void release_side() {
+    if (side) {
+      cudaStreamDestroy(side);
+      cudaEventDestroy(ev_fork);
+      cudaEventDestroy(ev_join);
+      side = nullptr;
+    }
+  }
   // row-shard decomposition (dense operators): data-space vectors hold the rows
   // [row0, row0 + rows_g / P) of a global data space with rows_g rows; the solution space and any
   // preconditioner are replicated (so sharded() -- the z-slab predicate -- is false)
@@ -339,6 +359,7 @@ void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, 
 void axpby_epi(Ctx* c, const double* x, double* out, RowShape s, const Epi& e);
 // z-slab halo: fill k ghost planes below/above a guarded local vector from the neighbours
 void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k);
+void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k, cudaStream_t s);
 // canonical reduction of this rank's segments of a z-sharded vector: bit-identical to the
 // unsharded reduction (block-aligned tree partials or raw segments are allgathered)
 // dist: the segments are this rank's share of a distributed vector (else: a local / replicated one)

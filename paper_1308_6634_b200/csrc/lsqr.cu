@@ -445,6 +445,23 @@ struct Runner {
 
   double* vbuf() const { return pc ? ws->v.p : ws->p.p; }
 
+  // z slabs, mlsqr mode: K_A's input vtilde is final after the V-cycle, so its R ghost planes
+  // travel on the side stream while fin_alpha, K_U and the w.q reduction run on the main
+  // stream (SURVEY §8e overlap); joined before the iteration ends (graph-capture safe).
+  bool vghost_async() const { return pc && c->sharded() && op->halo_planes_needed() > 0; }
+  void fork_vghost() {
+    if (!vghost_async()) return;
+    cudaStream_t s = c->side_stream();
+    MLSQR_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+    MLSQR_CUDA(cudaStreamWaitEvent(s, c->ev_fork, 0));
+    const size_t plane = op->plane_size();
+    halo_planes(c, ws->v.p, plane, (long)(op->cols / plane), op->halo_planes_needed(), s);
+    MLSQR_CUDA(cudaEventRecord(c->ev_join, s));
+  }
+  void join_vghost() {
+    if (vghost_async()) MLSQR_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  }
+
   void precond(const int* gate) {
     if (pc) {
       pc->solve(ws->p.p, ws->v.p, ws->seg_vp.p, gate, ws->sol);
@@ -474,6 +491,7 @@ struct Runner {
     reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, gate_active(), false);
     fin_p0_kernel<<<1, 1, 0, c->stream>>>(st);
     precond(gate_active());
+    fork_vghost();
     fin_alpha1_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p);
     store_basis(0);
     store_left(0);
@@ -482,6 +500,7 @@ struct Runner {
                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
     reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, gate_active(), false);
     fin_wq0_kernel<<<1, 1, 0, c->stream>>>(st);
+    join_vghost();
     c->count(6);
     c->check_launch();
   }
@@ -497,6 +516,7 @@ struct Runner {
     ea.seg = ws->seg_u.p;
     ea.gate = gate_active();
     ea.in_guarded = true;
+    ea.ghosts_ready = vghost_async();
     op->apply(vbuf(), ws->u.p, ea);
     reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true);
     fin_beta_kernel<<<1, 1, 0, c->stream>>>(st);
@@ -515,6 +535,7 @@ struct Runner {
     fin_p_kernel<<<1, 1, 0, c->stream>>>(st);
     // M^{-1}
     precond(flag(2));
+    fork_vghost();
     fin_alpha_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p, ws->betas.p);
     store_basis(1);
     // K_U
@@ -536,6 +557,7 @@ struct Runner {
       reduce(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active(), true);
     }
     fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
+    join_vghost();
     c->count(5);
     c->check_launch();
   }

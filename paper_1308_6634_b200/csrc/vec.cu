@@ -109,11 +109,13 @@ void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, do
 // ---------------------------------------------------------------------------
 // z-slab decomposition helpers
 // ---------------------------------------------------------------------------
-void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k) {
+void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k) { halo_planes(c, v, plane, nz_loc, k, c->stream); }
+
+void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k, cudaStream_t s) {
   if (!c->sharded() || k <= 0) return;
   require(nz_loc >= k, MLSQR_EDIM, "z slab thinner than the halo it must provide");
   const size_t cnt = plane * (size_t)k;
-  c->comm->halo(v, v + (size_t)(nz_loc - k) * plane, v - cnt, v + (size_t)nz_loc * plane, cnt, c->stream);
+  c->comm->halo(v, v + (size_t)(nz_loc - k) * plane, v - cnt, v + (size_t)nz_loc * plane, cnt, s);
 }
 
 size_t dist_gather_size(Ctx* c, size_t nseg) {
