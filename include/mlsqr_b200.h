@@ -34,6 +34,7 @@ extern "C" {
 #define MLSQR_ECUDA 4       /* CUDA runtime failure / no device              */
 #define MLSQR_ENCCL 5       /* collective failure                            */
 #define MLSQR_ECALLBACK 6   /* a host callback (plugin SpdMap) failed        */
+#define MLSQR_EFACTOR 7     /* FactorizationError(pivot_row) (errors.hpp:14-24) */
 
 #define MLSQR_HOST 0
 #define MLSQR_DEVICE 1
@@ -151,6 +152,16 @@ int mlsqr_vcycle_update(mlsqr_pc* pc, const double* f, int ptr_kind, int pen_kin
 typedef int (*mlsqr_host_map_fn)(void* user, const double* p, double* v);
 int mlsqr_callback_map_create(mlsqr_ctx* ctx, size_t n, mlsqr_host_map_fn fn, void* user,
                               mlsqr_pc** out);
+/* SpdSolver::factorize (spdsolve.hpp:42-70, spdsolve.cpp:22-75) + solve_cholesky (:101-117):
+ * envelope Cholesky of the level-0 M (+ shift) the V-cycle map `m` currently holds (set by
+ * mlsqr_vcycle_set_coefficients / _update; a 1-level V-cycle is a plain holder of M).  Factor
+ * and substitutions run on the device in the reference's operation order (sequential dots,
+ * bit-identical to its scalar backend).  MLSQR_EFACTOR on a nonpositive pivot, its row in
+ * *pivot_row (may be NULL).  For small grids: the envelope holds n * (bandwidth + 1) doubles. */
+int mlsqr_chol_map_create(mlsqr_pc* m, mlsqr_pc** out, long long* pivot_row);
+/* SpdSolver::inner_cg (spdsolve.cpp:77-85, solve_cg :119-137): exactly k_inner CG iterations
+ * from zero on a snapshot of the level-0 M of `m`, canonical device dots, graph-capturable. */
+int mlsqr_inner_cg_map_create(mlsqr_pc* m, int k_inner, mlsqr_pc** out);
 int mlsqr_pc_destroy(mlsqr_pc* pc);
 int mlsqr_pc_dimension(const mlsqr_pc* pc, size_t* n);
 /* SpdMap::solve: v ~= M^{-1} p */

@@ -584,7 +584,7 @@ double orc_penalty_functional(const orc_grid* g, const double* f, int kind, doub
 /* SPD maps                                                                  */
 /* ======================================================================== */
 
-enum { MAP_IDENTITY = 0, MAP_CHOL = 1, MAP_VCYCLE = 2, MAP_CALLBACK = 3 };
+enum { MAP_IDENTITY = 0, MAP_CHOL = 1, MAP_VCYCLE = 2, MAP_CALLBACK = 3, MAP_ENVCHOL = 4, MAP_INNERCG = 5 };
 
 typedef struct {
   size_t nx, ny, nz, n;
@@ -606,6 +606,10 @@ struct orc_map {
   /* callback */
   orc_map_fn fn;
   void* ctx;
+  /* envelope Cholesky / inner CG over a stencil M (grid extents, bandwidth, M snapshot) */
+  size_t gnx, gny, gnz, band;
+  double *mcx, *mcy, *mcz, meps;
+  int k_inner;
 };
 
 orc_map* orc_identity_map_new(size_t n) {
@@ -645,6 +649,97 @@ orc_map* orc_callback_map_new(size_t n, orc_map_fn fn, void* ctx) {
   m->n = n;
   m->fn = fn;
   m->ctx = ctx;
+  return m;
+}
+
+/* SpdSolver::factorize (spdsolve.cpp:22-75): envelope storage, row i = columns
+ * [first_col(i), i], first_col = the smallest column of row i of the assembled M
+ * (sparse.cpp row order: z-, y-, x- neighbour).  E(i, j) lives at l[i*(band+1) + band + j - i]. */
+static size_t env_first(const orc_map* m, size_t i) {
+  const size_t nxy = m->gnx * m->gny;
+  const size_t z = i / nxy, y = (i / m->gnx) % m->gny, x = i % m->gnx;
+  if (z > 0) return i - nxy;
+  if (y > 0) return i - m->gnx;
+  if (x > 0) return i - 1;
+  return i;
+}
+#define ENV(m, i, j) ((m)->l[(i) * ((m)->band + 1) + (m)->band + (j) - (i)])
+
+static orc_map* stencil_map_new(const orc_grid* g, const double* cx, const double* cy,
+                                const double* cz, double eps) {
+  if (grid_ok(g) || !(eps >= 0.0)) return NULL;
+  orc_map* m = (orc_map*)calloc(1, sizeof(orc_map));
+  grid_ext(g, &m->gnx, &m->gny, &m->gnz);
+  m->n = m->gnx * m->gny * m->gnz;
+  m->dims = g->dims;
+  m->band = g->dims >= 3 ? m->gnx * m->gny : g->dims >= 2 ? m->gnx : 1;
+  m->mcx = (double*)malloc(sizeof(double) * m->n);
+  memcpy(m->mcx, cx, sizeof(double) * m->n);
+  if (g->dims >= 2) {
+    m->mcy = (double*)malloc(sizeof(double) * m->n);
+    memcpy(m->mcy, cy, sizeof(double) * m->n);
+  }
+  if (g->dims >= 3) {
+    m->mcz = (double*)malloc(sizeof(double) * m->n);
+    memcpy(m->mcz, cz, sizeof(double) * m->n);
+  }
+  m->meps = eps;
+  return m;
+}
+
+orc_map* orc_env_chol_map_new(const orc_grid* g, const double* cx, const double* cy,
+                              const double* cz, double eps, long long* pivot_row) {
+  if (pivot_row) *pivot_row = -1;
+  orc_map* m = stencil_map_new(g, cx, cy, cz, eps);
+  if (!m) return NULL;
+  m->kind = MAP_ENVCHOL;
+  const size_t n = m->n, W = m->band + 1, nxy = m->gnx * m->gny;
+  m->l = (double*)calloc(n * W, sizeof(double));
+  /* lower triangle of M + eps I (spdsolve.cpp:40-48; values as assemble_m / with_shift) */
+  size_t i = 0;
+  for (size_t z = 0; z < m->gnz; ++z)
+    for (size_t y = 0; y < m->gny; ++y)
+      for (size_t x = 0; x < m->gnx; ++x, ++i) {
+        if (m->mcz && z > 0) ENV(m, i, i - nxy) = -m->mcz[i - nxy];
+        if (m->mcy && y > 0) ENV(m, i, i - m->gnx) = -m->mcy[i - m->gnx];
+        if (x > 0) ENV(m, i, i - 1) = -m->mcx[i - 1];
+        ENV(m, i, i) = diag_at(m->gnx, m->gny, m->gnz, x, y, z, i, m->mcx, m->mcy, m->mcz) + eps;
+      }
+  /* in-place skyline Cholesky (spdsolve.cpp:51-73): sum = E(i,j) - dot(...), sequential dot */
+  for (i = 0; i < n; ++i) {
+    const size_t fi = env_first(m, i);
+    for (size_t j = fi; j <= i; ++j) {
+      const size_t fj = env_first(m, j);
+      const size_t lo = fi > fj ? fi : fj;
+      double sum = ENV(m, i, j);
+      if (j > lo) {
+        double acc = 0.0;
+        for (size_t k = lo; k < j; ++k) acc += ENV(m, i, k) * ENV(m, j, k);
+        sum -= acc;
+      }
+      if (j < i) {
+        ENV(m, i, j) = sum / ENV(m, j, j);
+      } else {
+        if (!(sum > 0.0)) {
+          if (pivot_row) *pivot_row = (long long)i;
+          orc_map_free(m);
+          return NULL;
+        }
+        ENV(m, i, i) = sqrt(sum);
+      }
+    }
+  }
+  return m;
+}
+
+/* SpdSolver::inner_cg (spdsolve.cpp:77-85): the solver keeps its own copy of M */
+orc_map* orc_inner_cg_map_new(const orc_grid* g, const double* cx, const double* cy,
+                              const double* cz, double eps, int k_inner) {
+  if (k_inner < 1) return NULL;
+  orc_map* m = stencil_map_new(g, cx, cy, cz, eps);
+  if (!m) return NULL;
+  m->kind = MAP_INNERCG;
+  m->k_inner = k_inner;
   return m;
 }
 
@@ -797,6 +892,37 @@ int orc_vcycle_level(const orc_map* m, int l, size_t* dims3, double* cx, double*
   return ORC_OK;
 }
 
+/* solve_cg (spdsolve.cpp:119-137): exactly k_inner iterations from v = 0; dots in the
+ * active order (reference: sequential; device: canonical segments over rows of gnx) */
+static double dotL(const double* x, const double* y, size_t n, size_t L);
+static void inner_cg_solve(const orc_map* m, const double* p, double* v) {
+  const size_t n = m->n, L = m->gnx;
+  double* r = (double*)malloc(sizeof(double) * n);
+  double* d = (double*)malloc(sizeof(double) * n);
+  double* q = (double*)malloc(sizeof(double) * n);
+  memset(v, 0, sizeof(double) * n);
+  memcpy(r, p, sizeof(double) * n);
+  memcpy(d, r, sizeof(double) * n);
+  double rho = dotL(r, r, n, L);
+  for (int it = 0; it < m->k_inner; ++it) {
+    if (rho == 0.0) break;
+    m_apply_ext(m->gnx, m->gny, m->gnz, m->mcx, m->mcy, m->mcz, m->meps, d, q);
+    const double curv = dotL(d, q, n, L);
+    if (curv == 0.0) break;
+    const double gamma = rho / curv;
+    for (size_t i = 0; i < n; ++i) v[i] += gamma * d[i];
+    const double ng = -gamma;
+    for (size_t i = 0; i < n; ++i) r[i] += ng * q[i];
+    const double rho_next = dotL(r, r, n, L);
+    const double beta = rho_next / rho;
+    for (size_t i = 0; i < n; ++i) d[i] = r[i] + beta * d[i];
+    rho = rho_next;
+  }
+  free(r);
+  free(d);
+  free(q);
+}
+
 void orc_map_solve(const orc_map* m, const double* p, double* v) {
   switch (m->kind) {
     case MAP_IDENTITY: memcpy(v, p, sizeof(double) * m->n); break;
@@ -815,6 +941,27 @@ void orc_map_solve(const orc_map* m, const double* p, double* v) {
       break;
     }
     case MAP_VCYCLE: vcycle_level(m, 0, p, v); break;
+    case MAP_ENVCHOL: { /* solve_cholesky (spdsolve.cpp:101-117) */
+      const size_t n = m->n;
+      for (size_t i = 0; i < n; ++i) {
+        const size_t fi = env_first(m, i);
+        double sum = p[i];
+        if (i > fi) {
+          double acc = 0.0;
+          for (size_t k = fi; k < i; ++k) acc += ENV(m, i, k) * v[k];
+          sum -= acc;
+        }
+        v[i] = sum / ENV(m, i, i);
+      }
+      for (size_t ii = n; ii-- > 0;) {
+        const size_t fi = env_first(m, ii);
+        v[ii] /= ENV(m, ii, ii);
+        const double a = -v[ii];
+        for (size_t k = fi; k < ii; ++k) v[k] += a * ENV(m, ii, k);
+      }
+      break;
+    }
+    case MAP_INNERCG: inner_cg_solve(m, p, v); break;
     case MAP_CALLBACK: m->fn(m->ctx, p, v); break;
   }
 }
@@ -822,6 +969,9 @@ void orc_map_solve(const orc_map* m, const double* p, double* v) {
 void orc_map_free(orc_map* m) {
   if (!m) return;
   free(m->l);
+  free(m->mcx);
+  free(m->mcy);
+  free(m->mcz);
   if (m->lv) {
     for (int l = 0; l < m->levels; ++l) {
       vc_level* L = &m->lv[l];

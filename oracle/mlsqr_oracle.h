@@ -98,6 +98,14 @@ int orc_vcycle_level(const orc_map* m, int l, size_t* dims3, double* cx, double*
                      double* eps);
 typedef void (*orc_map_fn)(void* ctx, const double* p, double* v);
 orc_map* orc_callback_map_new(size_t n, orc_map_fn fn, void* ctx);
+/* SpdSolver::factorize (spdsolve.cpp:22-75): envelope Cholesky of M + eps I from edge
+ * coefficients, reference operation order in both modes (sequential dots); NULL and
+ * *pivot_row >= 0 on a nonpositive pivot (FactorizationError). */
+orc_map* orc_env_chol_map_new(const orc_grid* g, const double* cx, const double* cy,
+                              const double* cz, double eps, long long* pivot_row);
+/* SpdSolver::inner_cg (spdsolve.cpp:77-85, 119-137): k_inner CG iterations from zero */
+orc_map* orc_inner_cg_map_new(const orc_grid* g, const double* cx, const double* cy,
+                              const double* cz, double eps, int k_inner);
 void orc_map_free(orc_map* m);
 void orc_map_solve(const orc_map* m, const double* p, double* v);
 

@@ -130,6 +130,10 @@ class Oracle:
         L.orc_identity_map_new.argtypes = [C.c_size_t]
         L.orc_dense_chol_map_new.restype = C.c_void_p
         L.orc_dense_chol_map_new.argtypes = [C.c_size_t, dp]
+        L.orc_env_chol_map_new.restype = C.c_void_p
+        L.orc_env_chol_map_new.argtypes = [C.POINTER(Grid), dp, dp, dp, C.c_double, C.POINTER(C.c_longlong)]
+        L.orc_inner_cg_map_new.restype = C.c_void_p
+        L.orc_inner_cg_map_new.argtypes = [C.POINTER(Grid), dp, dp, dp, C.c_double, C.c_int]
         L.orc_vcycle_new.restype = C.c_void_p
         L.orc_vcycle_new.argtypes = [C.POINTER(Grid), C.c_int, C.c_int, C.c_int, C.c_double, C.c_int]
         L.orc_vcycle_set.argtypes = [C.c_void_p, dp, dp, dp, C.c_double]
@@ -283,6 +287,23 @@ class Oracle:
         if not h:
             raise ValueError("matrix not SPD")
         return OrcMap(self, h, m_dense.shape[0])
+
+    def env_chol_map(self, grid, cx, cy, cz, eps):
+        """SpdSolver::factorize over the stencil M (spdsolve.cpp:22-75); ValueError(pivot row)."""
+        row = C.c_longlong(-1)
+        n = grid.nx * grid.ny * grid.nz
+        h = self.lib.orc_env_chol_map_new(C.byref(grid), _ptr(cx), _ptr(cy), _ptr(cz), eps, C.byref(row))
+        if not h:
+            raise ValueError(f"nonpositive pivot at row {row.value}")
+        return OrcMap(self, h, n)
+
+    def inner_cg_map(self, grid, cx, cy, cz, eps, k_inner):
+        """SpdSolver::inner_cg (spdsolve.cpp:77-85, 119-137)."""
+        n = grid.nx * grid.ny * grid.nz
+        h = self.lib.orc_inner_cg_map_new(C.byref(grid), _ptr(cx), _ptr(cy), _ptr(cz), eps, k_inner)
+        if not h:
+            raise ValueError("invalid inner-CG configuration")
+        return OrcMap(self, h, n)
 
     # -- solvers
     def mlsqr(self, op, pc, g, tau, st, snapshots=False, lsqr=False):
@@ -471,6 +492,7 @@ class Reference:
         L.ref_mlsqr_timed.argtypes = [C.POINTER(RefOp), C.POINTER(RefMap), dp, C.c_double,
                                       C.POINTER(Stop), C.c_int, dp, dp, C.POINTER(SolveInfo)]
         L.ref_select_backend.argtypes = [C.c_int]
+        L.ref_map_solve.argtypes = [C.POINTER(RefMap), dp, dp]
         L.ref_kernel_backend.restype = C.c_char_p
         self._keep = []
 
@@ -516,6 +538,13 @@ class Reference:
 
     def map_callback(self, n, fn, ctx):
         return RefMap(kind=4, n=n, solve=fn, ctx=ctx)
+
+    def map_solve(self, md, p):
+        """One SpdMap::solve of a freshly built reference map."""
+        v = np.zeros(md.n)
+        st = self.lib.ref_map_solve(C.byref(md), _ptr(np.ascontiguousarray(p, dtype=np.float64)), _ptr(v))
+        assert st == 0, st
+        return v
 
     def taps(self, n, sigma):
         R = C.c_int()

@@ -305,6 +305,15 @@ int ref_assemble_m_dense(int dims, size_t nx, size_t ny, double h, const double*
   });
 }
 
+// one SpdMap::solve (spdsolve.hpp:15-22) of a freshly built map
+int ref_map_solve(const ref_map_desc* md, const double* p, double* v) {
+  return guarded([&] {
+    MapHolder h = make_map(md);
+    const SpdMap& m = h.get();
+    m.solve(std::span<const double>(p, m.dimension()), std::span<double>(v, m.dimension()));
+  });
+}
+
 int ref_m_multiply(int dims, size_t nx, size_t ny, double h, const double* f, int kind, double T,
                    double eps, const double* x, double* y) {
   return guarded([&] {

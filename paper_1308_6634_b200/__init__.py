@@ -27,7 +27,8 @@ LIB_PATH = os.path.join(HERE, "libmlsqr_b200.so")
 __all__ = [
     "DimensionError", "BreakdownError", "CudaError", "Context", "default_context",
     "LinearOperator", "SeparableGaussianBlur", "DenseOperator", "FdotOperator",
-    "IdentityOperator", "SpdMap", "IdentityMap", "VCycleMap", "CallbackMap",
+    "IdentityOperator", "SpdMap", "IdentityMap", "VCycleMap", "CallbackMap", "CholeskyMap",
+    "InnerCgMap", "FactorizationError",
     "StoppingConfig", "IterationRecord", "SolveResult", "mlsqr", "lsqr", "PenaltySpec",
     "OuterConfig", "OuterStep", "OuterReport", "solve_nonlinear", "penalty_functional",
     "gaussian_taps", "gaussian_noise", "phantom_rects2d", "phantom_shapes2d",
@@ -54,7 +55,15 @@ class CudaError(RuntimeError):
     """CUDA failure or no B200 visible (the product has no CPU fallback)."""
 
 
-OK, EDIM, EINVAL, EBREAKDOWN, ECUDA, ENCCL, ECALLBACK = 0, 1, 2, 3, 4, 5, 6
+class FactorizationError(RuntimeError):
+    """Cholesky hit a nonpositive pivot (errors.hpp:14-24)."""
+
+    def __init__(self, msg: str, pivot_row: int):
+        super().__init__(msg)
+        self.pivot_row = pivot_row
+
+
+OK, EDIM, EINVAL, EBREAKDOWN, ECUDA, ENCCL, ECALLBACK, EFACTOR = 0, 1, 2, 3, 4, 5, 6, 7
 HOST, DEVICE = 0, 1
 STOP_NAMES = ["S1", "S2", "S3", "S4", "max_iters", "breakdown"]
 PEN_KINDS = {"tikhonov": 0, "tv": 1, "tv_smoothed": 1, "pm_log": 2, "perona_malik_log": 2,
@@ -138,6 +147,8 @@ SIGNATURES = {
                                       C.c_double, dp]),
     "mlsqr_callback_map_create": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                             C.POINTER(C.c_void_p)]),
+    "mlsqr_chol_map_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong)]),
+    "mlsqr_inner_cg_map_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "mlsqr_pc_destroy": (C.c_int, [C.c_void_p]),
     "mlsqr_pc_dimension": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
     "mlsqr_pc_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]),
@@ -203,6 +214,8 @@ def _check(status: int, info: Optional[_Info] = None) -> None:
         raise ValueError(msg)
     if status == EBREAKDOWN:
         raise BreakdownError(msg, info.breakdown_iteration if info is not None else -1)
+    if status == EFACTOR:
+        raise FactorizationError(msg, int(msg.rsplit(" ", 1)[-1]) if msg[-1:].isdigit() else -1)
     raise CudaError(f"[status {status}] {msg}")
 
 
@@ -508,6 +521,30 @@ class VCycleMap(SpdMap):
         out = np.zeros(self.n)
         _check(lib().mlsqr_vcycle_m_apply(self.h, xp, C.c_void_p(out.ctypes.data), xn, HOST))
         return out
+
+
+class CholeskyMap(SpdMap):
+    """SpdSolver::factorize (spdsolve.cpp:22-75): envelope Cholesky of the M (+ shift) a
+    V-cycle map holds (VCycleMap(levels=1) is a plain holder of M), factorized and applied on
+    the device in the reference's operation order.  FactorizationError on a nonpositive pivot."""
+
+    def __init__(self, m: "VCycleMap"):
+        h = C.c_void_p()
+        row = C.c_longlong(-1)
+        _check(lib().mlsqr_chol_map_create(m.h, C.byref(h), C.byref(row)))
+        self.grid_shape = m.grid_shape
+        super().__init__(h, m.ctx)
+
+
+class InnerCgMap(SpdMap):
+    """SpdSolver::inner_cg (spdsolve.cpp:77-85, 119-137): k_inner CG iterations from zero on a
+    snapshot of the M a V-cycle map holds; device-resident (graph-capturable)."""
+
+    def __init__(self, m: "VCycleMap", k_inner: int):
+        h = C.c_void_p()
+        _check(lib().mlsqr_inner_cg_map_create(m.h, int(k_inner), C.byref(h)))
+        self.grid_shape = m.grid_shape
+        super().__init__(h, m.ctx)
 
 
 class CallbackMap(SpdMap):

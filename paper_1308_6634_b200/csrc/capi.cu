@@ -367,6 +367,23 @@ int mlsqr_vcycle_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t n
   });
 }
 
+int mlsqr_chol_map_create(mlsqr_pc* m, mlsqr_pc** out, long long* pivot_row) {
+  if (pivot_row) *pivot_row = -1;
+  return guard([&] {
+    require(m && m->vc && out, MLSQR_EINVAL, "the Cholesky map is built from the M of a V-cycle map");
+    set_device(m->impl->ctx);
+    *out = new mlsqr_pc{make_chol_map(m->vc, pivot_row), nullptr};
+  });
+}
+
+int mlsqr_inner_cg_map_create(mlsqr_pc* m, int k_inner, mlsqr_pc** out) {
+  return guard([&] {
+    require(m && m->vc && out, MLSQR_EINVAL, "the inner-CG map is built from the M of a V-cycle map");
+    set_device(m->impl->ctx);
+    *out = new mlsqr_pc{make_inner_cg_map(m->vc, k_inner), nullptr};
+  });
+}
+
 int mlsqr_vcycle_set_coefficients(mlsqr_pc* pc, const double* cx, const double* cy,
                                   const double* cz, double eps, int kind) {
   return guard([&] {

@@ -396,6 +396,9 @@ void penalty_functional_async(Ctx* c, int dims, size_t nx, size_t ny, size_t nz,
                               const double* f, int kind, double T, double* seg, double* scratch,
                               double* gathered, double* fguard, double* out);
 Pc* make_callback_map(Ctx* c, size_t n, mlsqr_host_map_fn fn, void* user);
+// SpdSolver::factorize / inner_cg over the level-0 M (+ shift) of a V-cycle map (spdmaps.cu)
+Pc* make_chol_map(VCycle* src, long long* pivot_row);
+Pc* make_inner_cg_map(VCycle* src, int k_inner);
 double penalty_functional_dev(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h,
                               const double* f, int pen_kind, double T);
 

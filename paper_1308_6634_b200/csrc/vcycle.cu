@@ -414,6 +414,19 @@ class VCycle final : public Pc {
     build(eps_cfg);
   }
   const double* eps_dev() const { return eps_.p; }
+  void level0(int* dims, int* nx, int* ny, int* nz, double* h, const double** cx, const double** cy,
+              const double** cz, const double** eps) const {
+    const Level& L = lv_[0];
+    *dims = dims_;
+    *nx = L.nx;
+    *ny = L.ny;
+    *nz = L.nz;
+    *h = h_;
+    *cx = L.cx.p;
+    *cy = dims_ >= 2 ? L.cy.p : nullptr;
+    *cz = dims_ >= 3 ? L.cz.p : nullptr;
+    *eps = eps_.p;
+  }
 
   void m_apply(const double* x, double* y) {
     const Level& L0 = lv_[0];
@@ -577,6 +590,10 @@ void vcycle_update_async(VCycle* v, const double* f, int kind, double T, double 
   v->update_async(f, kind, T, eps);
 }
 const double* vcycle_eps_dev(VCycle* v) { return v->eps_dev(); }
+void vcycle_level0(VCycle* v, int* dims, int* nx, int* ny, int* nz, double* h, const double** cx,
+                   const double** cy, const double** cz, const double** eps) {
+  v->level0(dims, nx, ny, nz, h, cx, cy, cz, eps);
+}
 Pc* vcycle_as_pc(VCycle* v) { return v; }
 void vcycle_m_apply(VCycle* v, const double* x, double* y) { v->m_apply(x, y); }
 

@@ -182,6 +182,22 @@ def main():
             out[pre + "_inner"] = np.array([s_["inner_iterations"] for s_ in rep["steps"]])
             out[pre + "_trigger"] = np.array(rep["triggered_at"])
 
+    # --- SpdSolver maps over the assembled M (spdsolve.cpp:22-137): envelope Cholesky and
+    #     inner CG, one solve each; own generator so the arrays above keep their inputs
+    rng2 = np.random.default_rng(22137)
+    for dims, shape, h in [(1, (33,), 1 / 33), (2, (9, 7), 0.1), (2, (24, 24), 1 / 24)]:
+        nn = int(np.prod(shape))
+        tag = "x".join(map(str, shape))
+        f, p = rng2.standard_normal(nn), rng2.standard_normal(nn)
+        out[f"maps_{tag}_f"], out[f"maps_{tag}_p"] = f, p
+        for backend in ("scalar", "avx2"):
+            assert r.select_backend(backend == "scalar"), backend
+            for kind, T in KINDS[:3]:
+                out[f"{backend}_maps_{tag}_{kind}_chol"] = r.map_solve(
+                    r.map_assembled(dims, shape, h, f, kind, T), p)
+                out[f"{backend}_maps_{tag}_{kind}_cg7"] = r.map_solve(
+                    r.map_assembled(dims, shape, h, f, kind, T, inner_cg=7), p)
+
     # --- SignFlipMap breakdown (test_krylov.cpp:131-145)
     @VEC_FN
     def flip(ctx, p, v):

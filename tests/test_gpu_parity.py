@@ -570,3 +570,76 @@ def test_bidiagonal_relation_with_stored_bases(ctx):
     bnorm2 = sum(al[j] ** 2 + be[j + 1] ** 2 for j in range(iters))
     assert np.sqrt(num2) <= 1e-8 * np.sqrt(bnorm2)
     assert np.abs(U @ U.T - np.eye(iters + 1)).max() < 1e-6  # left basis orthonormal
+
+
+# ---------------------------------------------------------------------------
+# the reference's SpdSolver modes on the device (spdsolve.cpp:22-137)
+# ---------------------------------------------------------------------------
+MAP_GRIDS = [(1, (33,), 1 / 33), (2, (9, 7), 0.1), (2, (24, 24), 1 / 24)]
+
+
+@pytest.mark.parametrize("dims,shape,h", MAP_GRIDS)
+@pytest.mark.parametrize("pen,T", [("tikhonov", 1.0), ("tv", 0.5), ("pm_log", 0.25)])
+def test_cholesky_and_inner_cg_maps(ctx, dev, golden, dims, shape, h, pen, T):
+    """CholeskyMap is bit-identical to the REFERENCE's own SpdSolver::factorize + solve
+    (scalar backend golden); InnerCgMap to the oracle's device-order restatement of solve_cg."""
+    tag = "x".join(map(str, shape))
+    f, p = golden[f"maps_{tag}_f"], golden[f"maps_{tag}_p"]
+    m = mb.VCycleMap(shape, h, 1)
+    eps = m.update(f, mb.PenaltySpec(pen, T))
+    chol = mb.CholeskyMap(m)
+    grid = dev.grid(dims, shape, h)
+    cx, cy, cz = dev.edge_coeffs(grid, f, pen, T)
+    assert eps == 1e-8 * dev.max_diag(grid, cx, cy, cz)
+    vc = chol.solve(p)
+    assert np.array_equal(vc, dev.env_chol_map(grid, cx, cy, cz, eps).solve(p))
+    ref = golden[f"scalar_maps_{tag}_{pen}_chol"]
+    if pen != "tv":
+        assert np.array_equal(vc, ref)  # the reference itself, bit for bit
+    else:
+        # TV's c(t) = 1/hypot(T, t): the device hypot (IEEE basic ops) and glibc's differ by
+        # an ulp in some edge coefficients, which the exact inverse's eps-mode amplifies
+        assert rel(vc, ref) <= max(1e-7, 10 * rel(golden[f"avx2_maps_{tag}_{pen}_chol"], ref))
+    cg = mb.InnerCgMap(m, 7)
+    assert np.array_equal(cg.solve(p), dev.inner_cg_map(grid, cx, cy, cz, eps, 7).solve(p))
+    # snapshot semantics: re-assembling the source M does not change either map
+    m.update(np.zeros_like(f), mb.PenaltySpec(pen, T))
+    assert np.array_equal(chol.solve(p), vc)
+    assert np.array_equal(cg.solve(p), dev.inner_cg_map(grid, cx, cy, cz, eps, 7).solve(p))
+
+
+def test_cholesky_map_factorization_error(ctx):
+    m = mb.VCycleMap((8,), 1 / 8, 1)
+    cx = np.full(8, -1.0)
+    m.set_coefficients(cx, eps=0.0)
+    with pytest.raises(mb.FactorizationError) as ei:
+        mb.CholeskyMap(m)
+    assert ei.value.pivot_row == 0
+    with pytest.raises(ValueError):
+        mb.InnerCgMap(m, 0)
+
+
+@pytest.mark.parametrize("mode", ["chol", "cg"])
+@pytest.mark.parametrize("tau", [0.0, 0.1])
+def test_mlsqr_with_reference_spd_solvers(ctx, dev, golden, mode, tau):
+    """The reference's own deconvolution test setup (test_krylov.cpp:350-360): 1D n=128,
+    ideal PM-log M, S4 stop.  Bit-exact vs the oracle's device order; against the reference
+    (sequential dots) within the scalar-vs-AVX2 spread of the reference itself."""
+    n = 128
+    ft, g = golden["scalar_deconv_ftrue"], golden["scalar_deconv_g"]
+    a = mb.SeparableGaussianBlur((n,), sigma_f=0.03)
+    m = mb.VCycleMap((n,), 1 / n, 1)
+    eps = m.update(ft, mb.PenaltySpec("pm_log", 0.005))
+    pc = mb.CholeskyMap(m) if mode == "chol" else mb.InnerCgMap(m, 8)
+    delta = 0.01 / np.sqrt(1.0 / n)
+    st = mb.StoppingConfig.discrepancy(delta, 1.1, 20)
+    gres = mb.mlsqr(a, pc, g, tau, st)
+    grid = dev.grid(1, (n,), 1 / n)
+    cx, cy, cz = dev.edge_coeffs(grid, ft, "pm_log", 0.005)
+    om = dev.env_chol_map(grid, cx, cy, cz, eps) if mode == "chol" else dev.inner_cg_map(grid, cx, cy, cz, eps, 8)
+    ores = dev.mlsqr(dev.blur(1, (n,), dev.taps(n, 0.03)), om, g, tau, ostop_from(st))
+    compare_solves(gres, ores)
+    if mode == "chol":
+        ref = golden[f"scalar_deconv_tau{tau}_f"]
+        assert gres.iterations == int(golden[f"scalar_deconv_tau{tau}_iters"])
+        assert rel(gres.solution, ref) <= max(1e-6, 10 * rel(golden[f"avx2_deconv_tau{tau}_f"], ref))

@@ -262,3 +262,53 @@ def test_solve_projected_validation():
         mb.solve_projected([1.0, 2.0], [1.0, 0.5], 1.0, 0.0)  # needs k+1 betas
     with pytest.raises(ValueError):
         mb.solve_projected([1.0], [1.0, 0.5], 1.0, -1.0)
+
+
+MAP_GRIDS = [(1, (33,), 1 / 33), (2, (9, 7), 0.1), (2, (24, 24), 1 / 24)]
+
+
+@pytest.mark.parametrize("dims,shape,h", MAP_GRIDS)
+@pytest.mark.parametrize("kind,T", KINDS[:3])
+def test_spd_solver_maps_bit_exact(orc, golden, dims, shape, h, kind, T):
+    """SpdSolver::factorize + solve_cholesky and SpdSolver::inner_cg (spdsolve.cpp:22-137)
+    restated over the stencil M: bit-exact with the reference's scalar backend; the AVX2
+    backend (reassociated dots) agrees to its own rounding spread."""
+    tag = "x".join(map(str, shape))
+    f, p = golden[f"maps_{tag}_f"], golden[f"maps_{tag}_p"]
+    g = orc.grid(dims, shape, h)
+    cx, cy, cz = orc.edge_coeffs(g, f, kind, T)
+    eps = 1e-8 * orc.max_diag(g, cx, cy, cz)  # auto_shift (diffusion.cpp:81)
+    chol = orc.env_chol_map(g, cx, cy, cz, eps).solve(p)
+    cg = orc.inner_cg_map(g, cx, cy, cz, eps, 7).solve(p)
+    assert np.array_equal(chol, golden[f"scalar_maps_{tag}_{kind}_chol"])
+    assert np.array_equal(cg, golden[f"scalar_maps_{tag}_{kind}_cg7"])
+    # the exact inverse amplifies the eps-mode: compare relative to the solution scale
+    assert rel(chol, golden[f"avx2_maps_{tag}_{kind}_chol"]) < 1e-8
+    assert rel(cg, golden[f"avx2_maps_{tag}_{kind}_cg7"]) < 1e-2
+
+
+def test_env_chol_map_rejects_non_spd(orc):
+    # FactorizationError on a nonpositive pivot (spdsolve.cpp:66-70): negative coefficients
+    g = orc.grid(1, (8,), 1 / 8)
+    cx = np.full(8, -1.0)
+    cx[-1] = 0.0
+    with pytest.raises(ValueError, match="row 0"):
+        orc.env_chol_map(g, cx, np.zeros(8), np.zeros(8), 0.0)
+
+
+def test_inner_cg_device_order_agrees_to_rounding(orc, golden):
+    tag = "24x24"
+    f, p = golden[f"maps_{tag}_f"], golden[f"maps_{tag}_p"]
+    g = orc.grid(2, (24, 24), 1 / 24)
+    cx, cy, cz = orc.edge_coeffs(g, f, "tv", 0.5)
+    eps = 1e-8 * orc.max_diag(g, cx, cy, cz)
+    ref = orc.inner_cg_map(g, cx, cy, cz, eps, 7).solve(p)
+    orc.set_device_order(True)
+    try:
+        dev = orc.inner_cg_map(g, cx, cy, cz, eps, 7).solve(p)
+        # the Cholesky map has one (sequential) order in both modes
+        c1 = orc.env_chol_map(g, cx, cy, cz, eps).solve(p)
+    finally:
+        orc.set_device_order(False)
+    assert rel(dev, ref) < 1e-12
+    assert np.array_equal(c1, golden[f"scalar_maps_{tag}_tv_chol"])
