@@ -209,6 +209,26 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
 int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
                       double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
                       double* left_basis, mlsqr_solve_info* info, int ptr_kind);
+/* SolveOptions (krylov.hpp:77-80) and where their outputs go (ptr_kind memory of the call):
+ *   record_snapshots -> snapshots[max_iters x n_cols]: f after each recorded iteration
+ *                       (SolveTrace::snapshots, krylov.cpp:159-161); info->iterations rows valid
+ *   store_basis      -> basis / left_basis as in mlsqr_solve_basis (left_basis may be NULL) */
+typedef struct {
+  int record_snapshots;
+  int store_basis;
+  double* snapshots;
+  double* basis;
+  double* left_basis;
+} mlsqr_solve_opts;
+/* mlsqr / lsqr (pc == NULL) with SolveOptions */
+int mlsqr_solve_with(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                     const mlsqr_solve_opts* opts, double* f, mlsqr_iter_rec* trace, double* alphas,
+                     double* betas, mlsqr_solve_info* info, int ptr_kind);
+/* cg_normal with SolveOptions::record_snapshots (krylov.cpp:608); store_basis is ignored like
+ * the reference (cg_normal has no bidiagonalization) */
+int mlsqr_cg_normal_solve_with(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau,
+                               const mlsqr_stop* stop, const mlsqr_solve_opts* opts, double* f,
+                               mlsqr_iter_rec* trace, mlsqr_solve_info* info, int ptr_kind);
 /* solve_projected (krylov.hpp:124-127, krylov.cpp:631-678): y[k] minimising
  * |[B_k; sqrt(tau) I] y - beta1 e1| from k alphas and k+1 betas (host arithmetic; one
  * bidiagonalization serves every tau).  No device needed. */
@@ -227,6 +247,13 @@ int mlsqr_reconstruct_from_basis(mlsqr_ctx* ctx, const double* basis, size_t n, 
 int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau,
                           const mlsqr_stop* stop, double* f, mlsqr_iter_rec* trace,
                           mlsqr_solve_info* info, int ptr_kind);
+
+/* krylov_basis (krylov.hpp:133-145, krylov.cpp:700-754): the first k orthonormalized vectors of
+ * K^{A^T A} (msolver = m = NULL), K^{A^T A + tau M} (m: a V-cycle map holding M) or
+ * K^{M^-1 A^T A} (msolver: any SpdMap), Gram-Schmidt with one reorthogonalization pass.
+ * vectors: k x n_cols (ptr_kind memory); *count rows are valid; *rank_exhausted as KrylovBasis. */
+int mlsqr_krylov_basis(mlsqr_op* op, mlsqr_pc* msolver, mlsqr_pc* m, double tau, const double* g,
+                       int k, double* vectors, int* count, int* rank_exhausted, int ptr_kind);
 
 /* ---- lagged-diffusivity outer loop (outer.hpp:13-62) --------------------- */
 typedef struct {            /* OuterConfig (outer.hpp:13-28) with a V-cycle M^{-1} */

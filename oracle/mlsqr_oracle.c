@@ -1688,3 +1688,69 @@ done:
   free(x); free(b); free(r); free(d); free(q); free(mx); free(tr);
   return status;
 }
+
+/* ======================================================================== */
+/* krylov_basis (krylov.cpp:700-754): Gram-Schmidt with one reorthogonalization */
+/* ======================================================================== */
+int orc_krylov_basis(const orc_linop* a, const orc_map* msolver, const orc_grid* mg,
+                     const double* cx, const double* cy, const double* cz, double eps, double tau,
+                     const double* g, int k, double* out, int* count, int* rank_exhausted) {
+  *count = 0;
+  *rank_exhausted = 0;
+  if (msolver && mg) return ORC_EINVAL;
+  if (k < 1) return ORC_EINVAL;
+  const size_t n = a->cols, L = a->sol_len;
+  size_t mnx = 0, mny = 0, mnz = 0;
+  if (mg) {
+    grid_ext(mg, &mnx, &mny, &mnz);
+    if (mnx * mny * mnz != n) return ORC_EDIM;
+    if (mg->dims < 2) cy = NULL;
+    if (mg->dims < 3) cz = NULL;
+  }
+  double* t = (double*)malloc(sizeof(double) * n);
+  double* scratch = (double*)malloc(sizeof(double) * n);
+  double* rows = (double*)malloc(sizeof(double) * a->rows);
+  orc_linop_adjoint(a, g, t);
+  if (msolver) {
+    orc_map_solve(msolver, t, scratch);
+    memcpy(t, scratch, sizeof(double) * n);
+  }
+  const double seed_norm = nrm2L(t, n, L);
+  if (seed_norm == 0.0) {
+    *rank_exhausted = 1;
+  } else {
+    for (int j = 0; j < k; ++j) {
+      if (j > 0) {
+        const double* prev = out + (size_t)(*count - 1) * n;
+        orc_linop_apply(a, prev, rows);
+        orc_linop_adjoint(a, rows, t);
+        if (mg && tau > 0.0) {
+          m_apply_ext(mnx, mny, mnz, cx, cy, cz, eps, prev, scratch);
+          axpy(tau, scratch, t, n);
+        }
+        if (msolver) {
+          orc_map_solve(msolver, t, scratch);
+          memcpy(t, scratch, sizeof(double) * n);
+        }
+      }
+      const double before = nrm2L(t, n, L);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int q = 0; q < *count; ++q) {
+          const double* qv = out + (size_t)q * n;
+          axpy(-dotL(qv, t, n, L), qv, t, n);
+        }
+      const double after = nrm2L(t, n, L);
+      if (after <= 1e-12 * (before > seed_norm ? before : seed_norm)) {
+        *rank_exhausted = 1;
+        break;
+      }
+      scal(1.0 / after, t, n);
+      memcpy(out + (size_t)*count * n, t, sizeof(double) * n);
+      ++*count;
+    }
+  }
+  free(t);
+  free(scratch);
+  free(rows);
+  return ORC_OK;
+}

@@ -200,6 +200,11 @@ void orc_fdot_matrix(size_t N, int n_src, int n_det, const double* gs, const dou
                      double* a);
 
 /* DEVICE arithmetic order switch (see mlsqr_oracle.c "arithmetic order") */
+/* krylov_basis (krylov.cpp:700-754): msolver XOR the stencil M (mg, cx, cy, cz, eps) or neither;
+ * out: k x cols; *count vectors written */
+int orc_krylov_basis(const orc_linop* a, const orc_map* msolver, const orc_grid* mg,
+                     const double* cx, const double* cy, const double* cz, double eps, double tau,
+                     const double* g, int k, double* out, int* count, int* rank_exhausted);
 void orc_set_device_order(int on);
 int orc_get_device_order(void);
 double orc_canon_dot(const double* x, const double* y, size_t n, size_t row_len);

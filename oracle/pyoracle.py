@@ -134,6 +134,8 @@ class Oracle:
         L.orc_env_chol_map_new.argtypes = [C.POINTER(Grid), dp, dp, dp, C.c_double, C.POINTER(C.c_longlong)]
         L.orc_inner_cg_map_new.restype = C.c_void_p
         L.orc_inner_cg_map_new.argtypes = [C.POINTER(Grid), dp, dp, dp, C.c_double, C.c_int]
+        L.orc_krylov_basis.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Grid), dp, dp, dp, C.c_double,
+                                        C.c_double, dp, C.c_int, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.orc_vcycle_new.restype = C.c_void_p
         L.orc_vcycle_new.argtypes = [C.POINTER(Grid), C.c_int, C.c_int, C.c_int, C.c_double, C.c_int]
         L.orc_vcycle_set.argtypes = [C.c_void_p, dp, dp, dp, C.c_double]
@@ -304,6 +306,21 @@ class Oracle:
         if not h:
             raise ValueError("invalid inner-CG configuration")
         return OrcMap(self, h, n)
+
+    def krylov_basis(self, op, msolver, k, g, tau=0.0, m=None):
+        """krylov_basis (krylov.cpp:700-754); m = (grid, cx, cy, cz, eps) for K^{A^T A + tau M}."""
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        out = np.zeros(k * op.cols)
+        cnt, ex = C.c_int(), C.c_int()
+        if m is not None:
+            grid, cx, cy, cz, eps = m
+            st = self.lib.orc_krylov_basis(op.h, None, C.byref(grid), _ptr(cx), _ptr(cy), _ptr(cz), eps, tau,
+                                           _ptr(g), k, _ptr(out), C.byref(cnt), C.byref(ex))
+        else:
+            st = self.lib.orc_krylov_basis(op.h, msolver.h if msolver is not None else None, None, None, None,
+                                           None, 0.0, tau, _ptr(g), k, _ptr(out), C.byref(cnt), C.byref(ex))
+        assert st == 0, st
+        return out[:cnt.value * op.cols].reshape(cnt.value, op.cols), bool(ex.value)
 
     # -- solvers
     def mlsqr(self, op, pc, g, tau, st, snapshots=False, lsqr=False):
@@ -492,6 +509,9 @@ class Reference:
         L.ref_mlsqr_timed.argtypes = [C.POINTER(RefOp), C.POINTER(RefMap), dp, C.c_double,
                                       C.POINTER(Stop), C.c_int, dp, dp, C.POINTER(SolveInfo)]
         L.ref_select_backend.argtypes = [C.c_int]
+        L.ref_krylov_basis.argtypes = [C.POINTER(RefOp), C.POINTER(RefMap), C.c_int, C.c_int, C.c_size_t,
+                                       C.c_size_t, C.c_double, dp, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       dp, C.c_int, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_map_solve.argtypes = [C.POINTER(RefMap), dp, dp]
         L.ref_kernel_backend.restype = C.c_char_p
         self._keep = []
@@ -538,6 +558,23 @@ class Reference:
 
     def map_callback(self, n, fn, ctx):
         return RefMap(kind=4, n=n, solve=fn, ctx=ctx)
+
+    def krylov_basis(self, od, cols, k, g, tau=0.0, md=None, m=None):
+        """krylov_basis; md: a map descriptor (priorconditioned space); m = (dims, shape, h, f, pen,
+        T, eps) for K^{A^T A + tau M}."""
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        out = np.zeros(k * cols)
+        cnt, ex = C.c_int(), C.c_int()
+        if m is not None:
+            dims, shape, h, f, pen, T, eps = m
+            nx, ny = (list(shape) + [1])[:2]
+            f = np.ascontiguousarray(f, dtype=np.float64)
+            args = (None, 1, dims, nx, ny, h, _ptr(f), PEN.get(pen, pen), T, eps)
+        else:
+            args = (C.byref(md) if md is not None else None, 0, 1, 0, 0, 0.0, None, 0, 0.0, -1.0)
+        st = self.lib.ref_krylov_basis(C.byref(od), *args, tau, _ptr(g), k, _ptr(out), C.byref(cnt), C.byref(ex))
+        assert st == 0, st
+        return out[:cnt.value * cols].reshape(cnt.value, cols), bool(ex.value)
 
     def map_solve(self, md, p):
         """One SpdMap::solve of a freshly built reference map."""

@@ -305,6 +305,32 @@ int ref_assemble_m_dense(int dims, size_t nx, size_t ny, double h, const double*
   });
 }
 
+// krylov_basis (krylov.cpp:700-754): md != null -> priorconditioned space; else with_m ->
+// K^{A^T A + tau M} with M assembled at f (shift eps < 0: auto); else K^{A^T A}
+int ref_krylov_basis(const ref_op_desc* od, const ref_map_desc* md, int with_m, int dims, size_t nx,
+                     size_t ny, double h, const double* f, int kind, double T, double eps, double tau,
+                     const double* g, int k, double* out, int* count, int* rank_exhausted) {
+  return guarded([&] {
+    auto a = make_op(od);
+    KrylovBasis b;
+    if (md) {
+      MapHolder mh = make_map(md);
+      b = krylov_basis(*a, &mh.get(), nullptr, tau, std::span<const double>(g, a->n_rows()), k);
+    } else if (with_m) {
+      const Grid grid = make_grid(dims, nx, ny, h);
+      SparseSpd m = assemble_m(grid, std::span<const double>(f, grid.num_nodes()), make_spec(kind, T), 0.0);
+      m = m.with_shift(eps >= 0.0 ? eps : auto_shift(m));
+      b = krylov_basis(*a, nullptr, &m, tau, std::span<const double>(g, a->n_rows()), k);
+    } else {
+      b = krylov_basis(*a, nullptr, nullptr, tau, std::span<const double>(g, a->n_rows()), k);
+    }
+    *count = (int)b.vectors.size();
+    *rank_exhausted = b.rank_exhausted ? 1 : 0;
+    for (size_t j = 0; j < b.vectors.size(); ++j)
+      std::copy(b.vectors[j].begin(), b.vectors[j].end(), out + j * a->n_cols());
+  });
+}
+
 // one SpdMap::solve (spdsolve.hpp:15-22) of a freshly built map
 int ref_map_solve(const ref_map_desc* md, const double* p, double* v) {
   return guarded([&] {

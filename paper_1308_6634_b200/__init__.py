@@ -28,7 +28,7 @@ __all__ = [
     "DimensionError", "BreakdownError", "CudaError", "Context", "default_context",
     "LinearOperator", "SeparableGaussianBlur", "DenseOperator", "FdotOperator",
     "IdentityOperator", "SpdMap", "IdentityMap", "VCycleMap", "CallbackMap", "CholeskyMap",
-    "InnerCgMap", "FactorizationError",
+    "InnerCgMap", "FactorizationError", "krylov_basis", "cg_normal",
     "StoppingConfig", "IterationRecord", "SolveResult", "mlsqr", "lsqr", "PenaltySpec",
     "OuterConfig", "OuterStep", "OuterReport", "solve_nonlinear", "penalty_functional",
     "gaussian_taps", "gaussian_noise", "phantom_rects2d", "phantom_shapes2d",
@@ -160,6 +160,14 @@ SIGNATURES = {
     "mlsqr_solve_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop), C.c_void_p,
                                     C.POINTER(_IterRec), dp, dp, C.c_void_p, C.c_void_p, C.POINTER(_Info),
                                     C.c_int]),
+    "mlsqr_solve_with": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop),
+                                   C.c_void_p, C.c_void_p, C.POINTER(_IterRec), dp, dp, C.POINTER(_Info),
+                                   C.c_int]),
+    "mlsqr_cg_normal_solve_with": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(_Stop),
+                                             C.c_void_p, C.c_void_p, C.POINTER(_IterRec), C.POINTER(_Info),
+                                             C.c_int]),
+    "mlsqr_krylov_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_int,
+                                     C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]),
     "mlsqr_solve_projected": (C.c_int, [dp, C.c_size_t, dp, C.c_size_t, C.c_double, C.c_double, dp]),
     "mlsqr_reconstruct_from_basis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, dp, C.c_size_t, C.c_void_p,
                                                C.c_int]),
@@ -643,10 +651,17 @@ class SolveResult:
     betas: np.ndarray
     basis: object = None       # [n_alphas, n] right basis when store_basis was requested
     left_basis: object = None  # [n_left, m] left basis u_1 .. u_{k+1}
+    snapshots: object = None   # [iterations, n] f after each iteration (record_snapshots)
+
+
+class _SolveOpts(C.Structure):  # mlsqr_solve_opts (SolveOptions, krylov.hpp:77-80)
+    _fields_ = [("record_snapshots", C.c_int), ("store_basis", C.c_int), ("snapshots", C.c_void_p),
+                ("basis", C.c_void_p), ("left_basis", C.c_void_p)]
 
 
 def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: StoppingConfig,
-         f_out=None, cgn: bool = False, store_basis: bool = False) -> SolveResult:
+         f_out=None, cgn: bool = False, store_basis: bool = False,
+         record_snapshots: bool = False) -> SolveResult:
     stop.validate()
     if not tau >= 0.0:
         raise ValueError("tau must be nonnegative")
@@ -660,30 +675,37 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
     al = np.zeros(k + 1)
     be = np.zeros(k + 2)
     info = _Info()
-    if kind == DEVICE:
-        import torch
-        f = torch.empty(op.n_cols, dtype=torch.float64, device=g.device) if f_out is None else f_out
-        fptr = C.c_void_p(f.data_ptr())
-    else:
-        f = np.zeros(op.n_cols) if f_out is None else f_out
-        fptr = C.c_void_p(f.ctypes.data)
-    sc = stop._c()
-    basis = None
-    if store_basis:
-        rows, lrows = (k + 1) * op.n_cols, (k + 1) * op.n_rows
+
+    def buf(count):
         if kind == DEVICE:
             import torch
-            basis = torch.empty(rows, dtype=torch.float64, device=g.device)
-            left = torch.empty(lrows, dtype=torch.float64, device=g.device)
-            bptr, lptr = C.c_void_p(basis.data_ptr()), C.c_void_p(left.data_ptr())
-        else:
-            basis, left = np.zeros(rows), np.zeros(lrows)
-            bptr, lptr = C.c_void_p(basis.ctypes.data), C.c_void_p(left.ctypes.data)
-        st = lib().mlsqr_solve_basis(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
-                                     _ptr(al), _ptr(be), bptr, lptr, C.byref(info), kind)
-    elif cgn:
-        st = lib().mlsqr_cg_normal_solve(op.h, pc.h if pc is not None else None, gp, tau, C.byref(sc), fptr, tr,
-                                         C.byref(info), kind)
+            t = torch.empty(count, dtype=torch.float64, device=g.device)
+            return t, C.c_void_p(t.data_ptr())
+        a = np.zeros(count)
+        return a, C.c_void_p(a.ctypes.data)
+
+    if f_out is None:
+        f, fptr = buf(op.n_cols)
+    else:
+        f = f_out
+        fptr = C.c_void_p(f.data_ptr() if kind == DEVICE else f.ctypes.data)
+    sc = stop._c()
+    opts = _SolveOpts()
+    basis = left = snaps = None
+    if store_basis and not cgn:
+        basis, opts.basis = buf((k + 1) * op.n_cols)
+        left, opts.left_basis = buf((k + 1) * op.n_rows)
+        opts.store_basis = 1
+    if record_snapshots:
+        snaps, opts.snapshots = buf(k * op.n_cols)
+        opts.record_snapshots = 1
+    pch = pc.h if pc is not None else None
+    if cgn:
+        st = lib().mlsqr_cg_normal_solve_with(op.h, pch, gp, tau, C.byref(sc), C.byref(opts), fptr, tr,
+                                              C.byref(info), kind)
+    elif opts.store_basis or opts.record_snapshots:
+        st = lib().mlsqr_solve_with(op.h, pch, gp, tau, C.byref(sc), C.byref(opts), fptr, tr, _ptr(al),
+                                    _ptr(be), C.byref(info), kind)
     elif pc is None:
         st = lib().mlsqr_lsqr_solve(op.h, gp, tau, C.byref(sc), fptr, tr, _ptr(al), _ptr(be), C.byref(info), kind)
     else:
@@ -696,21 +718,27 @@ def _run(op: LinearOperator, pc: Optional[SpdMap], g, tau: float, stop: Stopping
     if basis is not None:
         basis = basis[:info.n_alphas * op.n_cols].reshape(info.n_alphas, op.n_cols)
         left_basis = left[:info.n_left_basis * op.n_rows].reshape(info.n_left_basis, op.n_rows)
+    if snaps is not None:
+        snaps = snaps[:info.iterations * op.n_cols].reshape(info.iterations, op.n_cols)
+    if cgn:
+        al, be = np.zeros(0), np.zeros(0)
+        info.n_alphas = info.n_betas = 0
     return SolveResult(f, info.iterations, STOP_NAMES[info.stop_reason], trace,
-                       al[:info.n_alphas].copy(), be[:info.n_betas].copy(), basis, left_basis)
+                       al[:info.n_alphas].copy(), be[:info.n_betas].copy(), basis, left_basis, snaps)
 
 
 def mlsqr(a: LinearOperator, msolver: SpdMap, g, tau: float, stop: StoppingConfig, f_out=None,
-          store_basis: bool = False) -> SolveResult:
-    """Factorization-free priorconditioned LSQR (krylov.hpp:89-95).  store_basis
-    (SolveOptions, krylov.hpp:77-79) also returns the right basis vtilde_1..k as `.basis`."""
-    return _run(a, msolver, g, tau, stop, f_out, store_basis=store_basis)
+          store_basis: bool = False, record_snapshots: bool = False) -> SolveResult:
+    """Factorization-free priorconditioned LSQR (krylov.hpp:89-95).  SolveOptions (krylov.hpp:77-80):
+    store_basis also returns the right basis vtilde_1..k as `.basis`; record_snapshots the iterate
+    after every iteration as `.snapshots`."""
+    return _run(a, msolver, g, tau, stop, f_out, store_basis=store_basis, record_snapshots=record_snapshots)
 
 
 def lsqr(a: LinearOperator, g, tau: float, stop: StoppingConfig, f_out=None,
-         store_basis: bool = False) -> SolveResult:
+         store_basis: bool = False, record_snapshots: bool = False) -> SolveResult:
     """Damped LSQR (krylov.hpp:80-87)."""
-    return _run(a, None, g, tau, stop, f_out, store_basis=store_basis)
+    return _run(a, None, g, tau, stop, f_out, store_basis=store_basis, record_snapshots=record_snapshots)
 
 
 def solve_projected(alphas, betas, beta1: float, tau: float) -> np.ndarray:
@@ -747,13 +775,32 @@ def reconstruct_from_basis(basis, y, ctx: Optional[Context] = None, f_out=None):
 
 
 def cg_normal(a: LinearOperator, m: Optional["VCycleMap"], tau: float, g, stop: StoppingConfig,
-              f_out=None) -> SolveResult:
+              f_out=None, record_snapshots: bool = False) -> SolveResult:
     """CG on the normal equation (A^T A + tau M) f = A^T g (krylov.hpp:116-122), the
     unpriorconditioned baseline.  M is the level-0 operator of the V-cycle map `m` (None when
     tau == 0).  Argument order follows the reference: (a, m, tau, g, stop)."""
     if m is not None and not isinstance(m, VCycleMap):
         raise ValueError("cg_normal's M comes from a VCycleMap (its level-0 edge operator)")
-    return _run(a, m, g, tau, stop, f_out, cgn=True)
+    return _run(a, m, g, tau, stop, f_out, cgn=True, record_snapshots=record_snapshots)
+
+
+def krylov_basis(a: LinearOperator, msolver: Optional[SpdMap], m: Optional["VCycleMap"], tau: float, g,
+                 k: int):
+    """krylov_basis (krylov.hpp:133-145): (vectors [count, n] host array, rank_exhausted) for
+    K^{A^T A} (msolver = m = None), K^{A^T A + tau M} (m) or K^{M^-1 A^T A} (msolver)."""
+    if m is not None and not isinstance(m, VCycleMap):
+        raise ValueError("krylov_basis's M comes from a VCycleMap (its level-0 edge operator)")
+    gp, gn, kind, keep = _vec_in(g)
+    if gn != a.n_rows:
+        raise DimensionError("right-hand side length mismatch")
+    out = np.zeros(max(int(k), 1) * a.n_cols)
+    cnt, ex = C.c_int(), C.c_int()
+    if kind == DEVICE:
+        gp = C.c_void_p(np.ascontiguousarray(g.cpu().numpy()).ctypes.data)
+    _check(lib().mlsqr_krylov_basis(a.h, msolver.h if msolver is not None else None,
+                                    m.h if m is not None else None, tau, gp, int(k),
+                                    C.c_void_p(out.ctypes.data), C.byref(cnt), C.byref(ex), HOST))
+    return out[:cnt.value * a.n_cols].reshape(cnt.value, a.n_cols), bool(ex.value)
 
 
 # ---------------------------------------------------------------------------

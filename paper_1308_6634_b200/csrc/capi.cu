@@ -500,51 +500,89 @@ int mlsqr_lsqr_solve(mlsqr_op* op, const double* g, double tau, const mlsqr_stop
   return run_solve(op, nullptr, g, tau, stop, f, trace, alphas, betas, info, ptr_kind, true);
 }
 
-int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
-                      double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
-                      double* left_basis, mlsqr_solve_info* info, int kind) {
+// mlsqr / lsqr with SolveOptions: basis, left basis and snapshots staged for HOST calls
+static int solve_with_impl(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                           double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
+                           double* left_basis, double* snaps, mlsqr_solve_info* info, int kind) {
   int bd_iter = 0;
   if (info) std::memset(info, 0, sizeof(*info));
   const int st = guard([&] {
-    require(op && stop && basis, MLSQR_EINVAL, "operator, stopping config and basis are required");
+    require(op && stop, MLSQR_EINVAL, "operator and stopping config are required");
     Op* o = op->impl;
     Ctx* c = o->ctx;
     set_device(c);
     In gin(c, g, o->rows, kind);
     Out fout(c, f, o->cols, kind);
     const size_t nb = ((size_t)stop->max_iters + 1) * o->cols;
-    DevBuf<double> staged, staged_l;
+    const size_t nl = ((size_t)stop->max_iters + 1) * o->rows;
+    const size_t ns = (size_t)stop->max_iters * o->cols;
+    DevBuf<double> staged, staged_l, staged_s;
     double* bd = basis;
     double* ld = left_basis;
-    const size_t nl = ((size_t)stop->max_iters + 1) * o->rows;
+    double* sd = snaps;
     if (kind != MLSQR_DEVICE) {
-      staged.alloc(nb);
-      bd = staged.p;
+      if (basis) {
+        staged.alloc(nb);
+        bd = staged.p;
+      }
       if (left_basis) {
         staged_l.alloc(nl);
         ld = staged_l.p;
+      }
+      if (snaps) {
+        staged_s.alloc(ns);
+        sd = staged_s.p;
       }
     }
     mlsqr_solve_info inf{};
     try {
       solve_mlsqr(o, pc ? pc->impl : nullptr, gin.d, tau, *stop, fout.d, trace, alphas, betas, &inf, nullptr, true, bd,
-                  ld);
+                  ld, sd);
     } catch (const Error& e) {
       if (e.code == MLSQR_EBREAKDOWN) bd_iter = e.iteration;
       if (info) *info = inf;
       throw;
     }
     if (info) *info = inf;
-    if (kind != MLSQR_DEVICE && inf.n_alphas > 0)
+    if (kind != MLSQR_DEVICE && basis && inf.n_alphas > 0)
       MLSQR_CUDA(cudaMemcpyAsync(basis, bd, sizeof(double) * (size_t)inf.n_alphas * o->cols, cudaMemcpyDeviceToHost,
                                  c->stream));
     if (kind != MLSQR_DEVICE && left_basis && inf.n_left_basis > 0)
       MLSQR_CUDA(cudaMemcpyAsync(left_basis, ld, sizeof(double) * (size_t)inf.n_left_basis * o->rows,
                                  cudaMemcpyDeviceToHost, c->stream));
+    if (kind != MLSQR_DEVICE && snaps && inf.iterations > 0)
+      MLSQR_CUDA(cudaMemcpyAsync(snaps, sd, sizeof(double) * (size_t)inf.iterations * o->cols,
+                                 cudaMemcpyDeviceToHost, c->stream));
     fout.finish();
   });
   if (st == MLSQR_EBREAKDOWN && info) info->breakdown_iteration = bd_iter;
   return st;
+}
+
+int mlsqr_solve_basis(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                      double* f, mlsqr_iter_rec* trace, double* alphas, double* betas, double* basis,
+                      double* left_basis, mlsqr_solve_info* info, int kind) {
+  if (!basis) {
+    g_err = "operator, stopping config and basis are required";
+    if (info) std::memset(info, 0, sizeof(*info));
+    return MLSQR_EINVAL;
+  }
+  return solve_with_impl(op, pc, g, tau, stop, f, trace, alphas, betas, basis, left_basis, nullptr, info, kind);
+}
+
+int mlsqr_solve_with(mlsqr_op* op, mlsqr_pc* pc, const double* g, double tau, const mlsqr_stop* stop,
+                     const mlsqr_solve_opts* opts, double* f, mlsqr_iter_rec* trace, double* alphas,
+                     double* betas, mlsqr_solve_info* info, int kind) {
+  mlsqr_solve_opts o{};
+  if (opts) o = *opts;
+  if ((o.record_snapshots && !o.snapshots) || (o.store_basis && !o.basis)) {
+    g_err = "SolveOptions requests an output without a buffer";
+    if (info) std::memset(info, 0, sizeof(*info));
+    return MLSQR_EINVAL;
+  }
+  return solve_with_impl(op, pc, g, tau, stop, f, trace, alphas, betas, o.store_basis ? o.basis : nullptr,
+                         o.store_basis ? o.left_basis : nullptr, o.record_snapshots ? o.snapshots : nullptr,
+                         info, kind);
 }
 
 int mlsqr_solve_projected(const double* alphas, size_t k, const double* betas, size_t n_betas, double beta1,
@@ -572,8 +610,8 @@ int mlsqr_reconstruct_from_basis(mlsqr_ctx* ctx, const double* basis, size_t n, 
   });
 }
 
-int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau, const mlsqr_stop* stop,
-                          double* f, mlsqr_iter_rec* trace, mlsqr_solve_info* info, int kind) {
+static int cg_normal_impl(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau, const mlsqr_stop* stop,
+                          double* f, mlsqr_iter_rec* trace, mlsqr_solve_info* info, double* snaps, int kind) {
   int bd_iter = 0;
   if (info) std::memset(info, 0, sizeof(*info));
   const int st = guard([&] {
@@ -585,15 +623,69 @@ int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau
     In gin(c, g, o->rows, kind);
     Out fout(c, f, o->cols, kind);
     try {
-      solve_cg_normal(o, m ? m->vc : nullptr, gin.d, tau, *stop, fout.d, trace, info);
+      DevBuf<double> staged;
+      double* sd = snaps;
+      if (snaps && kind != MLSQR_DEVICE) {
+        staged.alloc((size_t)stop->max_iters * o->cols);
+        sd = staged.p;
+      }
+      mlsqr_solve_info inf{};
+      solve_cg_normal(o, m ? m->vc : nullptr, gin.d, tau, *stop, fout.d, trace, &inf, sd);
+      if (info) *info = inf;
+      if (snaps && kind != MLSQR_DEVICE && inf.iterations > 0)
+        MLSQR_CUDA(cudaMemcpyAsync(snaps, sd, sizeof(double) * (size_t)inf.iterations * o->cols,
+                                   cudaMemcpyDeviceToHost, c->stream));
+      fout.finish();
     } catch (const Error& e) {
       if (e.code == MLSQR_EBREAKDOWN) bd_iter = e.iteration;
       throw;
     }
-    fout.finish();
   });
   if (st == MLSQR_EBREAKDOWN && info) info->breakdown_iteration = bd_iter;
   return st;
+}
+
+int mlsqr_cg_normal_solve(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau, const mlsqr_stop* stop,
+                          double* f, mlsqr_iter_rec* trace, mlsqr_solve_info* info, int kind) {
+  return cg_normal_impl(op, m, g, tau, stop, f, trace, info, nullptr, kind);
+}
+
+int mlsqr_cg_normal_solve_with(mlsqr_op* op, mlsqr_pc* m, const double* g, double tau, const mlsqr_stop* stop,
+                               const mlsqr_solve_opts* opts, double* f, mlsqr_iter_rec* trace,
+                               mlsqr_solve_info* info, int kind) {
+  if (opts && opts->record_snapshots && !opts->snapshots) {
+    g_err = "SolveOptions requests snapshots without a buffer";
+    if (info) std::memset(info, 0, sizeof(*info));
+    return MLSQR_EINVAL;
+  }
+  return cg_normal_impl(op, m, g, tau, stop, f, trace, info,
+                        opts && opts->record_snapshots ? opts->snapshots : nullptr, kind);
+}
+
+int mlsqr_krylov_basis(mlsqr_op* op, mlsqr_pc* msolver, mlsqr_pc* m, double tau, const double* g, int k,
+                       double* vectors, int* count, int* rank_exhausted, int kind) {
+  if (count) *count = 0;
+  if (rank_exhausted) *rank_exhausted = 0;
+  return guard([&] {
+    require(op && g && vectors && count && rank_exhausted, MLSQR_EINVAL, "krylov_basis: null argument");
+    require(m == nullptr || m->vc != nullptr, MLSQR_EINVAL, "krylov_basis's M comes from a V-cycle map");
+    require(k >= 1, MLSQR_EINVAL, "need at least one basis vector");
+    Op* o = op->impl;
+    Ctx* c = o->ctx;
+    set_device(c);
+    In gin(c, g, o->rows, kind);
+    DevBuf<double> staged;
+    double* vd = vectors;
+    if (kind != MLSQR_DEVICE) {
+      staged.alloc((size_t)k * o->cols);
+      vd = staged.p;
+    }
+    const int cnt = krylov_basis(o, msolver ? msolver->impl : nullptr, m ? m->vc : nullptr, tau, gin.d, k, vd,
+                                 rank_exhausted);
+    *count = cnt;
+    if (kind != MLSQR_DEVICE && cnt > 0)
+      MLSQR_CUDA(cudaMemcpy(vectors, vd, sizeof(double) * (size_t)cnt * o->cols, cudaMemcpyDeviceToHost));
+  });
 }
 
 int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, size_t ny,

@@ -72,7 +72,7 @@ __global__ void cgn_xpby_kernel(const double* __restrict__ r, double beta, doubl
 }  // namespace
 
 void solve_cg_normal(Op* op, VCycle* m, const double* g, double tau, const mlsqr_stop& stop,
-                     double* x, mlsqr_iter_rec* trace, mlsqr_solve_info* info) {
+                     double* x, mlsqr_iter_rec* trace, mlsqr_solve_info* info, double* snap) {
   Ctx* c = op->ctx;
   validate_stop(stop);
   require(tau >= 0.0, MLSQR_EINVAL, "tau must be nonnegative");
@@ -163,6 +163,9 @@ void solve_cg_normal(Op* op, VCycle* m, const double* g, double tau, const mlsqr
     row.cond_est = nan;
     row.xnorm_est = std::sqrt(xx);
     if (trace) trace[iter - 1] = row;
+    if (snap)  // SolveOptions::record_snapshots (krylov.cpp:608)
+      MLSQR_CUDA(cudaMemcpyAsync(snap + (size_t)(iter - 1) * n, x, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                 c->stream));
     inf.iterations = iter;
     if (stop.use_s4 && row.res_data <= stop.eta * stop.delta) {
       inf.stop_reason = MLSQR_STOP_S4;

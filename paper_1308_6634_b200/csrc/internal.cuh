@@ -418,7 +418,7 @@ void workspace_free(Workspace* w);
 int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
                 mlsqr_solve_info* info, Workspace* ws = nullptr, bool use_graph = true,
-                double* basis_dev = nullptr, double* left_dev = nullptr);
+                double* basis_dev = nullptr, double* left_dev = nullptr, double* snap_dev = nullptr);
 // solve_projected (krylov.cpp:631-678), host arithmetic (projected.cu)
 std::vector<double> solve_projected(const double* alphas, size_t k, const double* betas, size_t nb,
                                     double beta1, double tau);
@@ -426,7 +426,11 @@ void reconstruct_from_basis(Ctx* c, const double* basis, size_t n, const double*
 void validate_stop(const mlsqr_stop& s);
 // cg_normal (krylov.cpp:551-628) on the device; M = the V-cycle's level-0 operator (cgn.cu)
 void solve_cg_normal(Op* op, VCycle* m, const double* g, double tau, const mlsqr_stop& stop,
-                     double* f_dev, mlsqr_iter_rec* trace, mlsqr_solve_info* info);
+                     double* f_dev, mlsqr_iter_rec* trace, mlsqr_solve_info* info,
+                     double* snap_dev = nullptr);
+// krylov_basis (krylov.cpp:700-754) on the device (basis.cu); returns the vector count
+int krylov_basis(Op* op, Pc* msolver, VCycle* m, double tau, const double* g, int k, double* vecs,
+                 int* rank_exhausted);
 // stateful outer step (outer.cu)
 class OuterSolver {
  public:

@@ -255,6 +255,15 @@ __global__ void left_basis_kernel(DevState* __restrict__ s, const double* __rest
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
     out[i] = u[i] * su;
 }
+// SolveOptions::record_snapshots (krylov.cpp:159-161): f after this iteration's update, row
+// iter-1, for every iteration that records a trace row (active at its start)
+__global__ void snapshot_kernel(const DevState* __restrict__ s, const double* __restrict__ f,
+                                double* __restrict__ snaps, size_t n) {
+  if (!s->flags[0]) return;
+  double* row = snaps + (size_t)(s->iter - 1) * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    row[i] = f[i];
+}
 __global__ void left_count_kernel(DevState* s, int in_loop) {
   if (!s->flags[0] || (in_loop && !s->flags[1])) return;
   s->n_left = in_loop ? s->n_left + 1 : 1;
@@ -417,6 +426,14 @@ struct Runner {
   Ctx* c;
   double* basis = nullptr;  // [(max_iters + 1) x cols] when the basis is stored
   double* lbasis = nullptr; // [(max_iters + 1) x rows] left basis
+  double* snaps = nullptr;  // [max_iters x cols] f snapshots (record_snapshots)
+  void store_snapshot() {
+    if (!snaps) return;
+    const size_t n = op->cols;
+    const unsigned g = (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    snapshot_kernel<<<g, 256, 0, c->stream>>>(st, ws->f.p, snaps, n);
+    c->count();
+  }
   void store_left(int in_loop) {
     if (!lbasis) return;
     const size_t m = op->rows;
@@ -556,6 +573,7 @@ struct Runner {
       op->apply(ws->f.p, ws->tmp_rows.p, er);
       reduce(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active(), true);
     }
+    store_snapshot();
     fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
     join_vghost();
     c->count(5);
@@ -568,7 +586,7 @@ struct Runner {
 int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_stop& stop,
                 double* f_dev, mlsqr_iter_rec* trace, double* alphas, double* betas,
                 mlsqr_solve_info* info, Workspace* ws_in, bool use_graph, double* basis_dev,
-                double* left_dev) {
+                double* left_dev, double* snap_dev) {
   Ctx* c = op->ctx;
   validate_stop(stop);
   require(tau >= 0.0, MLSQR_EINVAL, "tau must be nonnegative");
@@ -604,7 +622,7 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
   ws->f.p = f_dev;
   ws->f.n = op->cols;
 
-  Runner r{op, pc, ws, tau, stop, ws->st.p, c, basis_dev, left_dev};
+  Runner r{op, pc, ws, tau, stop, ws->st.p, c, basis_dev, left_dev, snap_dev};
   const bool host_cb = pc && pc->host_callback();
   const bool graph = use_graph && !host_cb && !c->timing && (!c->comm || c->comm->capturable());
   r.init(g_dev);

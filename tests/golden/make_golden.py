@@ -198,6 +198,23 @@ def main():
                 out[f"{backend}_maps_{tag}_{kind}_cg7"] = r.map_solve(
                     r.map_assembled(dims, shape, h, f, kind, T, inner_cg=7), p)
 
+    # --- krylov_basis (krylov.cpp:700-754): the three spaces the runner dumps (runner.cpp:245-275)
+    for backend in ("scalar", "avx2"):
+        assert r.select_backend(backend == "scalar"), backend
+        ft, gg = out["scalar_deconv_ftrue"], out["scalar_deconv_g"]
+        od = r.op_conv1d(128, 0.03)
+        out[f"{backend}_kb_plain"] = r.krylov_basis(od, 128, 6, gg)[0]
+        out[f"{backend}_kb_tauM"] = r.krylov_basis(od, 128, 6, gg, tau=0.1,
+                                                   m=(1, (128,), 1 / 128, ft, "pm_log", 0.005, -1.0))[0]
+        out[f"{backend}_kb_pc"] = r.krylov_basis(
+            od, 128, 4, gg, md=r.map_assembled(1, (128,), 1 / 128, ft, "pm_log", 0.005))[0]
+        out[f"{backend}_kb_pc_cg"] = r.krylov_basis(
+            od, 128, 4, gg, md=r.map_assembled(1, (128,), 1 / 128, ft, "pm_log", 0.005, inner_cg=8))[0]
+        # rank exhaustion: 3x3 identity has a 1-D Krylov space
+        kb, ex = r.krylov_basis(r.op_identity(3), 3, 3, np.array([1.0, 2.0, 3.0]))
+        out[f"{backend}_kb_ident"] = kb
+        out[f"{backend}_kb_ident_exhausted"] = np.array(int(ex))
+
     # --- SignFlipMap breakdown (test_krylov.cpp:131-145)
     @VEC_FN
     def flip(ctx, p, v):

@@ -643,3 +643,64 @@ def test_mlsqr_with_reference_spd_solvers(ctx, dev, golden, mode, tau):
         ref = golden[f"scalar_deconv_tau{tau}_f"]
         assert gres.iterations == int(golden[f"scalar_deconv_tau{tau}_iters"])
         assert rel(gres.solution, ref) <= max(1e-6, 10 * rel(golden[f"avx2_deconv_tau{tau}_f"], ref))
+
+
+# ---------------------------------------------------------------------------
+# SolveOptions::record_snapshots and krylov_basis (the runner's trace / basis artifacts)
+# ---------------------------------------------------------------------------
+def test_snapshots_bit_exact(ctx, dev, golden):
+    """record_snapshots (krylov.cpp:159-161, 608): f after every recorded iteration."""
+    n = 128
+    ft, g = golden["scalar_deconv_ftrue"], golden["scalar_deconv_g"]
+    a = mb.SeparableGaussianBlur((n,), sigma_f=0.03)
+    m = mb.VCycleMap((n,), 1 / n, 1)
+    eps = m.update(ft, mb.PenaltySpec("pm_log", 0.005))
+    delta = 0.01 / np.sqrt(1.0 / n)
+    st = mb.StoppingConfig.discrepancy(delta, 1.1, 25)
+    grid = dev.grid(1, (n,), 1 / n)
+    cx, cy, cz = dev.edge_coeffs(grid, ft, "pm_log", 0.005)
+    o = dev.blur(1, (n,), dev.taps(n, 0.03))
+    for pc, om in ((mb.CholeskyMap(m), dev.env_chol_map(grid, cx, cy, cz, eps)), (None, None)):
+        gres = mb.mlsqr(a, pc, g, 0.0, st, record_snapshots=True) if pc else \
+            mb.lsqr(a, g, 0.0, st, record_snapshots=True)
+        ores = dev.mlsqr(o, om, g, 0.0, ostop_from(st), snapshots=True, lsqr=pc is None)
+        compare_solves(gres, ores)
+        assert gres.snapshots.shape == (gres.iterations, n)
+        assert np.array_equal(gres.snapshots, ores.snapshots)
+        assert np.array_equal(gres.snapshots[-1], gres.solution)
+    # cg_normal: snapshots of x, last == solution
+    r = mb.cg_normal(a, m, 0.1, g, mb.StoppingConfig(max_iters=12), record_snapshots=True)
+    assert r.snapshots.shape == (12, n) and np.array_equal(r.snapshots[-1], r.solution)
+    r2 = mb.cg_normal(a, m, 0.1, g, mb.StoppingConfig(max_iters=5))
+    assert np.array_equal(r.snapshots[4], r2.solution)
+
+
+def test_krylov_basis_bit_exact(ctx, dev, golden):
+    """krylov_basis (krylov.cpp:700-754) in the three spaces: bit-exact vs the oracle's device
+    order, and vs the reference's own vectors to its scalar-vs-AVX2 spread."""
+    n = 128
+    ft, g = golden["scalar_deconv_ftrue"], golden["scalar_deconv_g"]
+    a = mb.SeparableGaussianBlur((n,), sigma_f=0.03)
+    m = mb.VCycleMap((n,), 1 / n, 1)
+    eps = m.update(ft, mb.PenaltySpec("pm_log", 0.005))
+    grid = dev.grid(1, (n,), 1 / n)
+    cx, cy, cz = dev.edge_coeffs(grid, ft, "pm_log", 0.005)
+    o = dev.blur(1, (n,), dev.taps(n, 0.03))
+    cases = [
+        ("plain", mb.krylov_basis(a, None, None, 0.0, g, 6), dev.krylov_basis(o, None, 6, g)),
+        ("tauM", mb.krylov_basis(a, None, m, 0.1, g, 6),
+         dev.krylov_basis(o, None, 6, g, tau=0.1, m=(grid, cx, cy, cz, eps))),
+        ("pc", mb.krylov_basis(a, mb.CholeskyMap(m), None, 0.0, g, 4),
+         dev.krylov_basis(o, dev.env_chol_map(grid, cx, cy, cz, eps), 4, g)),
+        ("pc_cg", mb.krylov_basis(a, mb.InnerCgMap(m, 8), None, 0.0, g, 4),
+         dev.krylov_basis(o, dev.inner_cg_map(grid, cx, cy, cz, eps, 8), 4, g)),
+    ]
+    for name, (kb, ex), (okb, oex) in cases:
+        assert kb.shape == okb.shape and ex == oex and np.array_equal(kb, okb), name
+        ref = golden[f"scalar_kb_{name}"]
+        floor = rel(golden[f"avx2_kb_{name}"], ref)
+        assert rel(kb, ref) <= max(1e-9, 10 * floor), name
+    kb, ex = mb.krylov_basis(mb.IdentityOperator(3), None, None, 0.0, np.array([1.0, 2.0, 3.0]), 3)
+    assert kb.shape == (1, 3) and ex
+    with pytest.raises(ValueError):
+        mb.krylov_basis(a, mb.CholeskyMap(m), m, 0.1, g, 3)

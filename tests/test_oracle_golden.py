@@ -312,3 +312,27 @@ def test_inner_cg_device_order_agrees_to_rounding(orc, golden):
         orc.set_device_order(False)
     assert rel(dev, ref) < 1e-12
     assert np.array_equal(c1, golden[f"scalar_maps_{tag}_tv_chol"])
+
+
+def test_krylov_basis_bit_exact(orc, golden):
+    """krylov_basis (krylov.cpp:700-754) in its three spaces, bit-exact with the reference's
+    scalar backend; rank exhaustion as KrylovBasis::rank_exhausted."""
+    ft, g = golden["scalar_deconv_ftrue"], golden["scalar_deconv_g"]
+    n = 128
+    op = orc.blur(1, (n,), orc.taps(n, 0.03))
+    grid = orc.grid(1, (n,), 1 / n)
+    cx, cy, cz = orc.edge_coeffs(grid, ft, "pm_log", 0.005)
+    eps = 1e-8 * orc.max_diag(grid, cx, cy, cz)
+    kb, ex = orc.krylov_basis(op, None, 6, g)
+    assert np.array_equal(kb, golden["scalar_kb_plain"]) and not ex
+    kb, _ = orc.krylov_basis(op, None, 6, g, tau=0.1, m=(grid, cx, cy, cz, eps))
+    assert np.array_equal(kb, golden["scalar_kb_tauM"])
+    kb, _ = orc.krylov_basis(op, orc.env_chol_map(grid, cx, cy, cz, eps), 4, g)
+    assert np.array_equal(kb, golden["scalar_kb_pc"])
+    kb, _ = orc.krylov_basis(op, orc.inner_cg_map(grid, cx, cy, cz, eps, 8), 4, g)
+    assert np.array_equal(kb, golden["scalar_kb_pc_cg"])
+    kb, ex = orc.krylov_basis(orc.identity(3), None, 3, np.array([1.0, 2.0, 3.0]))
+    assert np.array_equal(kb, golden["scalar_kb_ident"]) and ex == bool(golden["scalar_kb_ident_exhausted"])
+    # orthonormal (the reference's own property)
+    kb, _ = orc.krylov_basis(op, None, 6, g)
+    assert np.abs(kb @ kb.T - np.eye(6)).max() < 1e-10
