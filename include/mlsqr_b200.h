@@ -267,7 +267,13 @@ typedef struct {            /* OuterConfig (outer.hpp:13-28) with a V-cycle M^{-
   double epsilon;                 /* < 0: auto shift */
   int mg_levels, nu_pre, nu_post, coarse_sweeps;
   double omega;
+  int spd_mode;  /* M^{-1} per outer step: MLSQR_SPD_VCYCLE (mg_* fields), MLSQR_SPD_CHOLESKY or
+                    MLSQR_SPD_INNER_CG (SpdSolverMode, spdsolve.hpp:35-38; outer.cpp:64-70) */
+  int k_inner;   /* inner-CG iteration count */
 } mlsqr_outer_cfg;
+#define MLSQR_SPD_VCYCLE 0
+#define MLSQR_SPD_CHOLESKY 1
+#define MLSQR_SPD_INNER_CG 2
 
 typedef struct {            /* OuterStep (outer.hpp:33-41) */
   int k;

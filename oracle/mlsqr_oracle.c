@@ -1357,12 +1357,14 @@ int orc_nonlinear(const orc_linop* a, const double* g, const orc_grid* grid,
 
   /* mg_levels == 0: exact dense Cholesky of the assembled M per outer step, i.e. the
    * reference's SpdSolverMode::direct_cholesky (outer.cpp:64-67); small grids only. */
-  const int dense_mode = cfg->mg_levels == 0;
+  const int stencil_mode = cfg->spd_mode == 1 || cfg->spd_mode == 2;
+  if (cfg->spd_mode < 0 || cfg->spd_mode > 2 || (cfg->spd_mode == 2 && cfg->k_inner < 1)) return ORC_EINVAL;
+  const int dense_mode = !stencil_mode && cfg->mg_levels == 0;
   orc_map* mg = NULL;
   double* mdense = NULL;
   if (dense_mode) {
     mdense = (double*)malloc(sizeof(double) * n * n);
-  } else {
+  } else if (!stencil_mode) {
     mg = orc_vcycle_new(grid, cfg->mg_levels, cfg->nu_pre, cfg->nu_post, cfg->omega,
                         cfg->coarse_sweeps);
     if (!mg) return ORC_EINVAL;
@@ -1382,7 +1384,12 @@ int orc_nonlinear(const orc_linop* a, const double* g, const orc_grid* grid,
     orc_edge_coeffs(grid, prev, cfg->pen_kind, cfg->T, cx, cy, cz);
     const double eps = cfg->epsilon >= 0.0 ? cfg->epsilon
                                            : 1e-8 * orc_max_diag(grid, cx, cy, cz);
-    if (dense_mode) {
+    if (stencil_mode) { /* outer.cpp:64-70: this step's SpdSolver */
+      orc_map_free(mg);
+      mg = cfg->spd_mode == 1 ? orc_env_chol_map_new(grid, cx, cy, cz, eps, NULL)
+                              : orc_inner_cg_map_new(grid, cx, cy, cz, eps, cfg->k_inner);
+      if (!mg) { st = ORC_EINVAL; break; }
+    } else if (dense_mode) {
       double* e = (double*)calloc(n, sizeof(double));
       double* col = (double*)malloc(sizeof(double) * n);
       for (size_t j = 0; j < n; ++j) {

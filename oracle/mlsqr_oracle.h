@@ -161,6 +161,9 @@ typedef struct {
   double epsilon;                /* < 0: auto shift 1e-8 * max diag */
   int mg_levels, nu_pre, nu_post, coarse_sweeps;
   double omega;
+  int spd_mode; /* 0: V-cycle (mg_levels > 0) or dense Cholesky (mg_levels == 0);
+                   1: envelope Cholesky (SpdSolver::factorize); 2: inner CG (k_inner) */
+  int k_inner;
 } orc_outer_cfg;
 
 typedef struct {

@@ -68,7 +68,8 @@ class OuterCfg(C.Structure):
                 ("inner_stop", Stop), ("inner_cap", C.c_int),
                 ("rel_decrease_threshold", C.c_double), ("max_outer", C.c_int),
                 ("epsilon", C.c_double), ("mg_levels", C.c_int), ("nu_pre", C.c_int),
-                ("nu_post", C.c_int), ("coarse_sweeps", C.c_int), ("omega", C.c_double)]
+                ("nu_post", C.c_int), ("coarse_sweeps", C.c_int), ("omega", C.c_double),
+                ("spd_mode", C.c_int), ("k_inner", C.c_int)]
 
 
 class OuterStep(C.Structure):
@@ -361,9 +362,9 @@ class Oracle:
 
     def nonlinear(self, op, g, grid, *, tau, pen, T, inner_stop, inner_cap, max_outer,
                   threshold=0.0, epsilon=-1.0, levels=3, nu_pre=2, nu_post=2, coarse_sweeps=4,
-                  omega=2.0 / 3.0, keep=False):
+                  omega=2.0 / 3.0, keep=False, spd_mode=0, k_inner=30):
         cfg = OuterCfg(tau, PEN.get(pen, pen), T, inner_stop, inner_cap, threshold, max_outer,
-                       epsilon, levels, nu_pre, nu_post, coarse_sweeps, omega)
+                       epsilon, levels, nu_pre, nu_post, coarse_sweeps, omega, spd_mode, k_inner)
         n = op.cols
         f = np.zeros(n)
         steps = (OuterStep * max_outer)()

@@ -66,6 +66,7 @@ class FactorizationError(RuntimeError):
 OK, EDIM, EINVAL, EBREAKDOWN, ECUDA, ENCCL, ECALLBACK, EFACTOR = 0, 1, 2, 3, 4, 5, 6, 7
 HOST, DEVICE = 0, 1
 STOP_NAMES = ["S1", "S2", "S3", "S4", "max_iters", "breakdown"]
+SPD_MODES = {"vcycle": 0, "cholesky": 1, "inner_cg": 2}
 PEN_KINDS = {"tikhonov": 0, "tv": 1, "tv_smoothed": 1, "pm_log": 2, "perona_malik_log": 2,
              "pm_exp": 3, "perona_malik_exp": 3}
 dp = C.POINTER(C.c_double)
@@ -97,7 +98,8 @@ class _OuterCfg(C.Structure):
     _fields_ = [("tau", C.c_double), ("pen_kind", C.c_int), ("T", C.c_double), ("inner_stop", _Stop),
                 ("inner_cap", C.c_int), ("rel_decrease_threshold", C.c_double), ("max_outer", C.c_int),
                 ("epsilon", C.c_double), ("mg_levels", C.c_int), ("nu_pre", C.c_int),
-                ("nu_post", C.c_int), ("coarse_sweeps", C.c_int), ("omega", C.c_double)]
+                ("nu_post", C.c_int), ("coarse_sweeps", C.c_int), ("omega", C.c_double),
+                ("spd_mode", C.c_int), ("k_inner", C.c_int)]
 
 
 class _OuterStep(C.Structure):
@@ -856,12 +858,14 @@ class OuterConfig:
     nu_post: int = 2
     coarse_sweeps: int = 4
     omega: float = 2.0 / 3.0
+    spd_mode: str = "vcycle"  # SpdSolverMode: "vcycle" | "cholesky" | "inner_cg" (outer.cpp:64-70)
+    k_inner: int = 30
 
     def _c(self) -> _OuterCfg:
         return _OuterCfg(self.tau, self.penalty.kind_code, self.penalty.threshold, self.inner_stop._c(),
                          self.inner_cap, self.rel_decrease_threshold, self.max_outer,
                          -1.0 if self.epsilon is None else self.epsilon, self.mg_levels, self.nu_pre,
-                         self.nu_post, self.coarse_sweeps, self.omega)
+                         self.nu_post, self.coarse_sweeps, self.omega, SPD_MODES[self.spd_mode], self.k_inner)
 
 
 @dataclass

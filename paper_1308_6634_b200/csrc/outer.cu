@@ -40,8 +40,14 @@ OuterSolver::OuterSolver(Op* o, int dims, size_t nx, size_t ny, size_t nz, doubl
   require(o->sol_shape.len == nx, MLSQR_EDIM, "operator solution rows must follow the grid x extent");
   inner_ = cfg.inner_stop;
   if (cfg.inner_cap < inner_.max_iters) inner_.max_iters = cfg.inner_cap;
-  vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, cfg.mg_levels, cfg.nu_pre, cfg.nu_post, cfg.omega,
-                    cfg.coarse_sweeps);
+  require(cfg.spd_mode >= MLSQR_SPD_VCYCLE && cfg.spd_mode <= MLSQR_SPD_INNER_CG, MLSQR_EINVAL,
+          "unknown SpdSolver mode");
+  require(cfg.spd_mode != MLSQR_SPD_INNER_CG || cfg.k_inner >= 1, MLSQR_EINVAL, "inner-CG mode needs k_inner >= 1");
+  if (cfg.spd_mode == MLSQR_SPD_VCYCLE)
+    vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, cfg.mg_levels, cfg.nu_pre, cfg.nu_post, cfg.omega,
+                      cfg.coarse_sweeps);
+  else  // a one-level V-cycle is the device holder of M; the SpdSolver is rebuilt from it per step
+    vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, 1, 1, 0, 1.0, 1);
   ws_ = workspace_new(o->ctx, o->rows, o->cols, o->data_shape, o->sol_shape, inner_.max_iters, op_guard(o));
   RowShape s{nx, ey * ez};
   const size_t J = s.segments(), G = dist_gather_size(o->ctx, J);
@@ -69,8 +75,12 @@ void OuterSolver::step(const double* g, const double* f_prev, double* f_out, mls
                        int k) {
   Ctx* c = op->ctx;
   vcycle_update_async(vc_, f_prev, cfg_.pen_kind, cfg_.T, cfg_.epsilon);
+  // outer.cpp:64-70: SpdSolver::factorize / inner_cg of this step's M, or the V-cycle itself
+  std::unique_ptr<Pc> solver;
+  if (cfg_.spd_mode == MLSQR_SPD_CHOLESKY) solver.reset(make_chol_map(vc_, nullptr));
+  if (cfg_.spd_mode == MLSQR_SPD_INNER_CG) solver.reset(make_inner_cg_map(vc_, cfg_.k_inner));
   mlsqr_solve_info info{};
-  solve_mlsqr(op, vcycle_as_pc(vc_), g, cfg_.tau, inner_, f_out, trace_.data(), al_.data(),
+  solve_mlsqr(op, solver ? solver.get() : vcycle_as_pc(vc_), g, cfg_.tau, inner_, f_out, trace_.data(), al_.data(),
               be_.data(), &info, ws_);
   penalty_functional_async(c, dims_, nx_, ny_, nz_, h_, f_out, cfg_.pen_kind, cfg_.T, pseg_.p,
                            pscr_.p, pgat_.p, pfg_.p ? pfg_.p + nx_ * (dims_ >= 2 ? ny_ : 1) : nullptr,

@@ -170,16 +170,18 @@ def test_mlsqr_deblur2d(orc, golden):
         assert own[:15].max() < 1e-13 and own[20:].max() > 1e-3
 
 
+@pytest.mark.parametrize("spd_mode", [0, 1])
 @pytest.mark.parametrize("pen,T", [("pm_log", 0.005), ("tikhonov", 1.0), ("tv", 0.01)])
-def test_nonlinear_outer_loop_scalar_bit_exact(orc, golden, pen, T):
-    """outer.cpp:40-100 restated; with the exact Cholesky M^-1 the restatement
-    reproduces the reference's scalar backend bit-for-bit over every outer step."""
+def test_nonlinear_outer_loop_scalar_bit_exact(orc, golden, pen, T, spd_mode):
+    """outer.cpp:40-100 restated; with the exact Cholesky M^-1 (dense, or the envelope
+    SpdSolver::factorize restatement the device mirrors) the restatement reproduces the
+    reference's scalar backend bit-for-bit over every outer step."""
     n = 128
     g = golden["scalar_deconv_g"]
     st = stop(1000, s4=True, delta=0.01 / np.sqrt(1 / n), eta=1.1)
     rep = orc.nonlinear(orc.blur(1, (n,), orc.taps(n, 0.03)), g, orc.grid(1, (n,), 1 / n), tau=0.0,
                         pen=pen, T=T, inner_stop=st, inner_cap=20, max_outer=25, threshold=0.15,
-                        levels=0, keep=True)
+                        levels=0, keep=True, spd_mode=spd_mode)
     pre = f"scalar_outer_{pen}"
     assert rep["triggered_at"] == int(golden[pre + "_trigger"])
     assert [s["inner_iterations"] for s in rep["steps"]] == list(golden[pre + "_inner"])
