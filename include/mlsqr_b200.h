@@ -113,6 +113,12 @@ int mlsqr_ctx_set_row_shard(mlsqr_ctx* ctx, size_t rows_global, size_t row_offse
  * values, identical on every axis; zero extension; self-adjoint. */
 int mlsqr_blur_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
                       const double* taps, int radius, mlsqr_op** out);
+/* SeparableGaussianBlur2D (linop.hpp:110-126, linop.cpp:142-170) with one factor per axis,
+ * kx_(nx) and ky_(ny) (linop.cpp:144-147): on a non-square grid the spacings 1/nx, 1/ny give
+ * different taps and radii.  x pass then y pass, separate mul + add: bit-identical to the
+ * reference's scalar backend. */
+int mlsqr_blur2d_create_axes(mlsqr_ctx* ctx, size_t nx, size_t ny, const double* taps_x, int radius_x,
+                             const double* taps_y, int radius_y, mlsqr_op** out);
 /* DenseOperator (linop.hpp:59-71): row-major rows x cols.  a_kind HOST copies to device.
  * sol_row_len: row length of solution-space vectors for the canonical reductions
  * (the x-extent of the voxel grid; 0 = cols). */

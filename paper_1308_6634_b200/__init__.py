@@ -129,6 +129,8 @@ SIGNATURES = {
     "mlsqr_ctx_set_row_shard": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
     "mlsqr_blur_create": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, dp,
                                     C.c_int, C.POINTER(C.c_void_p)]),
+    "mlsqr_blur2d_create_axes": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, dp, C.c_int, dp, C.c_int,
+                                           C.POINTER(C.c_void_p)]),
     "mlsqr_dense_create": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
                                      C.c_size_t, C.POINTER(C.c_void_p)]),
     "mlsqr_dense_create_fdot": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, dp, dp,
@@ -405,7 +407,7 @@ class SeparableGaussianBlur(LinearOperator):
     reference's ceil(6 sigma / h)."""
 
     def __init__(self, shape, sigma_f: Optional[float] = None, radius: Optional[int] = None,
-                 taps=None, ctx: Optional[Context] = None):
+                 taps=None, ctx: Optional[Context] = None, taps_y=None):
         ctx = ctx or default_context()
         shape = tuple(int(s) for s in shape)
         dims = len(shape)
@@ -414,8 +416,17 @@ class SeparableGaussianBlur(LinearOperator):
         taps = _f64(taps)
         nx, ny, nz = (list(shape) + [1, 1])[:3]
         h = C.c_void_p()
-        _check(lib().mlsqr_blur_create(ctx.h, dims, nx, ny, nz, _ptr(taps), (taps.size - 1) // 2, C.byref(h)))
-        self.grid_shape, self.taps = shape, taps
+        if taps_y is None and dims == 2 and nx != ny and sigma_f is not None and radius is None:
+            # the reference's 2D operator builds ky_(ny, sigma_f) on its own spacing (linop.cpp:144-147)
+            taps_y = gaussian_taps(ny, sigma_f, -1)
+        if taps_y is not None:
+            ty = _f64(taps_y)
+            _check(lib().mlsqr_blur2d_create_axes(ctx.h, nx, ny, _ptr(taps), (taps.size - 1) // 2, _ptr(ty),
+                                                  (ty.size - 1) // 2, C.byref(h)))
+        else:
+            _check(lib().mlsqr_blur_create(ctx.h, dims, nx, ny, nz, _ptr(taps), (taps.size - 1) // 2,
+                                           C.byref(h)))
+        self.grid_shape, self.taps, self.taps_y = shape, taps, taps_y
         super().__init__(h, ctx)
 
 

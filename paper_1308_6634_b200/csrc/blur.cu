@@ -24,7 +24,8 @@
 
 namespace mlsqr_b200 {
 
-constexpr int kMaxRadius = 36;
+constexpr int kMaxRadius = 36;   // taps passed by value (tile / fused kernels)
+constexpr int kMaxWide = 512;    // 1D / 2D pass kernels with taps in device memory
 
 struct Taps {
   double t[2 * kMaxRadius + 1];
@@ -95,9 +96,16 @@ __global__ void __launch_bounds__(256) blur2d_tile_kernel(const double* __restri
 // ---------------------------------------------------------------------------
 // generic single-axis pass (1D operator; z pass of the generic 3D path)
 // ---------------------------------------------------------------------------
-template <int AXIS, bool FMA>
+// taps by value (kernel parameter, radius <= kMaxRadius) or from device memory (wide kernels:
+// the reference's 6 sigma radius on fine 1D/2D grids, e.g. deconv1d n = 512, sigma 0.03 -> R = 93)
+struct WideTaps {
+  const double* t;
+  int R;
+};
+
+template <int AXIS, bool FMA, class TT = Taps>
 __global__ void blur_pass_kernel(const double* __restrict__ in, double* __restrict__ out,
-                                 size_t nx, size_t ny, size_t nz, Taps taps, EpiArgs e,
+                                 size_t nx, size_t ny, size_t nz, TT taps, EpiArgs e,
                                  bool first, bool last) {
   if (e.gate && *e.gate == 0) return;
   const size_t rows = ny * nz;
@@ -158,14 +166,27 @@ class BlurOp final : public Op {
   BlurOp(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, const double* taps, int radius)
       : dims_(dims), nx_(nx), ny_(dims >= 2 ? ny : 1), nz_(dims >= 3 ? nz : 1) {
     ctx = c;
-    require(radius >= 0 && radius <= kMaxRadius, MLSQR_EINVAL,
-            "blur radius must lie in [0, " + std::to_string(kMaxRadius) + "]");
+    require(radius >= 0 && radius <= (dims <= 2 ? kMaxWide : kMaxRadius), MLSQR_EINVAL,
+            "blur radius must lie in [0, " + std::to_string(dims <= 2 ? kMaxWide : kMaxRadius) + "]");
     require(nx_ >= 1 && ny_ >= 1 && nz_ >= 1, MLSQR_EDIM, "blur grid must be non-empty");
+    if (radius > kMaxRadius) {
+      // wide 1D/2D taps live in device memory; 2D runs as x pass + y pass
+      wide_ = true;
+      dtx_.alloc((size_t)(2 * radius + 1));
+      MLSQR_CUDA(cudaMemcpy(dtx_.p, taps, sizeof(double) * (2 * radius + 1), cudaMemcpyHostToDevice));
+      dty_ = dtx_.p;
+      ry_ = radius;
+      if (dims_ == 2) {
+        axes_ = true;
+        tmp_.alloc(nx_ * ny_);
+      }
+      radius = 0;  // the by-value copy is unused
+    }
     for (int k = 0; k < 2 * radius + 1; ++k) taps_.t[k] = taps[k];
-    taps_.R = radius;
+    taps_.R = wide_ ? (int)(dtx_.n / 2) : radius;
     rows = cols = nx_ * ny_ * nz_;
     data_shape = sol_shape = RowShape{nx_, ny_ * nz_};
-    if (dims_ >= 2) {
+    if (dims_ >= 2 && !wide_) {
       smem_ = sizeof(double) * ((size_t)(kTY + 2 * radius) * (32 + 2 * radius) + (size_t)(kTY + 2 * radius) * 32);
       if (smem_ > 48 * 1024) {
         MLSQR_CUDA(cudaFuncSetAttribute(blur2d_tile_kernel<kTY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
@@ -204,6 +225,23 @@ class BlurOp final : public Op {
     }
   }
 
+  // SeparableGaussianBlur2D with per-axis factors (linop.cpp:142-149: kx_(nx), ky_(ny) -- a
+  // non-square grid has different spacings, hence different taps and radii per axis)
+  void set_y_taps(const double* ty, int ry) {
+    require(dims_ == 2 && !ctx->sharded(), MLSQR_EINVAL, "per-axis taps are for the 2D operator");
+    require(ry >= 0 && ry <= kMaxWide, MLSQR_EINVAL, "blur radius must lie in [0, " + std::to_string(kMaxWide) + "]");
+    if (!wide_) {  // move the x taps to device memory too: both passes read WideTaps
+      dtx_.alloc((size_t)(2 * taps_.R + 1));
+      MLSQR_CUDA(cudaMemcpy(dtx_.p, taps_.t, sizeof(double) * dtx_.n, cudaMemcpyHostToDevice));
+      wide_ = true;
+    }
+    dtyo_.alloc((size_t)(2 * ry + 1));
+    MLSQR_CUDA(cudaMemcpy(dtyo_.p, ty, sizeof(double) * dtyo_.n, cudaMemcpyHostToDevice));
+    dty_ = dtyo_.p;
+    ry_ = ry;
+    axes_ = true;
+    tmp_.alloc(rows);
+  }
   void apply(const double* x, double* y, const Epi& e) override { run(x, y, e); }
   void adjoint(const double* y, double* x, const Epi& e) override { run(y, x, e); }  // A = A^T
   int halo_planes_needed() const override { return ctx->sharded() && dims_ == 3 ? taps_.R : 0; }
@@ -227,14 +265,30 @@ class BlurOp final : public Op {
     const size_t rows_ = ny_ * nz_;
     dim3 blk(32, 8);
     dim3 grd((unsigned)((nx_ + 31) / 32), (unsigned)((rows_ + 7) / 8));
-    if (dims_ == 1) {
+    const WideTaps wx{dtx_.p, (int)(dtx_.n / 2)}, wy{dty_, ry_};
+    if (dims_ == 1 && wide_) {
+      blur_pass_kernel<0, false, WideTaps><<<grd, blk, 0, ctx->stream>>>(in, out, nx_, ny_, nz_, wx, a, true, true);
+      ctx->count();
+    } else if (dims_ == 1) {
       blur_pass_kernel<0, false><<<grd, blk, 0, ctx->stream>>>(in, out, nx_, ny_, nz_, taps_, a, true, true);
       ctx->count();
     } else if (dims_ == 3 && fused_) {
       fused3d(ctx, taps_.R, in, out, (int)nx_, (int)ny_, (int)nz_, taps_, a);
     } else {
       dim3 g2((unsigned)((nx_ + 31) / 32), (unsigned)((ny_ + kTY - 1) / kTY), (unsigned)nz_);
-      if (dims_ == 2) {
+      if (dims_ == 2 && axes_) {
+        // rows first (x, contiguous), then columns (linop.cpp:151-162), separate mul + add
+        EpiArgs first = a;
+        first.old = nullptr;
+        first.seg = nullptr;
+        blur_pass_kernel<0, false, WideTaps><<<grd, blk, 0, ctx->stream>>>(in, tmp_.p, nx_, ny_, nz_, wx, first, true,
+                                                                          false);
+        EpiArgs last = a;
+        last.sx = nullptr;
+        blur_pass_kernel<1, false, WideTaps><<<grd, blk, 0, ctx->stream>>>(tmp_.p, out, nx_, ny_, nz_, wy, last, false,
+                                                                          true);
+        ctx->count(2);
+      } else if (dims_ == 2) {
         blur2d_tile_kernel<kTY, false><<<g2, blk, smem_, ctx->stream>>>(in, out, (int)nx_, (int)ny_, (int)nz_, taps_, a);
         ctx->count();
       } else {
@@ -258,12 +312,28 @@ class BlurOp final : public Op {
   size_t smem_ = 0;
   bool fused_ = false;
   Taps taps_{};
+  bool axes_ = false;       // 2D as x pass + y pass with per-axis (device) taps
+  bool wide_ = false;       // taps in device memory (radius > kMaxRadius or per-axis)
+  DevBuf<double> dtx_, dtyo_;
+  const double* dty_ = nullptr;
+  int ry_ = 0;
   DevBuf<double> tmp_;
 };
 
 Op* make_blur(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, const double* taps, int radius) {
   require(dims >= 1 && dims <= 3, MLSQR_EINVAL, "blur dims must be 1, 2 or 3");
   return new BlurOp(c, dims, nx, ny, nz, taps, radius);
+}
+
+Op* make_blur2d_axes(Ctx* c, size_t nx, size_t ny, const double* tx, int rx, const double* ty, int ry) {
+  BlurOp* b = new BlurOp(c, 2, nx, ny, 1, tx, rx);
+  try {
+    b->set_y_taps(ty, ry);
+  } catch (...) {
+    delete b;
+    throw;
+  }
+  return b;
 }
 
 }  // namespace mlsqr_b200

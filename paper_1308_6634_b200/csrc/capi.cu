@@ -267,6 +267,15 @@ int mlsqr_ctx_set_row_shard(mlsqr_ctx* ctx, size_t rows_global, size_t row_offse
 }
 
 // ---- operators ----
+int mlsqr_blur2d_create_axes(mlsqr_ctx* ctx, size_t nx, size_t ny, const double* tx, int rx, const double* ty,
+                             int ry, mlsqr_op** out) {
+  return guard([&] {
+    require(ctx && tx && ty && out, MLSQR_EINVAL, "blur2d_create_axes: null argument");
+    set_device(&ctx->impl);
+    *out = new mlsqr_op{make_blur2d_axes(&ctx->impl, nx, ny, tx, rx, ty, ry)};
+  });
+}
+
 int mlsqr_blur_create(mlsqr_ctx* ctx, int dims, size_t nx, size_t ny, size_t nz,
                       const double* taps, int radius, mlsqr_op** out) {
   return guard([&] {

@@ -374,6 +374,7 @@ size_t dist_gather_size(Ctx* c, size_t nseg);
 // operator / map factories (blur.cu, dense.cu, vcycle.cu)
 // ---------------------------------------------------------------------------
 Op* make_blur(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, const double* taps, int radius);
+Op* make_blur2d_axes(Ctx* c, size_t nx, size_t ny, const double* tx, int rx, const double* ty, int ry);
 Op* make_dense(Ctx* c, size_t rows, size_t cols, const double* a, bool a_on_device,
                size_t sol_row_len);
 Op* make_dense_fdot(Ctx* c, size_t nvox, int nsrc, int ndet, const double* gs, const double* gd,

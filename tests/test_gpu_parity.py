@@ -53,6 +53,7 @@ BLUR_CASES = [
     (1, (50,), 0.05, 3), (1, (128,), 0.03, -1), (1, (1000,), 0.01, 12),
     (2, (40, 40), 0.05, 6), (2, (33, 21), 0.04, 4), (2, (128, 128), 2 / 128, 6),
     (2, (96, 64), 3 / 96, 9), (2, (64, 64), 0.05, 36),
+    (1, (512,), 0.03, -1), (2, (64, 64), 0.2, -1),  # wide: the reference's 6 sigma radius (R = 93, 77)
     (3, (16, 12, 10), 0.08, 3), (3, (32, 32, 32), 2 / 32, 6), (3, (40, 24, 20), 0.05, 4),
     (3, (20, 18, 16), 0.1, 7), (3, (64, 48, 80), 0.03, 6), (3, (33, 65, 70), 0.04, 12),
 ]
@@ -75,6 +76,16 @@ def test_blur_reference_radius_matches_reference_2d(ctx, orc, golden):
     assert np.array_equal(g.apply(golden["scalar_blur2d_40x40_x"]), golden["scalar_blur2d_40x40_y"])
     g1 = mb.SeparableGaussianBlur((50,), sigma_f=0.05)
     assert np.array_equal(g1.apply(golden["scalar_conv1d_x"]), golden["scalar_conv1d_y"])
+
+
+def test_blur2d_nonsquare_reference_bit_exact(ctx, golden):
+    # the reference's SeparableGaussianBlur2D(33, 21, 0.04): kx_(33) and ky_(21) have different
+    # spacings, taps and radii (linop.cpp:142-149); per-axis factors, bit-exact with its scalar backend
+    g = mb.SeparableGaussianBlur((33, 21), sigma_f=0.04)
+    assert g.taps_y is not None and g.taps_y.size != g.taps.size
+    x = golden["scalar_blur2d_33x21_x"]
+    assert np.array_equal(g.apply(x), golden["scalar_blur2d_33x21_y"])
+    assert np.array_equal(g.apply_adjoint(x), golden["scalar_blur2d_33x21_y"])
 
 
 def test_operator_dimension_errors(ctx):
