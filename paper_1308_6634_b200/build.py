@@ -66,14 +66,42 @@ def build(verbose: bool = True) -> str:
     cu, cpp = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), cu + cpp))
-    if _newer(LIB, objs):
+    lib_changed = _newer(LIB, objs)
+    if lib_changed:
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed\n{r.stdout}\n{r.stderr}")
         if verbose:
             print(f"  linked {LIB}")
+    build_runner(verbose)
     return LIB
+
+
+# the reference's `mlsqr run | compare` harness on the device path (runner/mlsqr_b200_run.cpp);
+# JSON via nlohmann/json 3.11.3 -- the library the reference's config.cpp uses, header-only
+RUNNER_SRC = os.path.join(HERE, "runner", "mlsqr_b200_run.cpp")
+RUNNER = os.path.join(HERE, "mlsqr-b200")
+JSON_DIRS = [os.environ.get("MLSQR_JSON_INCLUDE", ""),
+             "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann",
+             "/usr/include/nlohmann"]
+
+
+def build_runner(verbose: bool = True) -> str:
+    inc = next((d for d in JSON_DIRS if d and os.path.exists(os.path.join(d, "json.hpp"))), None)
+    if inc is None:
+        raise RuntimeError("nlohmann/json.hpp not found (set MLSQR_JSON_INCLUDE)")
+    deps = [RUNNER_SRC, LIB, os.path.join(HERE, "..", "include", "mlsqr_b200.h")]
+    if not _newer(RUNNER, deps):
+        return RUNNER
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-ffp-contract=off", "-I", inc, RUNNER_SRC, "-o", RUNNER,
+           "-L", HERE, "-lmlsqr_b200", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"runner build failed\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(f"  built {RUNNER}")
+    return RUNNER
 
 
 if __name__ == "__main__":

@@ -729,8 +729,8 @@ RunSummary run_experiment(const ExperimentConfig& cfg, const fs::path& out_overr
       stop_reason = "max_outer";
       for (int k = 1; k <= s.max_outer; ++k) {
         Pc m, owned;
-        const double eps = assemble_m(ctx, b, s, prev, s.epsilon, holder_levels, m);
-        eps_used.push_back(eps);
+        // (the reference's lagged branch leaves derived.epsilon_used empty, runner.cpp:186-201)
+        assemble_m(ctx, b, s, prev, s.epsilon, holder_levels, m);
         Solve r = run_krylov(b, spd_solver(s, m, owned), s.tau, inner, snaps, false);
         const double pv = penalty_R(ctx, b, s, r.f.data());
         history.push_back(pv);
