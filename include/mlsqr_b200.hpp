@@ -37,6 +37,10 @@ inline void check(int status, int breakdown_iteration = 0) {
 #ifdef MLSQR_B200_WITH_REFERENCE_API
   if (status == MLSQR_EDIM) throw mlsqr::DimensionError(msg);
   if (status == MLSQR_EBREAKDOWN) throw mlsqr::BreakdownError(msg, breakdown_iteration);
+  if (status == MLSQR_EFACTOR) {  // "... nonpositive pivot at row N" (spdsolve.cpp:66-70)
+    const auto sp = msg.find_last_of(' ');
+    throw mlsqr::FactorizationError(msg, sp == std::string::npos ? 0 : std::stoul(msg.substr(sp + 1)));
+  }
 #else
   (void)breakdown_iteration;
   if (status == MLSQR_EDIM) throw std::invalid_argument(msg);
