@@ -95,7 +95,9 @@ def test_operator_dimension_errors(ctx):
     with pytest.raises(mb.DimensionError):
         g.apply_adjoint(np.zeros(257))
     with pytest.raises(ValueError):
-        mb.SeparableGaussianBlur((16, 16), taps=np.ones(2 * 40 + 1))  # radius > 36
+        mb.SeparableGaussianBlur((16, 16), taps=np.ones(2 * 513 + 1))  # 1D/2D radius > 512
+    with pytest.raises(ValueError):
+        mb.SeparableGaussianBlur((16, 16, 16), taps=np.ones(2 * 40 + 1))  # 3D radius > 36
 
 
 @pytest.mark.parametrize("m,n,L", [(17, 23, 0), (40, 30, 0), (64, 512, 8), (96, 4096, 16), (8, 100000, 0)])
