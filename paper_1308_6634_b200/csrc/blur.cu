@@ -145,6 +145,17 @@ __global__ void blur_pass_kernel(const double* __restrict__ in, double* __restri
 }
 
 #include "blur3d_pipe.cuh"
+#include "blur3d_mma.cuh"
+
+// x / y passes on the FP64 tensor cores (blur3d_mma.cuh) for the BASELINE radii; bit-identical
+// to blur3d_pipe.  MLSQR_BLUR_MMA=0 selects the all-DFMA kernel (A/B measurements).
+static bool blur_mma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MLSQR_BLUR_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 // radius dispatch for the fused kernel (BASELINE taps: 9 (R=4) and 13 (R=6))
 static bool fused3d(Ctx* c, int R, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
                     const EpiArgs& a) {
@@ -152,9 +163,13 @@ static bool fused3d(Ctx* c, int R, const double* in, double* out, int nx, int ny
     case 1: launch_b3<1>(c, in, out, nx, ny, nz, t, a); return true;
     case 2: launch_b3<2>(c, in, out, nx, ny, nz, t, a); return true;
     case 3: launch_b3<3>(c, in, out, nx, ny, nz, t, a); return true;
-    case 4: launch_b3<4>(c, in, out, nx, ny, nz, t, a); return true;
+    case 4:
+      if (!(blur_mma_enabled() && launch_b3m<4>(c, in, out, nx, ny, nz, t, a))) launch_b3<4>(c, in, out, nx, ny, nz, t, a);
+      return true;
     case 5: launch_b3<5>(c, in, out, nx, ny, nz, t, a); return true;
-    case 6: launch_b3<6>(c, in, out, nx, ny, nz, t, a); return true;
+    case 6:
+      if (!(blur_mma_enabled() && launch_b3m<6>(c, in, out, nx, ny, nz, t, a))) launch_b3<6>(c, in, out, nx, ny, nz, t, a);
+      return true;
     case 8: launch_b3<8>(c, in, out, nx, ny, nz, t, a); return true;
     case 12: launch_b3<12>(c, in, out, nx, ny, nz, t, a); return true;
     default: return false;

@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__
         const int p = pb + u;
         if (p <= zhi + 1) {  // block-uniform
           // plane p+1 (x-pass input of this phase, old plane of the next) has landed
-          if (TMA) {
-            if (p + 1 <= zhi) mbar_wait(bars + stage(p + 1), parity(p + 1));
+          if (TMA) {  // one warp polls the TMA barrier; the CTA barrier publishes the plane
+            if (tid < 32 && p + 1 <= zhi) mbar_wait(bars + stage(p + 1), parity(p + 1));
           } else {
             cp_async_wait<1>();
           }
