@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
     const int bx = t % tiles_x;
     const int x0 = bx * C::TX, y0 = (t / tiles_x) * C::TY;
     const int zlo = z0 - R, zhi = z1 + R - 1;
-    auto inside = [&](int zz) { return zz >= zlo && zz <= zhi && zz + zoff >= 0 && zz + zoff < nzg; };
+    const int zin_lo = max(zlo, -zoff), zin_hi = min(zhi, nzg - 1 - zoff);  // in the segment and the grid
+    auto inside = [&](int zz) { return zz >= zin_lo && zz <= zin_hi; };
     auto stage = [&](int zz) { return (qbase + (unsigned)(zz - zlo)) & (C::NSTAGE - 1); };
     auto parity = [&](int zz) { return ((qbase + (unsigned)(zz - zlo)) >> 2) & 1u; };
     auto issue = [&](int zz) {
@@ -157,11 +158,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
                 const double* arow = tile + 32 * k * C::P;
                 double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                for (int q = 0; q < C::KS; ++q) {
-                  double a = arow[4 * q];
-                  if (e.sx) a = a * sx;
-                  dmma8844(d0, d1, a, tq[q]);
-                }
+                for (int q = 0; q < C::KS; ++q) dmma8844(d0, d1, arow[4 * q] * sx, tq[q]);  // x * 1.0 == x
                 if (k == 0 || xrow1_ok)
                   *reinterpret_cast<double2*>(xw + 32 * k * C::XP) = make_double2(d0, d1);
               }
