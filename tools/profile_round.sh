@@ -21,7 +21,7 @@ cap() {  # name regex skip
     -k "regex:$2" -s $3 -c 1 -o $O/${TAG}_full_$1 python profiles/kernel_driver.py --reps 2 --iters 2 \
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
-cap blur 'blur3d_pipe' 5
+cap blur 'blur3d_(mma|pipe)' 5
 cap sweep_fn 'sweep_fn_kernel' 5
 cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2>' 3
 cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1>' 5
