@@ -23,7 +23,7 @@ cap() {  # name regex skip
 }
 cap blur 'blur3d_(mma|pipe)' 5
 cap sweep_fn 'sweep_fn_kernel' 5
-cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2>' 3
-cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1>' 5
+cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2' 3
+cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1' 5
 cap restrict 'restrict_zm_kernel' 4
 cap update 'update_kernel' 0
