@@ -22,7 +22,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmlsqr_b200.so")
+LIB_PATH = os.environ.get("MLSQR_LIB_PATH") or os.path.join(HERE, "libmlsqr_b200.so")  # override: A/B builds
 
 __all__ = [
     "DimensionError", "BreakdownError", "CudaError", "Context", "default_context",

@@ -17,11 +17,11 @@
 // 0 here where the unfused kernel read some finite in-domain value -- either way
 // it meets an exactly-zero boundary coefficient and acc + (+-0) == acc.
 namespace fn {
-constexpr int TX = 32, TY = 8;
+constexpr int TX = 32, TY = 16;
 constexpr int ROWS = TY + 2, COLS = TX + 2;
 constexpr int WARPS = ROWS + 1;  // rows y0-1 .. y0+TY, then the x-halo warp
 constexpr int THREADS = 32 * WARPS;
-constexpr int MINB = 2;  // resident blocks per SM (80 registers)
+constexpr int MINB = 1;  // resident blocks per SM (19 warps, 92 registers)
 }  // namespace fn
 
 constexpr int kFnL2Ahead = 2;  // L2 prefetch distance beyond the register prefetch (planes)
