@@ -751,3 +751,72 @@ def test_nonlinear_reference_spd_modes(ctx, dev, golden, spd_mode, pen, T):
         # order (above) and oracle reference order == reference (test_oracle_golden.py)
         floor = rel(golden[f"avx2_outer_{pen}_f"], golden[pre + "_f"])
         assert rel(rep.solution, golden[pre + "_f"]) <= max(TOL_F, 25 * floor)
+
+
+# ---------------------------------------------------------------------------
+# the reference's own SpdSolver / outer-loop property tests, mirrored on the device maps
+# ---------------------------------------------------------------------------
+def _phantom1d(n):  # Phantom1D::default_phantom realized at cell centres (problems.cpp:31-79)
+    jumps = [(0.00, 0.0), (0.10, 1.0), (0.28, 0.0), (0.40, 1.5), (0.62, 0.2), (0.76, 2.0), (0.80, 0.2), (0.90, 0.0)]
+    x = (np.arange(n) + 0.5) / n
+    return np.array([[lev for pos, lev in jumps if pos <= xi][-1] for xi in x])
+
+
+def _deconv1d(n, sigma_f, sigma_n, seed):  # make_deconv1d (problems.cpp:135-158)
+    a = mb.SeparableGaussianBlur((n,), sigma_f=sigma_f)
+    ft = _phantom1d(n)
+    g = a.apply(ft) + mb.gaussian_noise(seed, n, sigma_n)
+    return a, ft, g
+
+
+def test_spd_solver_maps_are_symmetric(ctx):
+    """test_spdsolve.cpp:149-168: both modes are symmetric maps (inner CG at full count)."""
+    rng = np.random.default_rng(6)
+    n = 14
+    m = mb.VCycleMap((n,), 1.0 / n, 1)
+    cx = rng.uniform(0.5, 2.0, n)
+    cx[-1] = 0.0
+    m.set_coefficients(cx, eps=2.0)
+    for s in (mb.CholeskyMap(m), mb.InnerCgMap(m, n)):
+        p, q = rng.standard_normal(n), rng.standard_normal(n)
+        sp, sq = s.solve(p), s.solve(q)
+        assert abs(sp @ q - p @ sq) <= 1e-12 * np.abs(sp * q).sum()
+
+
+def test_truncated_inner_cg_deterministic_and_monotone(ctx):
+    """test_spdsolve.cpp:170-189: bitwise repeatable, Euclidean error monotone in k."""
+    n = 64
+    m = mb.VCycleMap((n,), 1.0, 1)  # shifted Neumann Laplacian: unit edges + 1e-6 I
+    cx = np.ones(n)
+    cx[-1] = 0.0
+    m.set_coefficients(cx, eps=1e-6)
+    p = np.random.default_rng(7).standard_normal(n)
+    exact = mb.CholeskyMap(m).solve(p)
+    prev = np.linalg.norm(exact)
+    for k in (1, 2, 4, 8, 16, 32, 64):
+        cg = mb.InnerCgMap(m, k)
+        v1, v2 = cg.solve(p), cg.solve(p)
+        assert np.array_equal(v1, v2)
+        e = np.linalg.norm(v1 - exact)
+        assert e <= prev * (1.0 + 1e-10), k
+        prev = e
+    with pytest.raises(mb.DimensionError):
+        mb.CholeskyMap(m).solve(np.ones(3))
+
+
+def test_outer_inner_cg_matches_direct_and_is_deterministic(ctx):
+    """test_outer.cpp:134-163: reports are deterministic; with a heavy shift (kappa(M) ~ 4) the
+    inner-CG mode reaches the direct solution to 1e-6."""
+    n = 80
+    a, ft, g = _deconv1d(n, 0.05, 0.01, 6)
+    delta = 0.01 / np.sqrt(1.0 / n)
+    base = dict(tau=0.0, penalty=mb.PenaltySpec.perona_malik_log(0.005),
+                inner_stop=mb.StoppingConfig.discrepancy(delta, 1.1, 1000), inner_cap=20,
+                rel_decrease_threshold=0.15, max_outer=25, epsilon=50.0)
+    cg = mb.solve_nonlinear(a, g, (n,), 1.0 / n, mb.OuterConfig(spd_mode="inner_cg", k_inner=80, **base))
+    direct = mb.solve_nonlinear(a, g, (n,), 1.0 / n, mb.OuterConfig(spd_mode="cholesky", **base))
+    assert cg.steps and rel(cg.solution, direct.solution) <= 1e-6
+    again = mb.solve_nonlinear(a, g, (n,), 1.0 / n, mb.OuterConfig(spd_mode="cholesky", **base))
+    assert np.array_equal(again.solution, direct.solution)
+    assert [s.penalty_value for s in again.steps] == [s.penalty_value for s in direct.steps]
+    assert [s.inner_iterations for s in again.steps] == [s.inner_iterations for s in direct.steps]
