@@ -163,6 +163,9 @@ class Pc {
   virtual ~Pc() = default;
   Ctx* ctx = nullptr;
   size_t n = 0;
+  // (z-sharded) the caller's input p carries at least one writable guard plane per side, so the
+  // map may fill ghost planes of p in place (the Krylov workspace's guarded p does)
+  bool in_guarded = false;
   // v = B p on the device; seg (optional) <- segment partials of v*p laid out over
   // `shape` (the operator's solution space); gate as in Epi
   virtual void solve(const double* p, double* v, double* seg, const int* gate, RowShape shape) = 0;

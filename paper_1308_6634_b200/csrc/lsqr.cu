@@ -481,7 +481,9 @@ struct Runner {
 
   void precond(const int* gate) {
     if (pc) {
+      pc->in_guarded = ws->guard > 0;
       pc->solve(ws->p.p, ws->v.p, ws->seg_vp.p, gate, ws->sol);
+      pc->in_guarded = false;
     } else {
       seg_dot(c, ws->p.p, ws->p.p, ws->sol, ws->seg_vp.p, gate);
     }

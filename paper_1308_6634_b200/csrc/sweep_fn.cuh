@@ -12,6 +12,9 @@
 // L1/L2 hits, cz[i-nxy] stays in a register), so level-0 traffic drops from
 // 5 + 6 words per voxel (two sweeps) to 4 + 1.
 //
+// z slabs: planes -1 and nz are ghost planes (b, cx, cy, cz exchanged; cz two planes below), so
+// x1 on them is computed here too; `on` admits a plane iff it lies in the global grid.
+//
 // Bit-exactness: D and both row sums are formed in exactly the order of
 // sweep_zm_kernel (diag_at / m_row, sparse.cpp:65-74).  x1 outside the domain is
 // 0 here where the unfused kernel read some finite in-domain value -- either way
@@ -59,7 +62,7 @@ __device__ __forceinline__ double fn_diag(const FnPlane& s, double czm, double e
 __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, const double* __restrict__ b,
                                                                   double* __restrict__ out, double omega,
                                                                   double* __restrict__ seg, const int* gate,
-                                                                  int zc) {
+                                                                  int zc, int zoff, int nzg) {
   using namespace fn;
   if (gate && *gate == 0) return;
   __shared__ double ring[3][ROWS][COLS];
@@ -92,7 +95,8 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
   const long chunks = (nx + 31) / 32;
   const long col = inxy ? (long)py * nx + px : 0;
   auto idx = [&](int z) { return (long)z * nxy + col; };
-  auto on = [&](int z) { return inxy && z >= 0 && z < nz; };
+  // a plane exists if it is in the global grid and local or one of the two ghost planes
+  auto on = [&](int z) { return inxy && z >= -1 && z <= nz && z + zoff >= 0 && z + zoff < nzg; };
   auto first = [&](const FnPlane& s, double d, bool in) { return in ? 0.0 + (omega * (s.b - 0.0)) / d : 0.0; };
 
   // prologue: plane z0-1 (own column only), plane z0 (published), plane z0+1 (loaded)

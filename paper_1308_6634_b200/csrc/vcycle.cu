@@ -275,8 +275,7 @@ class VCycle final : public Pc {
   struct Level {
     int nx, ny, nz;
     size_t n;
-    GBuf cx, cy, cz, xa, xb;
-    DevBuf<double> b;
+    GBuf cx, cy, cz, xa, xb, b;
   };
 
   VCycle(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, double h, int levels, int nu_pre,
@@ -304,12 +303,15 @@ class VCycle final : public Pc {
       L.n = (size_t)L.nx * L.ny * L.nz;
       // guard: one plane + 64 (x[i +- nxy], and the prefetch of plane z+2 = nz)
       const size_t g = (size_t)L.nx * L.ny + 64;
-      L.cx.alloc(L.n, g, c->stream);
-      if (dims >= 2) L.cy.alloc(L.n, g, c->stream);
-      if (dims >= 3) L.cz.alloc(L.n, g, c->stream);
+      // coefficients: two guard planes -- the fused first sweeps on a slab form D on ghost plane -1
+      // (cz one plane further down, cy one row up: cy[i - nx] of row 0)
+      const size_t gc = g + (size_t)L.nx * L.ny;
+      L.cx.alloc(L.n, gc, c->stream);
+      if (dims >= 2) L.cy.alloc(L.n, gc, c->stream);
+      if (dims >= 3) L.cz.alloc(L.n, gc, c->stream);
       L.xa.alloc(L.n, g, c->stream);
       L.xb.alloc(L.n, g, c->stream);
-      if (l > 0) L.b.alloc(L.n);
+      if (l > 0) L.b.alloc(L.n, g, c->stream);  // guarded: ghost planes of the restricted rhs
     }
     if (c->sharded()) {
       // z slabs: every level's local planes must stay even-aligned with the global grid
@@ -362,10 +364,18 @@ class VCycle final : public Pc {
           dims_ >= 2 ? C.cy.p : nullptr, dims_ >= 3 ? C.cz.p : nullptr);
       ctx->count();
     }
-    // the sweeps read cz[z-1] of the plane below a slab: fill its ghost on every level
+    // the sweeps read cz[z-1] of the plane below a slab; the fused first sweeps also form D on
+    // the ghost planes -1 and nz (cx, cy there, cz two planes below): fill those ghosts on every level
     if (ctx->sharded() && dims_ >= 3)
-      for (size_t l = 0; l < lv_.size(); ++l)
-        halo_planes(ctx, lv_[l].cz.p, (size_t)lv_[l].nx * lv_[l].ny, lv_[l].nz, 1);
+      for (size_t l = 0; l < lv_.size(); ++l) {
+        const Level& L = lv_[l];
+        const size_t pl = (size_t)L.nx * L.ny;
+        halo_planes(ctx, L.cz.p, pl, L.nz, L.nz >= 2 ? 2 : 1);
+        if (L.nz >= 2) {
+          halo_planes(ctx, L.cx.p, pl, L.nz, 1);
+          halo_planes(ctx, L.cy.p, pl, L.nz, 1);
+        }
+      }
     ctx->check_launch();
   }
 
@@ -501,6 +511,7 @@ class VCycle final : public Pc {
       double* dst = (last_here && out) ? out : bufs[nb];
       double* sg = (last_here && out) ? seg : nullptr;
       if (fpair) {
+        if (ctx->sharded()) hx(l, b);  // x1 on the ghost planes needs b there
         sweep_fn(l, b, dst, sg, gate);
         ++s;
       } else if (s == 0) {
@@ -540,8 +551,14 @@ class VCycle final : public Pc {
     return cur;
   }
 
-  // first + second pre-sweep in one kernel (3D, unsharded: x1 halos are computed, not exchanged)
-  bool fn_ok(int) const { return fn_enabled_ && dims_ == 3 && !ctx->sharded(); }
+  // first + second pre-sweep in one kernel (3D): x1 halos are computed, not exchanged.  On a z
+  // slab the kernel also computes x1 on the two ghost planes, from ghost planes of b (level 0:
+  // only when the caller's p is guarded) and of the coefficients
+  bool fn_ok(int l) const {
+    if (!fn_enabled_ || dims_ != 3) return false;
+    if (!ctx->sharded()) return true;
+    return lv_[(size_t)l].nz >= 2 && (l > 0 || in_guarded);
+  }
 
   void sweep_fn(int l, const double* b, double* out, double* seg, const int* gate) {
     const Level& L = lv_[(size_t)l];
@@ -549,7 +566,8 @@ class VCycle final : public Pc {
     const int zc = fn_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + fn::TX - 1) / fn::TX), (unsigned)((L.ny + fn::TY - 1) / fn::TY),
              (unsigned)((L.nz + zc - 1) / zc));
-    sweep_fn_kernel<<<grd, dim3(32, fn::WARPS), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate, zc);
+    sweep_fn_kernel<<<grd, dim3(32, fn::WARPS), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate, zc, zoff_l(l),
+                                                                   nzg_l(l));
     ctx->count();
   }
 
