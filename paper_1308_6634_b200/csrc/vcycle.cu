@@ -232,6 +232,15 @@ __global__ void set_eps_kernel(const unsigned long long* __restrict__ maxd, doub
   }
 }
 
+// the eps chain of an agglomerated coarse hierarchy continues the fine one's: eps_l = e * 2^(d l)
+__global__ void set_eps_from_kernel(const double* __restrict__ e0, double mult, int levels, double* __restrict__ eps) {
+  double e = *e0;
+  for (int l = 0; l < levels; ++l) {
+    eps[l] = e;
+    e = e * mult;
+  }
+}
+
 // R(f): per-node sum of its x/y/z edge terms, canonical segment partials
 __global__ void penalty_kernel(const double* __restrict__ f, int nx, int ny, int nz, int dims,
                                int kind, double T, double h, double w, int zoff, int nzg,
@@ -324,6 +333,42 @@ class VCycle final : public Pc {
     maxd_.alloc(1);
     if (const char* e = getenv("MLSQR_FN_SWEEPS")) fn_enabled_ = e[0] != '0';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
+    if (c->sharded()) setup_agglomeration(nu_pre, nu_post, omega, kc);
+  }
+
+  ~VCycle() override {
+    delete coarse_;
+    delete cctx_;
+  }
+
+  // Coarse-level agglomeration: from the first level whose slab holds at most
+  // kAggPlanes planes, every rank runs the rest of the V-cycle redundantly on the whole coarse
+  // grid (an unsharded hierarchy on a private unsharded context) instead of exchanging ghost
+  // planes on every coarse sweep: one allgather of the restricted rhs per V-cycle replaces ~4
+  // latency-bound exchanges per coarse level.  Per element the arithmetic is the slab path's, so
+  // results stay bit-identical.  MLSQR_AGG_PLANES overrides the threshold (0 disables).
+  void setup_agglomeration(int nu_pre, int nu_post, double omega, int kc) {
+    int planes = kAggPlanes;
+    if (const char* e = getenv("MLSQR_AGG_PLANES")) planes = atoi(e);
+    const int P = ctx->comm->size;
+    for (int l = 1; l < (int)lv_.size() && planes > 0; ++l) {
+      const Level& L = lv_[(size_t)l];
+      if (L.nz > planes) continue;
+      if ((long)L.nz * P != nzg_l(l)) return;  // unequal slabs: stay sharded
+      la_ = l;
+      break;
+    }
+    if (la_ <= 0) return;
+    cctx_ = new Ctx();
+    cctx_->device = ctx->device;
+    cctx_->stream = ctx->stream;
+    cctx_->sm_count = ctx->sm_count;
+    cctx_->l2_bytes = ctx->l2_bytes;
+    const Level& A = lv_[(size_t)la_];
+    coarse_ = new VCycle(cctx_, dims_, (size_t)A.nx, (size_t)A.ny, (size_t)nzg_l(la_), h_ * (double)(1 << la_),
+                         (int)lv_.size() - la_, nu_pre, nu_post, omega, kc);
+    coarse_->fn_enabled_ = fn_enabled_;
+    cb_.alloc(coarse_->n);
   }
 
   Lvl view(int l) const {
@@ -357,6 +402,25 @@ class VCycle final : public Pc {
     if (ctx->sharded()) ctx->comm->allreduce_max_u64(maxd_.p, ctx->stream);  // order-free max
     set_eps_kernel<<<1, 1, 0, ctx->stream>>>(maxd_.p, eps_cfg, mult(), (int)lv_.size(), eps_.p);
     ctx->count();
+    coarsen_all();
+    if (coarse_) {
+      // the whole level-la_ operator on every rank: gather the slabs' coefficients (slabs are
+      // contiguous z ranges in rank order), continue the eps chain, coarsen from there
+      const Level& A = lv_[(size_t)la_];
+      VCycle::Level& C0 = coarse_->lv_[0];
+      ctx->comm->allgather(A.cx.p, A.n, C0.cx.p, ctx->stream);
+      ctx->comm->allgather(A.cy.p, A.n, C0.cy.p, ctx->stream);
+      ctx->comm->allgather(A.cz.p, A.n, C0.cz.p, ctx->stream);
+      set_eps_from_kernel<<<1, 1, 0, ctx->stream>>>(eps_.p + la_, mult(), (int)coarse_->lv_.size(), coarse_->eps_.p);
+      ctx->count();
+      coarse_->coarsen_all();
+      ctx->count((int)cctx_->launches);
+      cctx_->launches = 0;
+    }
+    ctx->check_launch();
+  }
+
+  void coarsen_all() {
     for (size_t l = 1; l < lv_.size(); ++l) {
       Level& C = lv_[l];
       coarsen_kernel<<<row_grid(C.nx, C.ny * C.nz), dim3(32, 8), 0, ctx->stream>>>(
@@ -527,7 +591,8 @@ class VCycle final : public Pc {
     Level& C = lv_[(size_t)l + 1];
     hx(l, cur);
     restrict_to(l, cur, b, gate);
-    const double* xc = level(l + 1, C.b.p, nullptr, nullptr, gate);
+    const bool agg = coarse_ && l + 1 == la_;
+    const double* xc = agg ? coarse_solve(C.b.p, gate) : level(l + 1, C.b.p, nullptr, nullptr, gate);
     if (nu_post_ == 0) {
       double* dst = out ? out : bufs[nb];
       sweep<kProlongOnly>(l, cur, xc, b, dst, out ? seg : nullptr, gate);
@@ -539,7 +604,7 @@ class VCycle final : public Pc {
       double* sg = (last && out) ? seg : nullptr;
       if (s == 0) {
         hx(l, cur);
-        hx(l + 1, xc);
+        if (!agg) hx(l + 1, xc);  // an agglomerated correction is whole: its neighbour planes are real
         sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
       } else {
         hx(l, cur);
@@ -584,6 +649,23 @@ class VCycle final : public Pc {
   DevBuf<double> eps_;
   DevBuf<unsigned long long> maxd_;
   GBuf fg_;  // guarded copy of the field for K_D (z-sharded)
+  // coarse-level agglomeration (z-sharded): levels >= la_ run whole on every rank
+  static constexpr int kAggPlanes = 8;
+  int la_ = 0;
+  VCycle* coarse_ = nullptr;
+  Ctx* cctx_ = nullptr;
+  DevBuf<double> cb_;
+
+  // the agglomerated coarse levels: gather this level's rhs slabs, run the rest of the V-cycle
+  // on the whole coarse grid, return this rank's slab of the (guarded, whole) coarse correction
+  const double* coarse_solve(const double* b_local, const int* gate) {
+    const Level& A = lv_[(size_t)la_];
+    ctx->comm->allgather(b_local, A.n, cb_.p, ctx->stream);
+    const double* xfull = coarse_->level(0, cb_.p, nullptr, nullptr, gate);
+    ctx->count((int)cctx_->launches);  // the coarse kernels are this library's launches too
+    cctx_->launches = 0;
+    return xfull + (size_t)zoff_l(la_) * A.nx * A.ny;
+  }
 
   // fill the one-plane ghosts of a level-l iterate (z-sharded)
   void hx(int l, const double* v) {

@@ -299,3 +299,32 @@ def test_outer_solver_steps_sharded_bit_exact(problem, P):
     for k in range(3):
         assert all(o[k][:3] == ref[k][:3] for o in out)
         assert np.array_equal(np.concatenate([o[k][3] for o in out]), ref[k][3])
+
+
+@pytest.mark.parametrize("agg_planes", ["0", "4", "8", "16", "32"])
+def test_coarse_agglomeration_bit_exact(problem, monkeypatch, agg_planes):
+    """Coarse-level agglomeration: from the first level whose slab holds at most
+    MLSQR_AGG_PLANES planes, every rank solves the remaining levels on the whole coarse grid
+    (one allgather of the restricted rhs per V-cycle instead of ghost exchanges on every coarse
+    sweep).  Every threshold -- none, late, early, from level 1 -- is bit-identical to one GPU."""
+    monkeypatch.setenv("MLSQR_AGG_PLANES", agg_planes)
+    shape, taps, f, g = problem
+    nx, ny, nz = shape
+    h = 1.0 / nx
+    pen = mb.PenaltySpec.tv_smoothed(0.01)
+    st = mb.StoppingConfig.max_iterations(8)
+    vc = mb.VCycleMap(shape, h, 4)
+    vc.update(f, pen)
+    ref = mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), vc, g, 5e-3, st)
+
+    for P in (2, 4):
+        def fn(r, ctx, sl):
+            loc = (nx, ny, sl.stop - sl.start)
+            m = mb.VCycleMap(loc, h, 4, ctx=ctx)
+            m.update(planes(f, shape)[sl].ravel(), pen)
+            o = mb.SeparableGaussianBlur(loc, taps=taps, ctx=ctx)
+            return mb.mlsqr(o, m, planes(g, shape)[sl].ravel(), 5e-3, st)
+
+        out = run_ranks(P, nz, fn)
+        assert all(np.array_equal(o.alphas, ref.alphas) for o in out), (P, agg_planes)
+        assert np.array_equal(np.concatenate([o.solution for o in out]), ref.solution), (P, agg_planes)
