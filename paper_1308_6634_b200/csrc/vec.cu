@@ -78,12 +78,41 @@ __global__ void __launch_bounds__(1024) reduce3_kernel(const double* __restrict_
   if (threadIdx.x == 0) out[blockIdx.x] = r;
 }
 
+// Two tree-32 levels per warp: warp k reduces in[1024k .. 1024k + 1023] (zero padded past J) --
+// lane l forms level 1 of group 32k + l serially, the warp's shuffle tree level 2 -- into out[k].
+// Whole canonical levels in any grouping give the same bits, so a reduction can take two levels
+// per pass with one warp per 1024 values instead of three per pass with one 1024-thread block per
+// 32768 (which leaves all but a few SMs idle on small vectors).
+__global__ void __launch_bounds__(256) reduce2_kernel(const double* __restrict__ in, size_t J, size_t K,
+                                                      double* __restrict__ out, const int* gate) {
+  if (gate && *gate == 0) return;
+  const size_t k = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (k >= K) return;  // whole warp
+  const int lane = threadIdx.x & 31;
+  const size_t base = k * 1024 + (size_t)lane * 32;
+  double v[32];
+  if (base + 32 <= J && !(reinterpret_cast<uintptr_t>(in + base) & 15)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double2 q = *reinterpret_cast<const double2*>(in + base + 2 * j);
+      v[2 * j] = q.x;
+      v[2 * j + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = base + j < J ? in[base + j] : 0.0;
+  }
+  const double r = tree32(tree32_serial(v));
+  if (lane == 0) out[k] = r;
+}
+
 size_t reduce_scratch_size(size_t nseg) {
   size_t tot = 0;
-  while (nseg > 32768) {
-    nseg = (nseg + 32767) / 32768;
+  while (nseg > 1024) {
+    nseg = (nseg + 1023) / 1024;
     tot += nseg;
   }
+  // (covers the block-aligned distributed path's nseg / 32768 level-3 partials too)
   return tot + 1;
 }
 
@@ -92,18 +121,17 @@ void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, do
   const double* cur = seg;
   size_t J = nseg;
   double* s = scratch;
-  while (J > 32768) {
-    const size_t K = (J + 32767) / 32768;
-    reduce3_kernel<<<(unsigned)K, 1024, 0, c->stream>>>(cur, J, s, gate);
+  for (;;) {
+    const size_t K = (J + 1023) / 1024;
+    double* dst = K == 1 ? out : s;
+    reduce2_kernel<<<(unsigned)((K + 7) / 8), 256, 0, c->stream>>>(cur, J, K, dst, gate);
     c->count();
     c->check_launch();
+    if (K == 1) break;
     cur = s;
     s += K;
     J = K;
   }
-  reduce3_kernel<<<1, 1024, 0, c->stream>>>(cur, J, out, gate);
-  c->count();
-  c->check_launch();
 }
 
 // ---------------------------------------------------------------------------

@@ -44,19 +44,27 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Three tree-32 levels over in[0 .. 32768) (zero padded past J); result in thread 0.
-// Requires blockDim.x == 1024.
+// Requires blockDim.x == 1024.  Thread t forms level 1 of group t (in[32t .. 32t+31]) with the
+// serial emulation of tree32 (32 independent loads, 31 adds with ILP 16/8/4/2/1), the warp's
+// shuffle tree forms level 2 over its 32 consecutive groups, warp 0 level 3 -- the canonical
+// order, without the 32 dependent shuffle chains per warp of a warp-per-group level 1.
 __device__ __forceinline__ double block_reduce3(const double* __restrict__ in, size_t J) {
   __shared__ double wres[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double keep = 0.0;
-#pragma unroll 4
-  for (int g = 0; g < 32; ++g) {
-    const size_t k = (size_t)w * 1024 + (size_t)g * 32 + (size_t)lane;
-    double v = k < J ? in[k] : 0.0;
-    v = tree32(v);
-    v = __shfl_sync(kFull, v, 0);
-    if (lane == g) keep = v;
+  const size_t base = (size_t)threadIdx.x * 32;
+  double v[32];
+  if (base + 32 <= J && !(reinterpret_cast<uintptr_t>(in + base) & 15)) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double2 q = *reinterpret_cast<const double2*>(in + base + 2 * k);
+      v[2 * k] = q.x;
+      v[2 * k + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = base + k < J ? in[base + k] : 0.0;
   }
+  double keep = tree32_serial(v);
   keep = tree32(keep);
   if (lane == 0) wres[w] = keep;
   __syncthreads();
