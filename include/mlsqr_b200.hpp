@@ -109,6 +109,19 @@ class GpuSpdMap final : public mlsqr::SpdMap {
     check(mlsqr_vcycle_create(c.get(), dims, nx, ny, nz, h, levels, nu_pre, nu_post, omega, coarse_sweeps, &pc));
     return GpuSpdMap(pc);
   }
+  // SpdSolver::factorize of the M a V-cycle map holds (spdsolve.cpp:22-75), on the device;
+  // throws mlsqr::FactorizationError(pivot_row) like the reference
+  static GpuSpdMap cholesky(const GpuSpdMap& m) {
+    mlsqr_pc* pc = nullptr;
+    check(mlsqr_chol_map_create(m.handle(), &pc, nullptr));
+    return GpuSpdMap(pc);
+  }
+  // SpdSolver::inner_cg (spdsolve.cpp:77-85): k_inner CG iterations on a snapshot of m's M
+  static GpuSpdMap inner_cg(const GpuSpdMap& m, int k_inner) {
+    mlsqr_pc* pc = nullptr;
+    check(mlsqr_inner_cg_map_create(m.handle(), k_inner, &pc));
+    return GpuSpdMap(pc);
+  }
   GpuSpdMap(GpuSpdMap&& o) noexcept : pc_(o.pc_) { o.pc_ = nullptr; }
   ~GpuSpdMap() override { mlsqr_pc_destroy(pc_); }
   using SpdMap::solve;
@@ -163,8 +176,9 @@ inline void fill_trace(mlsqr::SolveResult& r, const std::vector<mlsqr_iter_rec>&
 }
 }  // namespace detail
 
-// Device-resident mlsqr with the reference's signature semantics (krylov.hpp:94-95);
-// opts.store_basis also returns the right basis (SolveOptions, krylov.hpp:77-79).
+// Device-resident mlsqr with the reference's signature semantics (krylov.hpp:94-95) and its
+// SolveOptions (krylov.hpp:77-80): store_basis returns the right and left bases, record_snapshots
+// the iterate after every iteration (SolveTrace::snapshots).
 inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap& m,
                                     std::span<const double> g, double tau,
                                     const mlsqr::StoppingConfig& stop, const mlsqr::SolveOptions& opts = {}) {
@@ -175,20 +189,27 @@ inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap&
   const std::size_t n = a.n_cols(), k = static_cast<std::size_t>(stop.max_iters);
   r.solution.assign(n, 0.0);
   std::vector<mlsqr_iter_rec> tr(k);
-  std::vector<double> al(k + 1), be(k + 2), basis, left;
+  std::vector<double> al(k + 1), be(k + 2), basis, left, snaps;
   mlsqr_solve_info info{};
+  mlsqr_solve_opts o{};
   if (opts.store_basis) {
     basis.assign((k + 1) * n, 0.0);
     left.assign((k + 1) * a.n_rows(), 0.0);
-    check(mlsqr_solve_basis(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
-                            be.data(), basis.data(), left.data(), &info, MLSQR_HOST),
-          info.breakdown_iteration);
-  } else {
-    check(mlsqr_solve(a.handle(), m.handle(), g.data(), tau, &s, r.solution.data(), tr.data(), al.data(),
-                      be.data(), &info, MLSQR_HOST),
-          info.breakdown_iteration);
+    o.store_basis = 1;
+    o.basis = basis.data();
+    o.left_basis = left.data();
   }
+  if (opts.record_snapshots) {
+    snaps.assign(k * n, 0.0);
+    o.record_snapshots = 1;
+    o.snapshots = snaps.data();
+  }
+  check(mlsqr_solve_with(a.handle(), m.handle(), g.data(), tau, &s, &o, r.solution.data(), tr.data(), al.data(),
+                         be.data(), &info, MLSQR_HOST),
+        info.breakdown_iteration);
   detail::fill_trace(r, tr, info);
+  for (int j = 0; opts.record_snapshots && j < info.iterations; ++j)
+    r.trace.snapshots.emplace_back(snaps.begin() + j * n, snaps.begin() + (j + 1) * n);
   r.bidiag.alphas.assign(al.begin(), al.begin() + info.n_alphas);
   r.bidiag.betas.assign(be.begin(), be.begin() + info.n_betas);
   for (int j = 0; opts.store_basis && j < info.n_alphas; ++j)

@@ -135,6 +135,44 @@ int main() {
     EXPECT(std::sqrt(n2 / d2) < 1e-9);
   }
 
+  // both seams on the B200 inside the UNMODIFIED reference loop: the GPU blur as A and the
+  // GPU envelope Cholesky (SpdSolver::factorize on the device) as M^-1 -- bit for bit the all-CPU
+  // reference (PM-log: no hypot in the diffusivity, so the device M is the reference's M exactly)
+  {
+    auto holder = mlsqr_b200::GpuSpdMap::vcycle(ctx, 2, nx, nx, 1, 1.0 / nx, 1);
+    holder.update(bundle.f_true, MLSQR_PEN_PM_LOG, 0.05, 1.0);
+    const auto gchol = mlsqr_b200::GpuSpdMap::cholesky(holder);
+    const SparseSpd mp = assemble_m(bundle.grid, bundle.f_true, PenaltySpec::perona_malik_log(0.05), 0.0).with_shift(1.0);
+    const SpdSolver cchol = SpdSolver::factorize(mp);
+    const auto r_ref = mlsqr::mlsqr(cpu_op, cchol, bundle.g, 1e-2, stop);
+    const auto r_both = mlsqr::mlsqr(gpu_op, gchol, bundle.g, 1e-2, stop);
+    std::printf("reference mlsqr, GPU blur + GPU Cholesky vs all-CPU: %s\n",
+                r_both.solution == r_ref.solution ? "bit-identical" : "DIFFERENT");
+    EXPECT(r_both.solution == r_ref.solution);
+    EXPECT(r_both.bidiag.alphas == r_ref.bidiag.alphas);
+    // the inner-CG mode runs too (canonical dots inside the map: rounding-level agreement)
+    const auto gcg = mlsqr_b200::GpuSpdMap::inner_cg(holder, 60);
+    const auto r_cg = mlsqr::mlsqr(gpu_op, gcg, bundle.g, 1e-2, StoppingConfig::max_iterations(5));
+    EXPECT(r_cg.iterations == 5);
+    // SolveOptions::record_snapshots through the device loop
+    SolveOptions rs;
+    rs.record_snapshots = true;
+    const auto r_snap = mlsqr_b200::gpu_mlsqr(gpu_op, vc, bundle.g, 1e-2, stop, rs);
+    EXPECT(r_snap.trace.snapshots.size() == static_cast<std::size_t>(r_snap.iterations));
+    EXPECT(!r_snap.trace.snapshots.empty() && r_snap.trace.snapshots.back() == r_snap.solution);
+    // FactorizationError crosses the boundary as the reference's exception
+    bool fthrew = false;
+    auto bad = mlsqr_b200::GpuSpdMap::vcycle(ctx, 1, 8, 1, 1, 1.0 / 8, 1);
+    try {
+      std::vector<double> negc(8, -1.0);
+      mlsqr_b200::check(mlsqr_vcycle_set_coefficients(bad.handle(), negc.data(), nullptr, nullptr, 0.0, MLSQR_HOST));
+      const auto never = mlsqr_b200::GpuSpdMap::cholesky(bad);
+    } catch (const FactorizationError& e) {
+      fthrew = e.pivot_row() == 0;
+    }
+    EXPECT(fthrew);
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
