@@ -52,10 +52,11 @@ struct B3M {
   static_assert(8 * 3 + 4 * KS <= H, "y-pass window inside the x results (even R)");
 };
 
+// (not volatile: a pure function of its operands, so independent chains may interleave)
 __device__ __forceinline__ void dmma8844(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 template <int R>
@@ -151,17 +152,23 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
           if (inside(xz)) {
             const double* tile = tin + stage(xz) * C::IN_SLOT + xa_off;
             double* xw = xs + ((xz - zlo) & 1) * C::XS_DOUBLES + xd_off;
+            // pairs warp and warp + 16 (row tile (warp >> 2) + 4, same column tile): two independent
+            // DMMA chains, interleaved; x * 1.0 == x when there is no scale
+            if (warp + 16 < C::XPAIRS) {  // warp-uniform
+              const double* arow1 = tile + 32 * C::P;
+              double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              if (k == 0 || warp + 16 < C::XPAIRS) {  // warp-uniform
-                // pair warp + 16k: row tile (warp >> 2) + 4k, column tile warp & 3
-                const double* arow = tile + 32 * k * C::P;
-                double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-                for (int q = 0; q < C::KS; ++q) dmma8844(d0, d1, arow[4 * q] * sx, tq[q]);  // x * 1.0 == x
-                if (k == 0 || xrow1_ok)
-                  *reinterpret_cast<double2*>(xw + 32 * k * C::XP) = make_double2(d0, d1);
+              for (int q = 0; q < C::KS; ++q) {
+                dmma8844(d0, d1, tile[4 * q] * sx, tq[q]);
+                dmma8844(e0, e1, arow1[4 * q] * sx, tq[q]);
               }
+              *reinterpret_cast<double2*>(xw) = make_double2(d0, d1);
+              if (xrow1_ok) *reinterpret_cast<double2*>(xw + 32 * C::XP) = make_double2(e0, e1);
+            } else {
+              double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+              for (int q = 0; q < C::KS; ++q) dmma8844(d0, d1, tile[4 * q] * sx, tq[q]);
+              *reinterpret_cast<double2*>(xw) = make_double2(d0, d1);
             }
           }
           if (p >= zlo && p <= zhi) {
