@@ -356,6 +356,10 @@ struct DevBuf {
 void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, double* out,
                      const int* gate);
 size_t reduce_scratch_size(size_t nseg);
+// all passes but the last: returns the <= 1024 partials left (count in *J_out) for a final
+// one-warp pass that the caller may fuse with its scalar epilogue (vec.cuh reduce_final_fin)
+const double* reduce_segments_to_warp(Ctx* c, const double* seg, size_t nseg, double* scratch, const int* gate,
+                                      size_t* J_out);
 // segment partials of (x .* y) over a row shape (both unscaled)
 void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, const int* gate);
 // out = x * sx + coef * (old * so) elementwise (identity operator / copies), with seg of out^2

@@ -215,7 +215,7 @@ __global__ void fin_wq0_kernel(DevState* s) {
 }
 
 // F_b (krylov.cpp:391-395)
-__global__ void fin_beta_kernel(DevState* s) {
+__device__ __forceinline__ void fin_beta_dev(DevState* s) {
   if (!s->flags[0]) return;
   const double beta = sqrt(s->red_u);
   s->beta = beta;
@@ -228,7 +228,7 @@ __global__ void fin_beta_kernel(DevState* s) {
 }
 
 // F_p (krylov.cpp:398)
-__global__ void fin_p_kernel(DevState* s) {
+__device__ __forceinline__ void fin_p_dev(DevState* s) {
   if (!s->flags[0] || !s->flags[1]) return;
   s->flags[2] = sqrt(s->red_p) > 0.0 ? 1 : 0;
 }
@@ -270,7 +270,7 @@ __global__ void left_count_kernel(DevState* s, int in_loop) {
 }
 
 // F_a (krylov.cpp:399-431)
-__global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) {
+__device__ __forceinline__ void fin_alpha_dev(DevState* s, double* alphas, double* betas) {
   if (!s->flags[0]) return;
   double alpha_next = 0.0;
   int breakdown = 1;
@@ -300,7 +300,7 @@ __global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) {
 }
 
 // F_i: finish_iteration (krylov.cpp:131-180) + evaluate_stopping (krylov.cpp:240-254)
-__global__ void fin_iter_kernel(DevState* s, mlsqr_iter_rec* trace, mlsqr_stop stop) {
+__device__ __forceinline__ void fin_iter_dev(DevState* s, mlsqr_iter_rec* trace, mlsqr_stop stop) {
   if (!s->flags[0]) return;
   if (s->flags[3]) s->wnorm2 = s->red_wq;
   const int iter = s->iter;
@@ -411,6 +411,32 @@ void validate_stop(const mlsqr_stop& s) {  // StoppingConfig::validate (krylov.c
   require(s.atol >= 0.0 && s.btol >= 0.0, MLSQR_EINVAL, "tolerances must be >= 0");
 }
 
+__global__ void fin_beta_kernel(DevState* s) { fin_beta_dev(s); }
+__global__ void fin_p_kernel(DevState* s) { fin_p_dev(s); }
+__global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) { fin_alpha_dev(s, alphas, betas); }
+__global__ void fin_iter_kernel(DevState* s, mlsqr_iter_rec* trace, mlsqr_stop stop) { fin_iter_dev(s, trace, stop); }
+
+// the same scalar steps as epilogues of the final reduction pass (vec.cuh reduce_final_fin)
+struct FinBeta {
+  DevState* s;
+  __device__ void operator()() const { fin_beta_dev(s); }
+};
+struct FinP {
+  DevState* s;
+  __device__ void operator()() const { fin_p_dev(s); }
+};
+struct FinAlpha {
+  DevState* s;
+  double *alphas, *betas;
+  __device__ void operator()() const { fin_alpha_dev(s, alphas, betas); }
+};
+struct FinIter {
+  DevState* s;
+  mlsqr_iter_rec* trace;
+  mlsqr_stop stop;
+  __device__ void operator()() const { fin_iter_dev(s, trace, stop); }
+};
+
 // ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
@@ -460,6 +486,19 @@ struct Runner {
                          data ? c->data_distributed() : c->sharded());
   }
 
+  // reduce, then the scalar step F: one fused final pass when the partials are local, else the
+  // distributed reduction followed by the separate scalar kernel
+  template <class F, class K>
+  void reduce_fin(double* seg, size_t nseg, double* out, const int* gate, bool data, F fin, K kernel) {
+    const bool dist = data ? c->data_distributed() : c->sharded();
+    if (!dist) {
+      reduce_segments_fin(c, seg, nseg, ws->scratch.p, out, gate, fin);
+    } else {
+      reduce(seg, nseg, out, gate, data);
+      kernel();
+    }
+  }
+
   double* vbuf() const { return pc ? ws->v.p : ws->p.p; }
 
   // z slabs, mlsqr mode: K_A's input vtilde is final after the V-cycle, so its R ghost planes
@@ -479,7 +518,8 @@ struct Runner {
     if (vghost_async()) MLSQR_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   }
 
-  void precond(const int* gate) {
+  // M^{-1} p and the <v, p> partials; in the loop the reduction's final pass also runs F_a
+  void precond(const int* gate, bool fin_alpha = false) {
     if (pc) {
       pc->in_guarded = ws->guard > 0;
       pc->solve(ws->p.p, ws->v.p, ws->seg_vp.p, gate, ws->sol);
@@ -487,7 +527,15 @@ struct Runner {
     } else {
       seg_dot(c, ws->p.p, ws->p.p, ws->sol, ws->seg_vp.p, gate);
     }
-    reduce(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false);
+    if (!fin_alpha) {
+      reduce(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false);
+      return;
+    }
+    reduce_fin(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false, FinAlpha{st, ws->alphas.p, ws->betas.p},
+               [&] {
+                 fin_alpha_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p, ws->betas.p);
+                 c->count();
+               });
   }
 
   void init(const double* g) {
@@ -537,8 +585,8 @@ struct Runner {
     ea.in_guarded = true;
     ea.ghosts_ready = vghost_async();
     op->apply(vbuf(), ws->u.p, ea);
-    reduce(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true);
-    fin_beta_kernel<<<1, 1, 0, c->stream>>>(st);
+    reduce_fin(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true, FinBeta{st},
+               [&] { fin_beta_kernel<<<1, 1, 0, c->stream>>>(st); c->count(); });
     store_left(1);
     // K_B: p_s <- A^T(u_s*su) + (-beta)(p_s*sv)
     Epi eb;
@@ -550,12 +598,11 @@ struct Runner {
     eb.gate = flag(1);
     eb.in_guarded = true;
     op->adjoint(ws->u.p, ws->p.p, eb);
-    reduce(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1), false);
-    fin_p_kernel<<<1, 1, 0, c->stream>>>(st);
+    reduce_fin(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1), false, FinP{st},
+               [&] { fin_p_kernel<<<1, 1, 0, c->stream>>>(st); c->count(); });
     // M^{-1}
-    precond(flag(2));
+    precond(flag(2), true);  // + F_a
     fork_vghost();
-    fin_alpha_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p, ws->betas.p);
     store_basis(1);
     // K_U
     {
@@ -564,8 +611,13 @@ struct Runner {
       update_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
                                                 ws->sol.len, ws->sol.rows, ws->seg_wq.p);
     }
-    reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false);
+    store_snapshot();  // f is final after K_U; F_i (which advances iter / flags) runs last
+    auto fin_iter = [&] {
+      fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
+      c->count();
+    };
     if (tau != 0.0 && stop.use_s4) {
+      reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false);
       // exact data residual |g - A f| (krylov.cpp:142-144): (A f - g)^2 partials
       Epi er;
       er.old = g;
@@ -573,12 +625,14 @@ struct Runner {
       er.seg = ws->seg_res.p;
       er.gate = gate_active();
       op->apply(ws->f.p, ws->tmp_rows.p, er);
-      reduce(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active(), true);
+      reduce_fin(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active(), true,
+                 FinIter{st, ws->trace.p, stop}, fin_iter);
+    } else {
+      reduce_fin(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false, FinIter{st, ws->trace.p, stop},
+                 fin_iter);
     }
-    store_snapshot();
-    fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
     join_vghost();
-    c->count(5);
+    c->count(1);  // update_kernel
     c->check_launch();
   }
 };

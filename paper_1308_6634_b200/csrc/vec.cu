@@ -116,6 +116,24 @@ size_t reduce_scratch_size(size_t nseg) {
   return tot + 1;
 }
 
+const double* reduce_segments_to_warp(Ctx* c, const double* seg, size_t nseg, double* scratch, const int* gate,
+                                      size_t* J_out) {
+  const double* cur = seg;
+  size_t J = nseg;
+  double* s = scratch;
+  while (J > 1024) {
+    const size_t K = (J + 1023) / 1024;
+    reduce2_kernel<<<(unsigned)((K + 7) / 8), 256, 0, c->stream>>>(cur, J, K, s, gate);
+    c->count();
+    c->check_launch();
+    cur = s;
+    s += K;
+    J = K;
+  }
+  *J_out = J;
+  return cur;
+}
+
 void reduce_segments(Ctx* c, const double* seg, size_t nseg, double* scratch, double* out,
                      const int* gate) {
   const double* cur = seg;

@@ -74,4 +74,33 @@ __device__ __forceinline__ double block_reduce3(const double* __restrict__ in, s
   return r;
 }
 
+// Final canonical pass (<= 1024 partials, one warp: thread-serial level + shuffle level) fused
+// with the scalar step that consumes the result: thread 0 writes *out, then runs fin() -- also
+// when the reduction itself is gated off (the scalar steps test their own flags), exactly as the
+// separate reduce + fin kernels did.
+template <class F>
+__global__ void __launch_bounds__(32) reduce_final_fin(const double* __restrict__ in, size_t J,
+                                                       double* __restrict__ out, const int* gate, F fin) {
+  const int lane = threadIdx.x;
+  if (!(gate && *gate == 0)) {
+    const size_t base = (size_t)lane * 32;
+    double v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = base + j < J ? in[base + j] : 0.0;
+    const double r = tree32(tree32_serial(v));
+    if (lane == 0) *out = r;
+  }
+  if (lane == 0) fin();
+}
+
+template <class F>
+void reduce_segments_fin(Ctx* c, const double* seg, size_t nseg, double* scratch, double* out, const int* gate,
+                         F fin) {
+  size_t J = 0;
+  const double* cur = reduce_segments_to_warp(c, seg, nseg, scratch, gate, &J);
+  reduce_final_fin<F><<<1, 32, 0, c->stream>>>(cur, J, out, gate, fin);
+  c->count();
+  c->check_launch();
+}
+
 }  // namespace mlsqr_b200
