@@ -154,6 +154,63 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
   }
 }
 
+// 2D: the same pair on a 32 x 8 tile -- x1 on the tile plus its one-point halo ring goes to shared
+// memory (x1 is 0 outside the grid, where it meets exactly-zero boundary coefficients), then the
+// second sweep; D and the row sums in sweep_zm_kernel<2>'s order.  Level-0 traffic 4 + 1 words
+// per point instead of 3 + 5 for the two kernels, and one launch fewer per level.
+__global__ void __launch_bounds__(256) sweep_fn2d_kernel(Lvl L, const double* __restrict__ b,
+                                                         double* __restrict__ out, double omega,
+                                                         double* __restrict__ seg, const int* gate) {
+  if (gate && *gate == 0) return;
+  __shared__ double xs[10][35];
+  const int nx = L.nx, ny = L.ny;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const double eps = *L.eps;
+  auto diag = [&](long i) {  // diag_at order: x-, x+, y-, y+ ; then + eps
+    double d = 0.0;
+    d = d + L.cx[i - 1];
+    d = d + L.cx[i];
+    d = d + L.cy[i - nx];
+    d = d + L.cy[i];
+    return d + eps;
+  };
+  for (int k = tid; k < 10 * 34; k += 256) {
+    const int r = k / 34, cc = k - r * 34;
+    const int gx = x0 - 1 + cc, gy = y0 - 1 + r;
+    double x1 = 0.0;
+    if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
+      const long i = (long)gy * nx + gx;
+      x1 = 0.0 + (omega * (b[i] - 0.0)) / diag(i);
+    }
+    xs[r][cc] = x1;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int gx = x0 + tx, gy = y0 + ty;
+  if (gy >= ny) return;  // whole warp (one row segment)
+  double v = 0.0, bi = 0.0;
+  if (gx < nx) {
+    const long i = (long)gy * nx + gx;
+    const double d = diag(i);
+    bi = b[i];
+    const double xc = xs[ty + 1][tx + 1];
+    // m_row order: y-, x-, diag, x+, y+
+    double acc = 0.0;
+    acc = acc + -L.cy[i - nx] * xs[ty][tx + 1];
+    acc = acc + -L.cx[i - 1] * xs[ty + 1][tx];
+    acc = acc + d * xc;
+    acc = acc + -L.cx[i] * xs[ty + 1][tx + 2];
+    acc = acc + -L.cy[i] * xs[ty + 2][tx + 1];
+    v = xc + (omega * (bi - acc)) / d;
+    out[i] = v;
+  }
+  if (seg) {
+    const double s2 = tree32(v * bi);
+    if (tx == 0) seg[(long)gy * ((nx + 31) / 32) + blockIdx.x] = s2;
+  }
+}
+
 // z chunk minimising (waves x planes per block), chunks of >= 8 planes
 static inline int fn_chunk(int nx, int ny, int nz, int sms) {
   const long bxy = (long)((nx + fn::TX - 1) / fn::TX) * ((ny + fn::TY - 1) / fn::TY);

@@ -620,7 +620,7 @@ class VCycle final : public Pc {
   // slab the kernel also computes x1 on the two ghost planes, from ghost planes of b (level 0:
   // only when the caller's p is guarded) and of the coefficients
   bool fn_ok(int l) const {
-    if (!fn_enabled_ || dims_ != 3) return false;
+    if (!fn_enabled_ || dims_ < 2) return false;
     if (!ctx->sharded()) return true;
     return lv_[(size_t)l].nz >= 2 && (l > 0 || in_guarded);
   }
@@ -628,6 +628,11 @@ class VCycle final : public Pc {
   void sweep_fn(int l, const double* b, double* out, double* seg, const int* gate) {
     const Level& L = lv_[(size_t)l];
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    if (dims_ == 2) {
+      sweep_fn2d_kernel<<<row_grid(L.nx, L.ny), dim3(32, 8), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate);
+      ctx->count();
+      return;
+    }
     const int zc = fn_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + fn::TX - 1) / fn::TX), (unsigned)((L.ny + fn::TY - 1) / fn::TY),
              (unsigned)((L.nz + zc - 1) / zc));

@@ -27,3 +27,8 @@ cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2' 3
 cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1' 5
 cap restrict 'restrict_zm_kernel' 4
 cap update 'update_kernel' 0
+# the other BASELINE configs (parity configs; one bench line each, no CPU baseline)
+for c in c1 c2 c3 c4; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --steps 3 --warmup 3 > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err
+  echo "bench $c rc=$?"
+done
