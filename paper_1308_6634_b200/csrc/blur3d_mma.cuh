@@ -88,6 +88,9 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
     const int i = 4 * q + (lane & 3) - (lane >> 2);
     tq[q] = (i >= 0 && i <= 2 * R) ? taps.t[i <= R ? i : 2 * R - i] : 0.0;
   }
+  double tz[R + 1];  // symmetric z taps t[0..R] in registers (no per-phase constant-bank loads)
+#pragma unroll
+  for (int k = 0; k <= R; ++k) tz[k] = taps.t[k];
   // this thread's outputs: row yr, columns yc, yc + 1 of the tile (y-pass fragment of warp w)
   const int yr = 8 * (warp >> 2) + (lane >> 2), yc = 8 * (warp & 3) + 2 * (lane & 3);
   static_assert(C::XPAIRS > 16 && C::XPAIRS <= 32, "x-pass pairs: one or two per warp");
@@ -179,12 +182,13 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
 #pragma unroll
               for (int q = 0; q < C::KS; ++q) dmma8844(yv0, yv1, tq[q], xb[4 * q * C::XP]);
             }
-            // ---- z pass: output zo' = p - R + j takes tap 2R - j
+            // ---- z pass: output zo' = p - R + j takes tap 2R - j (taps from registers)
 #pragma unroll
             for (int j = 0; j < C::NT; ++j) {
               const int s = (u + j) % C::NT;
-              acc[0][s] = fma(TAP(2 * R - j), yv0, j == C::NT - 1 ? 0.0 : acc[0][s]);
-              acc[1][s] = fma(TAP(2 * R - j), yv1, j == C::NT - 1 ? 0.0 : acc[1][s]);
+              const double t = tz[(2 * R - j) <= R ? 2 * R - j : j];
+              acc[0][s] = fma(t, yv0, j == C::NT - 1 ? 0.0 : acc[0][s]);
+              acc[1][s] = fma(t, yv1, j == C::NT - 1 ? 0.0 : acc[1][s]);
             }
             const int zo = p - R;
             if (zo >= z0 && zo < z1) {
