@@ -149,6 +149,11 @@ class EnvelopeCholMap final : public Pc {
     require(bytes <= 8e9, MLSQR_EINVAL,
             "envelope Cholesky of this grid needs " + std::to_string(bytes / 1e9) +
                 " GB; use the V-cycle map for large grids");
+    // the recurrences are sequential (the reference's order): ~n b^2 / 2 dependent steps on one thread
+    const double steps = (double)n * (double)E_.b * (double)E_.b / 2.0;
+    require(steps <= 2e9, MLSQR_EINVAL,
+            "envelope Cholesky of this grid is ~" + std::to_string(steps / 1e9) +
+                " G sequential steps on one device thread; use the inner-CG or V-cycle map");
     env_.alloc(n * (E_.b + 1));
     E_.e = env_.p;
     DevBuf<long long> bad(1);
