@@ -93,12 +93,12 @@ def class_bytes(cfg, world=1):
     d = cfg["dims"]
     n = float(cfg["n"] ** d)
     r = 2.0 ** -d
-    if d >= 2 and world == 1:
+    if d >= 2:  # (z slabs fuse them too: the Krylov p the V-cycle receives is guarded)
         # level-0 smoothing launches per V(2,2): fused first+second sweep (b + d coefficient arrays
         # -> x), prolong+sweep (x, x_c, b, coefficients -> x), last sweep (x, b, coefficients -> x)
         sweep_words = [(1 + d) + 1, (3 + d + r), (3 + d)]
     else:
-        # z slabs at level 0 without a guarded rhs, or 1D: first-from-zero, normal, prolong+sweep, normal
+        # 1D: first-from-zero, normal, prolong+sweep, normal
         sweep_words = [(2 + d), (3 + d), (3 + d + r), (3 + d)]
     m = float(cfg["ns"] * cfg["nd"]) if cfg.get("kind") == "fdot" else n
     return {
