@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
   const long col = inxy ? (long)py * nx + px : 0;
   auto idx = [&](int z) { return (long)z * nxy + col; };
   // a plane exists if it is in the global grid and local or one of the two ghost planes
-  auto on = [&](int z) { return inxy && z >= -1 && z <= nz && z + zoff >= 0 && z + zoff < nzg; };
+  const int zon_lo = max(-1, -zoff), zon_hi = min(nz, nzg - 1 - zoff);
+  auto on = [&](int z) { return inxy && z >= zon_lo && z <= zon_hi; };
   auto first = [&](const FnPlane& s, double d, bool in) { return in ? 0.0 + (omega * (s.b - 0.0)) / d : 0.0; };
 
   // prologue: plane z0-1 (own column only), plane z0 (published), plane z0+1 (loaded)
@@ -110,10 +111,11 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
   if (act) ring[0][sr][sc] = x1c;
   FnPlane n = fn_load(L, b, on(z0 + 1), idx(z0 + 1), nx);
   int slot = 0;  // ring slot of plane z
-  for (int z = z0; z < z1; ++z) {
-    FnPlane f = fn_load(L, b, on(z + 2), idx(z + 2), nx);  // prefetch
+  long o = idx(z0);  // offset of plane z, advanced by one plane per step
+  for (int z = z0; z < z1; ++z, o += nxy) {
+    FnPlane f = fn_load(L, b, on(z + 2), o + 2 * nxy, nx);  // prefetch
     if (on(z + 2 + kFnL2Ahead)) {
-      const long i = idx(z + 2 + kFnL2Ahead);
+      const long i = o + (2 + kFnL2Ahead) * nxy;
       prefetch_l2(b + i);
       prefetch_l2(L.cx + i);
       prefetch_l2(L.cy + i);
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
         acc = acc + -c.cy * ring[slot][sr + 1][sc];
         acc = acc + -c.cz * x1n;
         v = x1c + (omega * (c.b - acc)) / dc;
-        out[idx(z)] = v;
+        out[o] = v;
       }
       if (seg) {
         const double s = tree32(v * (ix ? c.b : 0.0));
