@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
   FnPlane n = fn_load(L, b, on(z0 + 1), idx(z0 + 1), nx);
   int slot = 0;  // ring slot of plane z
   long o = idx(z0);  // offset of plane z, advanced by one plane per step
+#pragma unroll 3
   for (int z = z0; z < z1; ++z, o += nxy) {
     FnPlane f = fn_load(L, b, on(z + 2), o + 2 * nxy, nx);  // prefetch
     if (on(z + 2 + kFnL2Ahead)) {
