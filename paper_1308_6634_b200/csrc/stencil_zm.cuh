@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
       xn = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z0 + 1, i + nxy);
     }
   }
+#pragma unroll 2
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
       const I j = i + 3 * nxy;
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
   }
   const bool owner = ok && (tx % 2 == 0) && (D < 2 || ty % 2 == 0);
   double s = 0.0;
+#pragma unroll 2
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
       const I j = i + 3 * nxy;
