@@ -170,10 +170,13 @@ class LoopComm final : public Comm {
     g_->send_lo[rank] = send_lo;
     g_->send_hi[rank] = send_hi;
     g_->barrier();
+    // on the caller's stream and waited for: a device-to-device cudaMemcpy does not block the
+    // host, and the legacy stream it would run on does not order against non-blocking streams
     if (rank > 0)
-      MLSQR_CUDA(cudaMemcpy(recv_lo, g_->send_hi[rank - 1], count * sizeof(double), cudaMemcpyDeviceToDevice));
+      MLSQR_CUDA(cudaMemcpyAsync(recv_lo, g_->send_hi[rank - 1], count * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (rank + 1 < size)
-      MLSQR_CUDA(cudaMemcpy(recv_hi, g_->send_lo[rank + 1], count * sizeof(double), cudaMemcpyDeviceToDevice));
+      MLSQR_CUDA(cudaMemcpyAsync(recv_hi, g_->send_lo[rank + 1], count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MLSQR_CUDA(cudaStreamSynchronize(s));
     g_->barrier();
   }
   void allgather(const double* send, size_t count, double* recv, cudaStream_t s) override {
@@ -181,7 +184,9 @@ class LoopComm final : public Comm {
     g_->send[rank] = send;
     g_->barrier();
     for (int k = 0; k < size; ++k)
-      MLSQR_CUDA(cudaMemcpy(recv + (size_t)k * count, g_->send[k], count * sizeof(double), cudaMemcpyDeviceToDevice));
+      MLSQR_CUDA(cudaMemcpyAsync(recv + (size_t)k * count, g_->send[k], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 s));
+    MLSQR_CUDA(cudaStreamSynchronize(s));
     g_->barrier();
   }
   void allreduce_max_u64(unsigned long long* buf, cudaStream_t s) override {
@@ -191,11 +196,13 @@ class LoopComm final : public Comm {
     unsigned long long mx = 0;
     for (int k = 0; k < size; ++k) {
       unsigned long long v = 0;
-      MLSQR_CUDA(cudaMemcpy(&v, g_->maxbuf[k], sizeof(v), cudaMemcpyDeviceToHost));
+      MLSQR_CUDA(cudaMemcpyAsync(&v, g_->maxbuf[k], sizeof(v), cudaMemcpyDeviceToHost, s));
+      MLSQR_CUDA(cudaStreamSynchronize(s));
       if (v > mx) mx = v;
     }
     g_->barrier();
-    MLSQR_CUDA(cudaMemcpy(buf, &mx, sizeof(mx), cudaMemcpyHostToDevice));
+    MLSQR_CUDA(cudaMemcpyAsync(buf, &mx, sizeof(mx), cudaMemcpyHostToDevice, s));
+    MLSQR_CUDA(cudaStreamSynchronize(s));
     g_->barrier();
   }
 

@@ -352,27 +352,29 @@ __global__ void __launch_bounds__(256) update_kernel(const DevState* __restrict_
                                                      const double* __restrict__ p, size_t len,
                                                      size_t rows, double* __restrict__ seg) {
   if (!s->flags[0]) return;
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
+  // rows in a block-stride loop (the scalars and the column index are loaded / formed once)
   const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
   const bool upd = s->flags[3] != 0;
-  double prod = 0.0;
-  if (xi < len) {
-    const size_t i = row * len + xi;
-    const double wi = w[i];
-    f[i] = f[i] + s->sc * wi;
-    if (upd) {
-      const double sv = s->sv, ndc = s->neg_dc;
-      const double wn = v[i] * sv + ndc * wi;
-      const double qn = p[i] * sv + ndc * q[i];
-      w[i] = wn;
-      q[i] = qn;
-      prod = wn * qn;
+  const double sc = s->sc, sv = s->sv, ndc = s->neg_dc;
+  const size_t chunks = (len + 31) / 32, rstep = (size_t)gridDim.y * blockDim.y;
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += rstep) {
+    double prod = 0.0;
+    if (xi < len) {
+      const size_t i = row * len + xi;
+      const double wi = w[i];
+      f[i] = f[i] + sc * wi;
+      if (upd) {
+        const double wn = v[i] * sv + ndc * wi;
+        const double qn = p[i] * sv + ndc * q[i];
+        w[i] = wn;
+        q[i] = qn;
+        prod = wn * qn;
+      }
     }
-  }
-  if (upd) {
-    const double t = tree32(prod);
-    if (threadIdx.x == 0) seg[row * ((len + 31) / 32) + blockIdx.x] = t;
+    if (upd) {
+      const double t = tree32(prod);
+      if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = t;
+    }
   }
 }
 
@@ -608,8 +610,10 @@ struct Runner {
     {
       TimedRegion tr(c, MLSQR_TCLASS_UPDATE);
       dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
-      update_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
-                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
+      // four rows per thread (the row loop keeps every warp one row segment)
+      const dim3 grd4(grd.x, (unsigned)((ws->sol.rows + 31) / 32));
+      update_kernel<<<grd4, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
+                                                 ws->sol.len, ws->sol.rows, ws->seg_wq.p);
     }
     store_snapshot();  // f is final after K_U; F_i (which advances iter / flags) runs last
     auto fin_iter = [&] {
