@@ -188,7 +188,7 @@ class BlurOp final : public Op {
       // wide 1D/2D taps live in device memory; 2D runs as x pass + y pass
       wide_ = true;
       dtx_.alloc((size_t)(2 * radius + 1));
-      MLSQR_CUDA(cudaMemcpy(dtx_.p, taps, sizeof(double) * (2 * radius + 1), cudaMemcpyHostToDevice));
+      MLSQR_CUDA(cudaMemcpyAsync(dtx_.p, taps, sizeof(double) * (2 * radius + 1), cudaMemcpyHostToDevice, ctx->stream));
       dty_ = dtx_.p;
       ry_ = radius;
       if (dims_ == 2) {
@@ -222,7 +222,7 @@ class BlurOp final : public Op {
         DevBuf<double> probe(1);
         int zero = 0;
         DevBuf<int> g0(1);
-        MLSQR_CUDA(cudaMemcpy(g0.p, &zero, sizeof(int), cudaMemcpyHostToDevice));
+        MLSQR_CUDA(cudaMemcpyAsync(g0.p, &zero, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
         none.gate = g0.p;  // gated off: the kernel returns at once
         fused3d(ctx, radius, probe.p, probe.p, 1, 1, 1, taps_, none);
         MLSQR_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -247,11 +247,11 @@ class BlurOp final : public Op {
     require(ry >= 0 && ry <= kMaxWide, MLSQR_EINVAL, "blur radius must lie in [0, " + std::to_string(kMaxWide) + "]");
     if (!wide_) {  // move the x taps to device memory too: both passes read WideTaps
       dtx_.alloc((size_t)(2 * taps_.R + 1));
-      MLSQR_CUDA(cudaMemcpy(dtx_.p, taps_.t, sizeof(double) * dtx_.n, cudaMemcpyHostToDevice));
+      MLSQR_CUDA(cudaMemcpyAsync(dtx_.p, taps_.t, sizeof(double) * dtx_.n, cudaMemcpyHostToDevice, ctx->stream));
       wide_ = true;
     }
     dtyo_.alloc((size_t)(2 * ry + 1));
-    MLSQR_CUDA(cudaMemcpy(dtyo_.p, ty, sizeof(double) * dtyo_.n, cudaMemcpyHostToDevice));
+    MLSQR_CUDA(cudaMemcpyAsync(dtyo_.p, ty, sizeof(double) * dtyo_.n, cudaMemcpyHostToDevice, ctx->stream));
     dty_ = dtyo_.p;
     ry_ = ry;
     axes_ = true;
