@@ -122,9 +122,9 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
     auto inside = [&](int zz) { return zz >= zin_lo && zz <= zin_hi; };
     auto stage = [&](int zz) { return (qbase + (unsigned)(zz - zlo)) & (C::NSTAGE - 1); };
     auto parity = [&](int zz) { return ((qbase + (unsigned)(zz - zlo)) >> 2) & 1u; };
-    auto issue = [&](int zz) {
+    auto issue = [&](int zz) {  // called by thread 0 only
       if (zz > zhi) return;
-      if (tid == 0) {
+      {
         const int st = stage(zz);
         const int zo = zz - R;
         const bool lin = inside(zz);
@@ -139,8 +139,10 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
     const bool ok0 = gx < nx && gy < ny, ok1 = gx + 1 < nx && gy < ny;
     double* const obase = out + (size_t)gy * nx + gx;
     __syncthreads();
-    issue(zlo);
-    issue(zlo + 1);
+    if (tid == 0) {
+      issue(zlo);
+      issue(zlo + 1);
+    }
     for (int pb = zlo - 1; pb <= zhi + 1; pb += C::NT) {
 #pragma unroll
       for (int u = 0; u < C::NT; ++u) {
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(512, 1) blur3d_mma(const double* __restrict__ 
           // one warp polls the TMA barrier; the CTA barrier then publishes the landed plane
           if (warp == 0 && p + 1 <= zhi) mbar_wait(bars + stage(p + 1), parity(p + 1));
           __syncthreads();
-          issue(p + 3);
+          if (tid == 0) issue(p + 3);
           // ---- x pass of plane p+1 on the tensor cores: 4 * MT tiles over 16 warps
           const int xz = p + 1;
           if (inside(xz)) {
