@@ -820,3 +820,21 @@ def test_outer_inner_cg_matches_direct_and_is_deterministic(ctx):
     assert np.array_equal(again.solution, direct.solution)
     assert [s.penalty_value for s in again.steps] == [s.penalty_value for s in direct.steps]
     assert [s.inner_iterations for s in again.steps] == [s.inner_iterations for s in direct.steps]
+
+
+def test_solve_options_together(ctx, dev):
+    """store_basis and record_snapshots in one solve (mlsqr_solve_with): the same iterate and
+    bidiagonalization as a plain solve, every snapshot row, and the basis rows."""
+    shape = (32, 32)
+    taps, f, g, o = deblur_problem(dev, shape, 2.0, 6)
+    gop = mb.SeparableGaussianBlur(shape, taps=taps)
+    vc = mb.VCycleMap(shape, 1 / 32, 3)
+    vc.update(f, mb.PenaltySpec.tv_smoothed(0.05))
+    st = gstop(12)
+    plain = mb.mlsqr(gop, vc, g, 1e-2, st)
+    both = mb.mlsqr(gop, vc, g, 1e-2, st, store_basis=True, record_snapshots=True)
+    assert np.array_equal(both.solution, plain.solution) and np.array_equal(both.alphas, plain.alphas)
+    assert both.snapshots.shape == (12, 1024) and np.array_equal(both.snapshots[-1], plain.solution)
+    assert both.basis.shape == (len(both.alphas), 1024)
+    partial = mb.mlsqr(gop, vc, g, 1e-2, gstop(5))
+    assert np.array_equal(both.snapshots[4], partial.solution)
