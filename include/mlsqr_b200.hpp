@@ -73,6 +73,14 @@ class GpuLinearOperator final : public mlsqr::LinearOperator {
     check(mlsqr_blur_create(c.get(), dims, nx, ny, nz, taps.data(), static_cast<int>(taps.size() / 2), &op));
     return GpuLinearOperator(op);
   }
+  // SeparableGaussianBlur2D with its own per-axis factors kx_(nx), ky_(ny) (linop.cpp:142-149)
+  static GpuLinearOperator blur2d_axes(Context& c, std::size_t nx, std::size_t ny, std::span<const double> taps_x,
+                                       std::span<const double> taps_y) {
+    mlsqr_op* op = nullptr;
+    check(mlsqr_blur2d_create_axes(c.get(), nx, ny, taps_x.data(), static_cast<int>(taps_x.size() / 2),
+                                   taps_y.data(), static_cast<int>(taps_y.size() / 2), &op));
+    return GpuLinearOperator(op);
+  }
   static GpuLinearOperator dense(Context& c, std::size_t rows, std::size_t cols,
                                  std::span<const double> row_major, std::size_t sol_row_len = 0) {
     mlsqr_op* op = nullptr;

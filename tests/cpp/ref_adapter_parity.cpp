@@ -173,6 +173,16 @@ int main() {
     EXPECT(fthrew);
   }
 
+  // a non-square grid: the reference operator's two factors on the device, bit for bit
+  {
+    const SeparableGaussianBlur2D ref2(40, 24, 0.04);
+    GaussianConvolution1D kx(40, 0.04, 1.0), ky(24, 0.04, 1.0);
+    auto g2 = mlsqr_b200::GpuLinearOperator::blur2d_axes(ctx, 40, 24, kx.taps(), ky.taps());
+    std::vector<double> xin(40 * 24);
+    for (std::size_t i = 0; i < xin.size(); ++i) xin[i] = std::sin(0.37 * static_cast<double>(i));
+    EXPECT(g2.apply(xin) == ref2.apply(xin));
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
