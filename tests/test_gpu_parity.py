@@ -838,3 +838,19 @@ def test_solve_options_together(ctx, dev):
     assert both.basis.shape == (len(both.alphas), 1024)
     partial = mb.mlsqr(gop, vc, g, 1e-2, gstop(5))
     assert np.array_equal(both.snapshots[4], partial.solution)
+
+
+@pytest.mark.parametrize("dims,shape", [(1, (2,)), (2, (2, 2)), (2, (3, 2)), (3, (2, 2, 2))])
+def test_spd_solver_maps_smallest_grids(ctx, dev, dims, shape):
+    """Edge sizes for the SpdSolver maps: the smallest grids the reference's Grid admits (and the
+    3D extension), k_inner = 1, bit-exact with the oracle's device order."""
+    n = int(np.prod(shape))
+    rng = np.random.default_rng(n)
+    f, p = rng.standard_normal(n), rng.standard_normal(n)
+    m = mb.VCycleMap(shape, 1.0 / shape[0], 1)
+    eps = m.update(f, mb.PenaltySpec("pm_log", 0.3))
+    grid = dev.grid(dims, shape, 1.0 / shape[0])
+    cx, cy, cz = dev.edge_coeffs(grid, f, "pm_log", 0.3)
+    assert np.array_equal(mb.CholeskyMap(m).solve(p), dev.env_chol_map(grid, cx, cy, cz, eps).solve(p))
+    for k in (1, 3):
+        assert np.array_equal(mb.InnerCgMap(m, k).solve(p), dev.inner_cg_map(grid, cx, cy, cz, eps, k).solve(p))
