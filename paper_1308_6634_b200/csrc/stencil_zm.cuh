@@ -12,6 +12,15 @@
 // becomes acc + (+-0), which is acc exactly (the accumulators start at +0 and
 // can never reach -0).  Results are bit-identical to the oracle.
 
+#ifndef MLSQR_ZM_PREFETCH
+#define MLSQR_ZM_PREFETCH 1
+#endif
+constexpr bool kZmPrefetch = MLSQR_ZM_PREFETCH;
+#ifndef MLSQR_ZM_AHEAD
+#define MLSQR_ZM_AHEAD 3
+#endif
+constexpr int kZmAhead = MLSQR_ZM_AHEAD;  // planes ahead of the z march
+
 // iterate value at fine index j (plus the prolongated coarse correction)
 // I: element index type -- int where the level (with guards) fits 2^31 elements: every
 // access is then one IMAD.WIDE instead of a 64-bit add chain (same loads, same bits)
@@ -65,8 +74,8 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
   }
 #pragma unroll 2
   for (int z = z0; z < z1; ++z, i += nxy) {
-    if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
-      const I j = i + 3 * nxy;
+    if (kZmPrefetch && D >= 3 && z + kZmAhead < z1) {  // L2 prefetch of plane z+kZmAhead (no registers)
+      const I j = i + kZmAhead * nxy;
       prefetch_l2(b + j);
       prefetch_l2(cx + j);
       prefetch_l2(cy + j);
@@ -178,8 +187,8 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
   double s = 0.0;
 #pragma unroll 2
   for (int z = z0; z < z1; ++z, i += nxy) {
-    if (D >= 3 && z + 3 < z1) {  // L2 prefetch of plane z+3 (no registers)
-      const I j = i + 3 * nxy;
+    if (kZmPrefetch && D >= 3 && z + kZmAhead < z1) {  // L2 prefetch of plane z+kZmAhead (no registers)
+      const I j = i + kZmAhead * nxy;
       prefetch_l2(b + j);
       prefetch_l2(cx + j);
       prefetch_l2(cy + j);
