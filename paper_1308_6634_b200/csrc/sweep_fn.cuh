@@ -27,7 +27,7 @@ constexpr int THREADS = 32 * WARPS;
 constexpr int MINB = 1;  // resident blocks per SM (19 warps, 92 registers)
 }  // namespace fn
 
-constexpr int kFnL2Ahead = 2;  // L2 prefetch distance beyond the register prefetch (planes)
+constexpr int kFnL2Ahead = 1;  // L2 prefetch distance beyond the register prefetch (planes)
 
 struct FnPlane {
   double b, cx, cxm, cy, cym, cz;
