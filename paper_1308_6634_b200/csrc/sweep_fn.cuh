@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
     act = lane < 2 * TY;
   }
   const bool inxy = act && px >= 0 && px < nx && py >= 0 && py < ny;
-  const bool outw = w >= 1 && w <= TY;  // output rows (whole warps)
+  const bool outw = w >= 1 && w <= TY && py < ny;  // output rows (whole warps)
   const bool ix = inxy && outw;
   const double eps = *L.eps;
   const long chunks = (nx + 31) / 32;

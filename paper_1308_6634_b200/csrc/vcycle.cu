@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restr
 
 #include "stencil_zm.cuh"
 #include "sweep_fn.cuh"
+#include "sweep_pn.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
 __global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
@@ -332,6 +333,7 @@ class VCycle final : public Pc {
     eps_.alloc((size_t)levels);
     maxd_.alloc(1);
     if (const char* e = getenv("MLSQR_FN_SWEEPS")) fn_enabled_ = e[0] != '0';
+    if (const char* e = getenv("MLSQR_PN_SWEEPS")) pn_enabled_ = e[0] != '0';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
     if (c->sharded()) setup_agglomeration(nu_pre, nu_post, omega, kc);
   }
@@ -368,6 +370,7 @@ class VCycle final : public Pc {
     coarse_ = new VCycle(cctx_, dims_, (size_t)A.nx, (size_t)A.ny, (size_t)nzg_l(la_), h_ * (double)(1 << la_),
                          (int)lv_.size() - la_, nu_pre, nu_post, omega, kc);
     coarse_->fn_enabled_ = fn_enabled_;
+    coarse_->pn_enabled_ = pn_enabled_;
     cb_.alloc(coarse_->n);
   }
 
@@ -599,10 +602,14 @@ class VCycle final : public Pc {
       return dst;
     }
     for (int s = 0; s < nu_post_; ++s) {
-      const bool last = s + 1 == nu_post_;
+      const bool ppair = s == 0 && pn_ok(l);  // sweeps 3 + 4 in one kernel, x3 on chip
+      const bool last = s + (ppair ? 2 : 1) == nu_post_;
       double* dst = (last && out) ? out : bufs[nb];
       double* sg = (last && out) ? seg : nullptr;
-      if (s == 0) {
+      if (ppair) {
+        sweep_pn(l, cur, xc, b, dst, sg, gate);
+        ++s;
+      } else if (s == 0) {
         hx(l, cur);
         if (!agg) hx(l + 1, xc);  // an agglomerated correction is whole: its neighbour planes are real
         sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
@@ -625,6 +632,27 @@ class VCycle final : public Pc {
     return lv_[(size_t)l].nz >= 2 && (l > 0 || in_guarded);
   }
 
+  // prolongation + post-sweeps 3 and 4 in one kernel (3D, whole grids: on a z slab sweep 4
+  // would need x3 on the ghost planes, which the unfused path exchanges)
+  bool pn_ok(int) const { return pn_enabled_ && dims_ == 3 && !ctx->sharded() && nu_post_ >= 2; }
+
+  void sweep_pn(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
+                const int* gate) {
+    const Level& L = lv_[(size_t)l];
+    const Level& C = lv_[(size_t)l + 1];
+    TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    const int zc = fn_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
+    dim3 grd((unsigned)((L.nx + pn::TX - 1) / pn::TX), (unsigned)((L.ny + pn::TY - 1) / pn::TY),
+             (unsigned)((L.nz + zc - 1) / zc));
+    if (fits_i32(L))
+      sweep_pn_kernel<int><<<grd, dim3(32, pn::WARPS), 0, ctx->stream>>>(view(l), x, xc, C.nx, C.ny, b, out,
+                                                                          omega_, seg, gate, zc);
+    else
+      sweep_pn_kernel<long><<<grd, dim3(32, pn::WARPS), 0, ctx->stream>>>(view(l), x, xc, C.nx, C.ny, b, out,
+                                                                           omega_, seg, gate, zc);
+    ctx->count();
+  }
+
   void sweep_fn(int l, const double* b, double* out, double* seg, const int* gate) {
     const Level& L = lv_[(size_t)l];
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
@@ -643,6 +671,7 @@ class VCycle final : public Pc {
 
  public:
   bool fn_enabled_ = true;
+  bool pn_enabled_ = false;  // sweep_pn measured slower (sweep_pn.cuh)
 
  private:
 

@@ -165,6 +165,47 @@ def test_vcycle_explicit_coefficients_and_variants(ctx, dev):
         assert np.array_equal(vc.solve(x), om.solve(x)), (levels, pre, post, kc)
 
 
+@pytest.mark.parametrize("pn", ["1", "0"])
+def test_vcycle_3d_variants_fused_and_unfused(ctx, dev, monkeypatch, pn):
+    """3D V-cycles through the fused post-sweep kernel (sweep_pn: prolongation + sweeps 3, 4)
+    and, with MLSQR_PN_SWEEPS=0, through two sweep_zm launches: both bit-equal to the oracle,
+    on a grid whose x/y extents are not tile multiples, for several (pre, post, coarse) counts."""
+    monkeypatch.setenv("MLSQR_PN_SWEEPS", pn)
+    shape, h = (40, 24, 12), 1 / 40
+    n = 40 * 24 * 12
+    grid = dev.grid(3, shape, h)
+    rng = np.random.default_rng(17)
+    f = rng.standard_normal(n)
+    cx, cy, cz = dev.edge_coeffs(grid, f, "tv", 0.2)
+    for levels, pre, post, kc in [(3, 2, 2, 4), (3, 1, 3, 2), (2, 2, 1, 3), (3, 3, 4, 1), (1, 2, 2, 5)]:
+        vc = mb.VCycleMap(shape, h, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
+        vc.set_coefficients(cx, cy, cz, 1e-3)
+        om = dev.vcycle(grid, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
+        om.set(cx, cy, cz, 1e-3)
+        x = rng.uniform(-1, 1, n)
+        assert np.array_equal(vc.solve(x), om.solve(x)), (levels, pre, post, kc)
+
+
+@pytest.mark.parametrize("levels,pn", [(1, "0"), (2, "0"), (2, "1")])
+def test_mlsqr_3d_ragged_tiles_bit_exact(ctx, dev, monkeypatch, levels, pn):
+    """y extent 20 (not a multiple of the 16-row fused-sweep tile) with the <v, p> partials
+    written by the last sweep: the 1-level case ends in sweep_fn, the 2-level one in sweep_zm
+    or (MLSQR_PN_SWEEPS=1) sweep_pn."""
+    monkeypatch.setenv("MLSQR_PN_SWEEPS", pn)
+    shape = (24, 20, 16)
+    taps, f, g, o = deblur_problem(dev, shape, 1.5, 4, seed=21, noise=0.02)
+    h = 1 / 24
+    grid = dev.grid(3, shape, h)
+    vc = mb.VCycleMap(shape, h, levels, coarse_sweeps=2)
+    vc.update(f, mb.PenaltySpec.tv_smoothed(0.1))
+    cx, cy, cz = dev.edge_coeffs(grid, f, "tv", 0.1)
+    om = dev.vcycle(grid, levels, coarse_sweeps=2)
+    om.set(cx, cy, cz, 1e-8 * dev.max_diag(grid, cx, cy, cz))
+    st = gstop(25)
+    compare_solves(mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), vc, g, 5e-3, st),
+                   dev.mlsqr(o, om, g, 5e-3, ostop_from(st)))
+
+
 def test_vcycle_rejects_bad_hierarchy(ctx):
     with pytest.raises(ValueError):
         mb.VCycleMap((24, 24), 1 / 24, 5)  # 24 does not halve 4 times
