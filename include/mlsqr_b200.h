@@ -12,6 +12,12 @@
  * Pointer kinds: MLSQR_HOST buffers are copied in/out around the call (the
  * reference's std::span contract, linop.hpp:33-36); MLSQR_DEVICE buffers are
  * cudaMalloc'ed memory on the context's device and stay resident.
+ * Stream ordering of MLSQR_DEVICE buffers: the library reads and writes them on
+ * the context's stream only.  A library-owned stream (NULL at mlsqr_ctx_create)
+ * is created cudaStreamNonBlocking, so it does NOT wait for work the caller
+ * queued elsewhere: either create the context on the stream that produces the
+ * inputs, or synchronize that stream before the call.  Every call returns
+ * after the context's stream has drained, so outputs are ready on return.
  *
  * Arithmetic: fp64 everywhere, in the canonical device order documented in
  * DESIGN.md (bit-exact with the oracle's DEVICE order).

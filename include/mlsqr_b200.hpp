@@ -130,6 +130,12 @@ class GpuSpdMap final : public mlsqr::SpdMap {
     check(mlsqr_inner_cg_map_create(m.handle(), k_inner, &pc));
     return GpuSpdMap(pc);
   }
+  // a host SpdMap plug-in (mlsqr_callback_map_create): fn(user, p, v) on host vectors of length n
+  static GpuSpdMap callback(Context& c, std::size_t n, mlsqr_host_map_fn fn, void* user) {
+    mlsqr_pc* pc = nullptr;
+    check(mlsqr_callback_map_create(c.get(), n, fn, user, &pc));
+    return GpuSpdMap(pc);
+  }
   GpuSpdMap(GpuSpdMap&& o) noexcept : pc_(o.pc_) { o.pc_ = nullptr; }
   ~GpuSpdMap() override { mlsqr_pc_destroy(pc_); }
   using SpdMap::solve;
@@ -212,9 +218,11 @@ inline mlsqr::SolveResult gpu_mlsqr(const GpuLinearOperator& a, const GpuSpdMap&
     o.record_snapshots = 1;
     o.snapshots = snaps.data();
   }
-  check(mlsqr_solve_with(a.handle(), m.handle(), g.data(), tau, &s, &o, r.solution.data(), tr.data(), al.data(),
-                         be.data(), &info, MLSQR_HOST),
-        info.breakdown_iteration);
+  // status first: the breakdown iteration is only valid once the solve has returned
+  // (function arguments are evaluated in an unspecified order)
+  const int status = mlsqr_solve_with(a.handle(), m.handle(), g.data(), tau, &s, &o, r.solution.data(), tr.data(),
+                                      al.data(), be.data(), &info, MLSQR_HOST);
+  check(status, info.breakdown_iteration);
   detail::fill_trace(r, tr, info);
   for (int j = 0; opts.record_snapshots && j < info.iterations; ++j)
     r.trace.snapshots.emplace_back(snaps.begin() + j * n, snaps.begin() + (j + 1) * n);
@@ -239,9 +247,9 @@ inline mlsqr::SolveResult gpu_cg_normal(const GpuLinearOperator& a, const GpuSpd
   r.solution.assign(a.n_cols(), 0.0);
   std::vector<mlsqr_iter_rec> tr(static_cast<std::size_t>(stop.max_iters));
   mlsqr_solve_info info{};
-  check(mlsqr_cg_normal_solve(a.handle(), m ? m->handle() : nullptr, g.data(), tau, &s, r.solution.data(),
-                              tr.data(), &info, MLSQR_HOST),
-        info.breakdown_iteration);
+  const int status = mlsqr_cg_normal_solve(a.handle(), m ? m->handle() : nullptr, g.data(), tau, &s,
+                                           r.solution.data(), tr.data(), &info, MLSQR_HOST);
+  check(status, info.breakdown_iteration);
   detail::fill_trace(r, tr, info);
   return r;
 }

@@ -244,9 +244,15 @@ def _is_dev(t) -> bool:
 
 
 def _vec_in(x):
-    """(pointer, length, kind, keepalive) for a host array or a CUDA tensor."""
+    """(pointer, length, kind, keepalive) for a host array or a CUDA tensor.
+
+    Stream ordering (mlsqr_b200.h, MLSQR_DEVICE): a context's stream does not wait for
+    torch's streams, so before the library reads a CUDA tensor (or writes into memory that
+    torch work still pending may use) torch's current stream on that device is drained."""
     if _is_dev(x):
         assert str(x.dtype) == "torch.float64" and x.is_contiguous(), "device vectors must be contiguous float64"
+        import torch
+        torch.cuda.current_stream(x.device).synchronize()
         return C.c_void_p(x.data_ptr()), x.numel(), DEVICE, x
     a = _f64(x).ravel()
     return C.c_void_p(a.ctypes.data), a.size, HOST, a

@@ -109,38 +109,38 @@ __global__ void blur_pass_kernel(const double* __restrict__ in, double* __restri
                                  bool first, bool last) {
   if (e.gate && *e.gate == 0) return;
   const size_t rows = ny * nz;
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const size_t x = (size_t)blockIdx.x * 32 + threadIdx.x;
-  const int R = taps.R;
-  double v = 0.0;
-  if (x < nx) {
-    const size_t y = row % ny, z = row / ny;
-    long c, N;
-    size_t stride, base;
-    if (AXIS == 0) {
-      c = (long)x; N = (long)nx; stride = 1; base = row * nx;
-    } else if (AXIS == 1) {
-      c = (long)y; N = (long)ny; stride = nx; base = z * nx * ny + x;
-    } else {
-      c = (long)z; N = (long)nz; stride = nx * ny; base = y * nx + x;
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += (size_t)gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const size_t x = (size_t)blockIdx.x * 32 + threadIdx.x;
+    const int R = taps.R;
+    double v = 0.0;
+    if (x < nx) {
+      const size_t y = row % ny, z = row / ny;
+      long c, N;
+      size_t stride, base;
+      if (AXIS == 0) {
+        c = (long)x; N = (long)nx; stride = 1; base = row * nx;
+      } else if (AXIS == 1) {
+        c = (long)y; N = (long)ny; stride = nx; base = z * nx * ny + x;
+      } else {
+        c = (long)z; N = (long)nz; stride = nx * ny; base = y * nx + x;
+      }
+      const double sx = (first && e.sx) ? *e.sx : 1.0;
+      double acc = 0.0;
+      for (int k = 0; k <= 2 * R; ++k) {
+        const long j = c + k - R;
+        if (j < 0 || j >= N) continue;
+        double a = in[base + (size_t)j * stride];
+        if (first && e.sx) a = a * sx;
+        acc = mac<FMA>(taps.t[k], a, acc);
+      }
+      const size_t i = row * nx + x;
+      v = last ? epilogue(acc, e, i) : acc;
+      out[i] = v;
     }
-    const double sx = (first && e.sx) ? *e.sx : 1.0;
-    double acc = 0.0;
-    for (int k = 0; k <= 2 * R; ++k) {
-      const long j = c + k - R;
-      if (j < 0 || j >= N) continue;
-      double a = in[base + (size_t)j * stride];
-      if (first && e.sx) a = a * sx;
-      acc = mac<FMA>(taps.t[k], a, acc);
+    if (last && e.seg) {
+      const double s = tree32(v * v);
+      if (threadIdx.x == 0) e.seg[row * ((nx + 31) / 32) + blockIdx.x] = s;
     }
-    const size_t i = row * nx + x;
-    v = last ? epilogue(acc, e, i) : acc;
-    out[i] = v;
-  }
-  if (last && e.seg) {
-    const double s = tree32(v * v);
-    if (threadIdx.x == 0) e.seg[row * ((nx + 31) / 32) + blockIdx.x] = s;
   }
 }
 
@@ -176,6 +176,12 @@ static bool fused3d(Ctx* c, int R, const double* in, double* out, int nx, int ny
   }
 }
 
+static bool symmetric(const double* t, int R) {
+  for (int k = 0; k < R; ++k)
+    if (!(t[k] == t[2 * R - k])) return false;
+  return true;
+}
+
 class BlurOp final : public Op {
  public:
   BlurOp(Ctx* c, int dims, size_t nx, size_t ny, size_t nz, const double* taps, int radius)
@@ -184,6 +190,9 @@ class BlurOp final : public Op {
     require(radius >= 0 && radius <= (dims <= 2 ? kMaxWide : kMaxRadius), MLSQR_EINVAL,
             "blur radius must lie in [0, " + std::to_string(dims <= 2 ? kMaxWide : kMaxRadius) + "]");
     require(nx_ >= 1 && ny_ >= 1 && nz_ >= 1, MLSQR_EDIM, "blur grid must be non-empty");
+    // adjoint() runs the forward pass (A = A^T, linop.cpp:168-170), which holds only for
+    // symmetric taps: anything else would silently break the bidiagonalization
+    require(symmetric(taps, radius), MLSQR_EINVAL, "blur taps must be symmetric (t[k] == t[2R-k]): A^T = A");
     if (radius > kMaxRadius) {
       // wide 1D/2D taps live in device memory; 2D runs as x pass + y pass
       wide_ = true;
@@ -245,6 +254,7 @@ class BlurOp final : public Op {
   void set_y_taps(const double* ty, int ry) {
     require(dims_ == 2 && !ctx->sharded(), MLSQR_EINVAL, "per-axis taps are for the 2D operator");
     require(ry >= 0 && ry <= kMaxWide, MLSQR_EINVAL, "blur radius must lie in [0, " + std::to_string(kMaxWide) + "]");
+    require(symmetric(ty, ry), MLSQR_EINVAL, "blur taps must be symmetric (t[k] == t[2R-k]): A^T = A");
     if (!wide_) {  // move the x taps to device memory too: both passes read WideTaps
       dtx_.alloc((size_t)(2 * taps_.R + 1));
       MLSQR_CUDA(cudaMemcpyAsync(dtx_.p, taps_.t, sizeof(double) * dtx_.n, cudaMemcpyHostToDevice, ctx->stream));
@@ -279,7 +289,7 @@ class BlurOp final : public Op {
     EpiArgs a = to_args(e);
     const size_t rows_ = ny_ * nz_;
     dim3 blk(32, 8);
-    dim3 grd((unsigned)((nx_ + 31) / 32), (unsigned)((rows_ + 7) / 8));
+    dim3 grd((unsigned)((nx_ + 31) / 32), row_grid(rows_));
     const WideTaps wx{dtx_.p, (int)(dtx_.n / 2)}, wy{dty_, ry_};
     if (dims_ == 1 && wide_) {
       blur_pass_kernel<0, false, WideTaps><<<grd, blk, 0, ctx->stream>>>(in, out, nx_, ny_, nz_, wx, a, true, true);

@@ -18,21 +18,21 @@ namespace {
 __global__ void cgn_q_kernel(double* __restrict__ q, const double* __restrict__ mx, double tau,
                              const double* __restrict__ d, size_t len, size_t rows, size_t chunks,
                              double* __restrict__ seg) {
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
-  double v = 0.0;
-  if (xi < len) {
-    const size_t i = row * len + xi;
-    double qi = q[i];
-    if (mx) {
-      qi = qi + tau * mx[i];
-      q[i] = qi;
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += (size_t)gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+    double v = 0.0;
+    if (xi < len) {
+      const size_t i = row * len + xi;
+      double qi = q[i];
+      if (mx) {
+        qi = qi + tau * mx[i];
+        q[i] = qi;
+      }
+      v = d[i] * qi;
     }
-    v = d[i] * qi;
+    v = tree32(v);
+    if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
   }
-  v = tree32(v);
-  if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
 }
 
 // gamma = rho / curv (krylov.cpp:591), on the device so the update needs no host round trip
@@ -47,20 +47,20 @@ __global__ void cgn_update_kernel(double* __restrict__ x, double* __restrict__ r
                                   const double* __restrict__ d, const double* __restrict__ q,
                                   const double* __restrict__ gamma, size_t len, size_t rows,
                                   size_t chunks, double* __restrict__ seg) {
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
-  double v = 0.0;
-  if (xi < len) {
-    const size_t i = row * len + xi;
-    const double gm = gamma[0], ng = gamma[1];
-    x[i] = x[i] + gm * d[i];
-    const double ri = r[i] + ng * q[i];
-    r[i] = ri;
-    v = ri * ri;
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += (size_t)gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+    double v = 0.0;
+    if (xi < len) {
+      const size_t i = row * len + xi;
+      const double gm = gamma[0], ng = gamma[1];
+      x[i] = x[i] + gm * d[i];
+      const double ri = r[i] + ng * q[i];
+      r[i] = ri;
+      v = ri * ri;
+    }
+    v = tree32(v);
+    if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
   }
-  v = tree32(v);
-  if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
 }
 
 // d = r + beta d  (xpby, krylov.cpp:625)
@@ -97,7 +97,7 @@ void solve_cg_normal(Op* op, VCycle* m, const double* g, double tau, const mlsqr
   MLSQR_CUDA(cudaMemcpyAsync(m1_d, &minus_one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   MLSQR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
   MLSQR_CUDA(cudaMemsetAsync(qf_d, 0, sizeof(double), c->stream));
-  const dim3 blk(32, 8), grdS((unsigned)S.chunks(), (unsigned)((S.rows + 7) / 8));
+  const dim3 blk(32, 8), grdS((unsigned)S.chunks(), row_grid(S.rows));
   auto reduce = [&](double* out, size_t nseg) { reduce_segments(c, seg.p, nseg, scratch.p, out, nullptr); };
 
   // b = A^T g; r = b; d = r (krylov.cpp:564-566)

@@ -63,6 +63,13 @@ __device__ __forceinline__ double tree32_serial(double* v) {
 }
 
 // vector layout for reductions: `rows` rows of `len` elements, row-major
+// gridDim.y for the (32, 8)-block row kernels: one block row per 8 rows, capped at CUDA's
+// 65535 limit (those kernels loop over rows with a gridDim.y stride)
+inline unsigned row_grid(size_t rows) {
+  const size_t g = (rows + 7) / 8;
+  return (unsigned)(g < 65535 ? (g ? g : 1) : 65535);
+}
+
 struct RowShape {
   size_t len;   // elements per row (x extent)
   size_t rows;  // number of rows (ny * nz)

@@ -384,21 +384,21 @@ __global__ void init_wq_kernel(const DevState* __restrict__ s, double* __restric
                                const double* __restrict__ v, const double* __restrict__ p,
                                size_t len, size_t rows, double* __restrict__ seg) {
   if (!s->flags[0]) return;
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
-  double prod = 0.0;
-  if (xi < len) {
-    const size_t i = row * len + xi;
-    const double sv = s->sv;
-    const double wn = v[i] * sv, qn = p[i] * sv;
-    w[i] = wn;
-    q[i] = qn;
-    f[i] = 0.0;
-    prod = wn * qn;
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += (size_t)gridDim.y * blockDim.y) {
+    const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+    double prod = 0.0;
+    if (xi < len) {
+      const size_t i = row * len + xi;
+      const double sv = s->sv;
+      const double wn = v[i] * sv, qn = p[i] * sv;
+      w[i] = wn;
+      q[i] = qn;
+      f[i] = 0.0;
+      prod = wn * qn;
+    }
+    const double t = tree32(prod);
+    if (threadIdx.x == 0) seg[row * ((len + 31) / 32) + blockIdx.x] = t;
   }
-  const double t = tree32(prod);
-  if (threadIdx.x == 0) seg[row * ((len + 31) / 32) + blockIdx.x] = t;
 }
 
 __global__ void zero_kernel(double* __restrict__ f, size_t n) {
@@ -564,7 +564,7 @@ struct Runner {
     fin_alpha1_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p);
     store_basis(0);
     store_left(0);
-    dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
+    dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), row_grid(ws->sol.rows));
     init_wq_kernel<<<grd, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,
                                                ws->sol.len, ws->sol.rows, ws->seg_wq.p);
     reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, gate_active(), false);
@@ -609,7 +609,7 @@ struct Runner {
     // K_U
     {
       TimedRegion tr(c, MLSQR_TCLASS_UPDATE);
-      dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), (unsigned)((ws->sol.rows + 7) / 8));
+      dim3 blk(32, 8), grd((unsigned)ws->sol.chunks(), row_grid(ws->sol.rows));
       // four rows per thread (the row loop keeps every warp one row segment)
       const dim3 grd4(grd.x, (unsigned)((ws->sol.rows + 31) / 32));
       update_kernel<<<grd4, blk, 0, c->stream>>>(st, ws->f.p, ws->w.p, ws->q.p, vbuf(), ws->p.p,

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
                                                        double* __restrict__ out, double omega,
                                                        double* __restrict__ seg, const int* gate, int zc) {
   if (gate && *gate == 0) return;
-  constexpr bool P = MODE == kProlong || MODE == kProlongOnly;
+  constexpr bool P = MODE == kProlong;
   const int xx = blockIdx.x * 32 + threadIdx.x;
   const int yy = blockIdx.y * 8 + threadIdx.y;
   if (yy >= L.ny) return;  // whole warp (one row)
@@ -89,13 +89,11 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
       cxn = cx[i + nxy];
       if (D >= 2) cyn = cy[i + nxy];
       if (D >= 3) czn = cz[i + nxy];
-      if (D >= 3 && MODE != kFirst && MODE != kProlongOnly)
+      if (D >= 3 && MODE != kFirst)
         xnn = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z + 2, i + 2 * nxy);  // guard covers z+2 = nz
     }
     double v;
-    if (MODE == kProlongOnly) {
-      v = xcur;
-    } else {
+    {
       // diag_at order: x-, x+, y-, y+, z-, z+ ; then + eps
       const double cxm = cx[i - 1];
       double d = 0.0;
@@ -137,12 +135,8 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
     // roll
     czm = czc;
     xm = xcur;
-    if (MODE == kProlongOnly) {
-      if (z + 1 < z1) xcur = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z + 1, i + nxy);
-    } else {
-      xcur = xn;
-      xn = xnn;
-    }
+    xcur = xn;
+    xn = xnn;
     bc = bn;
     cxc = cxn;
     cyc = cyn;
@@ -263,14 +257,15 @@ __global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* _
 // grid does not exist; the branch-free rows rely on its coefficient being exactly 0)
 __global__ void zero_boundary_edges_kernel(Lvl L, int zoff, int nzg, double* cx, double* cy, double* cz) {
   const int rows = L.ny * L.nz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int xx = blockIdx.x * 32 + threadIdx.x;
-  if (row >= rows || xx >= L.nx) return;
-  const int yy = row % L.ny, zz = row / L.ny;
-  const long i = (long)row * L.nx + xx;
-  if (xx + 1 == L.nx) cx[i] = 0.0;
-  if (cy && yy + 1 == L.ny) cy[i] = 0.0;
-  if (cz && zz + zoff + 1 == nzg) cz[i] = 0.0;  // global top plane
+  if (xx >= L.nx) return;
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const int yy = row % L.ny, zz = row / L.ny;
+    const long i = (long)row * L.nx + xx;
+    if (xx + 1 == L.nx) cx[i] = 0.0;
+    if (cy && yy + 1 == L.ny) cy[i] = 0.0;
+    if (cz && zz + zoff + 1 == nzg) cz[i] = 0.0;  // global top plane
+  }
 }
 
 // z chunk: enough blocks to fill the GPU a few times; even (restriction pairs fine planes)

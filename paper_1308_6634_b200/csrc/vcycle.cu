@@ -73,89 +73,24 @@ __device__ __forceinline__ double m_row(const Lvl& L, const double* __restrict__
   return acc;
 }
 
-enum SweepMode { kFirst = 0, kNormal = 1, kProlong = 2, kProlongOnly = 3 };
+enum SweepMode { kFirst = 0, kNormal = 1, kProlong = 2 };
 
 // one omega-Jacobi sweep: out = x + (omega * (b - M x)) / D   (x = 0 for kFirst,
-// x = x + P xc for kProlong); seg (optional) <- partials of out * b
-template <int MODE>
-__global__ void __launch_bounds__(256) sweep_kernel(Lvl L, const double* __restrict__ x,
-                                                    const double* __restrict__ xc, int cnx, int cny,
-                                                    const double* __restrict__ b,
-                                                    double* __restrict__ out, double omega,
-                                                    double* __restrict__ seg, const int* gate) {
-  if (gate && *gate == 0) return;
-  const int rows = L.ny * L.nz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const int xx = blockIdx.x * 32 + threadIdx.x;
-  const int yy = row % L.ny, zz = row / L.ny;
-  double v = 0.0, bi = 0.0;
-  if (xx < L.nx) {
-    const size_t i = (size_t)row * L.nx + xx;
-    bi = b[i];
-    if (MODE == kProlongOnly) {
-      v = xval<true>(x, xc, L, cnx, cny, xx, yy, zz, i);
-    } else {
-      const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
-      if (MODE == kFirst) {
-        // M * 0 = +0 exactly, so x1 = 0 + (omega * (b - 0)) / d
-        const double mx = 0.0;
-        v = 0.0 + (omega * (bi - mx)) / d;
-      } else {
-        const bool P = MODE == kProlong;
-        const double mx = P ? m_row<true>(L, x, xc, cnx, cny, xx, yy, zz, i, d)
-                            : m_row<false>(L, x, xc, cnx, cny, xx, yy, zz, i, d);
-        const double xi = P ? xval<true>(x, xc, L, cnx, cny, xx, yy, zz, i) : x[i];
-        v = xi + (omega * (bi - mx)) / d;
-      }
-    }
-    out[i] = v;
-  }
-  if (seg) {
-    const double s = tree32(v * bi);
-    if (threadIdx.x == 0) seg[(size_t)row * ((L.nx + 31) / 32) + blockIdx.x] = s;
-  }
-}
-
+// x = x + P xc for kProlong); seg (optional) <- partials of out * b  (stencil_zm.cuh)
 #include "stencil_zm.cuh"
 #include "sweep_fn.cuh"
-#include "sweep_pn.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
 __global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
   const int rows = L.ny * L.nz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int xx = blockIdx.x * 32 + threadIdx.x;
-  if (row >= rows || xx >= L.nx) return;
-  const int yy = row % L.ny, zz = row / L.ny;
-  const size_t i = (size_t)row * L.nx + xx;
-  const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
-  y[i] = m_row<false>(L, x, nullptr, 0, 0, xx, yy, zz, i, d);
-}
-
-// b_c[I] = sum over the children (ascending fine index) of (b - M x)
-__global__ void __launch_bounds__(256) restrict_kernel(Lvl L, const double* __restrict__ x,
-                                                       const double* __restrict__ b, int cnx,
-                                                       int cny, int cnz, double* __restrict__ bc,
-                                                       const int* gate) {
-  if (gate && *gate == 0) return;
-  const int crows = cny * cnz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
-  const int X = blockIdx.x * 32 + threadIdx.x;
-  if (row >= crows || X >= cnx) return;
-  const int Y = row % cny, Z = row / cny;
-  const int zc = L.cz ? 2 : 1, yc = L.cy ? 2 : 1;
-  double s = 0.0;
-  for (int dz = 0; dz < zc; ++dz)
-    for (int dy = 0; dy < yc; ++dy)
-      for (int dx = 0; dx < 2; ++dx) {
-        const int zz = zc * Z + dz, yy = yc * Y + dy, xx = 2 * X + dx;
-        const size_t i = ((size_t)zz * L.ny + yy) * L.nx + xx;
-        const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
-        const double r = b[i] - m_row<false>(L, x, nullptr, 0, 0, xx, yy, zz, i, d);
-        s = s + r;
-      }
-  bc[(size_t)row * cnx + X] = s;
+  if (xx >= L.nx) return;
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const int yy = row % L.ny, zz = row / L.ny;
+    const size_t i = (size_t)row * L.nx + xx;
+    const double d = diag_at(L, xx, yy, zz, i) + *L.eps;
+    y[i] = m_row<false>(L, x, nullptr, 0, 0, xx, yy, zz, i, d);
+  }
 }
 
 // Galerkin coarse edges (oracle coarsen()): sum of the fine edges crossing each coarse face
@@ -163,28 +98,29 @@ __global__ void coarsen_kernel(Lvl F, int cnx, int cny, int cnz, int czoff, int 
                                double* __restrict__ ccx, double* __restrict__ ccy,
                                double* __restrict__ ccz) {
   const int crows = cny * cnz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int X = blockIdx.x * 32 + threadIdx.x;
-  if (row >= crows || X >= cnx) return;
-  const int Y = row % cny, Z = row / cny;
-  const size_t fnx = F.nx, fnxy = (size_t)F.nx * F.ny;
-  const int zc = F.cz ? 2 : 1, yc = F.cy ? 2 : 1;
-  double sx = 0.0, sy = 0.0, sz = 0.0;
-  for (int dz = 0; dz < zc; ++dz)
-    for (int dy = 0; dy < yc; ++dy)
-      if (X + 1 < cnx) sx = sx + F.cx[(size_t)(zc * Z + dz) * fnxy + (size_t)(yc * Y + dy) * fnx + 2 * X + 1];
-  if (F.cy)
+  if (X >= cnx) return;
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < crows; row += gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const int Y = row % cny, Z = row / cny;
+    const size_t fnx = F.nx, fnxy = (size_t)F.nx * F.ny;
+    const int zc = F.cz ? 2 : 1, yc = F.cy ? 2 : 1;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
     for (int dz = 0; dz < zc; ++dz)
-      for (int dx = 0; dx < 2; ++dx)
-        if (Y + 1 < cny) sy = sy + F.cy[(size_t)(zc * Z + dz) * fnxy + (size_t)(2 * Y + 1) * fnx + 2 * X + dx];
-  if (F.cz)
-    for (int dy = 0; dy < 2; ++dy)
-      for (int dx = 0; dx < 2; ++dx)
-        if (Z + czoff + 1 < cnzg) sz = sz + F.cz[(size_t)(2 * Z + 1) * fnxy + (size_t)(2 * Y + dy) * fnx + 2 * X + dx];
-  const size_t I = (size_t)row * cnx + X;
-  ccx[I] = sx;
-  if (ccy) ccy[I] = sy;
-  if (ccz) ccz[I] = sz;
+      for (int dy = 0; dy < yc; ++dy)
+        if (X + 1 < cnx) sx = sx + F.cx[(size_t)(zc * Z + dz) * fnxy + (size_t)(yc * Y + dy) * fnx + 2 * X + 1];
+    if (F.cy)
+      for (int dz = 0; dz < zc; ++dz)
+        for (int dx = 0; dx < 2; ++dx)
+          if (Y + 1 < cny) sy = sy + F.cy[(size_t)(zc * Z + dz) * fnxy + (size_t)(2 * Y + 1) * fnx + 2 * X + dx];
+    if (F.cz)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx)
+          if (Z + czoff + 1 < cnzg) sz = sz + F.cz[(size_t)(2 * Z + 1) * fnxy + (size_t)(2 * Y + dy) * fnx + 2 * X + dx];
+    const size_t I = (size_t)row * cnx + X;
+    ccx[I] = sx;
+    if (ccy) ccy[I] = sy;
+    if (ccz) ccz[I] = sz;
+  }
 }
 
 // K_D: edge coefficients from a field, plus the max unshifted diagonal (atomic max on
@@ -194,16 +130,17 @@ __global__ void edge_coeffs_kernel(const double* __restrict__ f, int nx, int ny,
                                    double* __restrict__ cx, double* __restrict__ cy,
                                    double* __restrict__ cz) {
   const int rows = ny * nz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int xx = blockIdx.x * 32 + threadIdx.x;
-  if (row >= rows || xx >= nx) return;
-  const int yy = row % ny, zz = row / ny;
-  const size_t i = (size_t)row * nx + xx, nxy = (size_t)nx * ny;
-  const double fi = f[i];
-  cx[i] = xx + 1 < nx ? diffusivity(kind, T, fabs((f[i + 1] - fi) / h)) * scale : 0.0;
-  if (dims >= 2) cy[i] = yy + 1 < ny ? diffusivity(kind, T, fabs((f[i + nx] - fi) / h)) * scale : 0.0;
-  // global top plane has no +z edge; a slab's top plane reads f from the ghost plane above
-  if (dims >= 3) cz[i] = zz + zoff + 1 < nzg ? diffusivity(kind, T, fabs((f[i + nxy] - fi) / h)) * scale : 0.0;
+  if (xx >= nx) return;
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const int yy = row % ny, zz = row / ny;
+    const size_t i = (size_t)row * nx + xx, nxy = (size_t)nx * ny;
+    const double fi = f[i];
+    cx[i] = xx + 1 < nx ? diffusivity(kind, T, fabs((f[i + 1] - fi) / h)) * scale : 0.0;
+    if (dims >= 2) cy[i] = yy + 1 < ny ? diffusivity(kind, T, fabs((f[i + nx] - fi) / h)) * scale : 0.0;
+    // global top plane has no +z edge; a slab's top plane reads f from the ghost plane above
+    if (dims >= 3) cz[i] = zz + zoff + 1 < nzg ? diffusivity(kind, T, fabs((f[i + nxy] - fi) / h)) * scale : 0.0;
+  }
 }
 
 __global__ void max_diag_kernel(Lvl L, unsigned long long* __restrict__ out) {
@@ -247,27 +184,27 @@ __global__ void penalty_kernel(const double* __restrict__ f, int nx, int ny, int
                                int kind, double T, double h, double w, int zoff, int nzg,
                                double* __restrict__ seg) {
   const int rows = ny * nz;
-  const int row = blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const int xx = blockIdx.x * 32 + threadIdx.x;
-  double v = 0.0;
-  if (xx < nx) {
-    const int yy = row % ny, zz = row / ny;
-    const size_t i = (size_t)row * nx + xx, nxy = (size_t)nx * ny;
-    const double fi = f[i];
-    if (xx + 1 < nx) v = v + w * r_value(kind, T, fabs((f[i + 1] - fi) / h));
-    if (dims >= 2 && yy + 1 < ny) v = v + w * r_value(kind, T, fabs((f[i + nx] - fi) / h));
-    if (dims >= 3 && zz + zoff + 1 < nzg) v = v + w * r_value(kind, T, fabs((f[i + nxy] - fi) / h));
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += gridDim.y * blockDim.y) {  // gridDim.y <= 65535
+    const int xx = blockIdx.x * 32 + threadIdx.x;
+    double v = 0.0;
+    if (xx < nx) {
+      const int yy = row % ny, zz = row / ny;
+      const size_t i = (size_t)row * nx + xx, nxy = (size_t)nx * ny;
+      const double fi = f[i];
+      if (xx + 1 < nx) v = v + w * r_value(kind, T, fabs((f[i + 1] - fi) / h));
+      if (dims >= 2 && yy + 1 < ny) v = v + w * r_value(kind, T, fabs((f[i + nx] - fi) / h));
+      if (dims >= 3 && zz + zoff + 1 < nzg) v = v + w * r_value(kind, T, fabs((f[i + nxy] - fi) / h));
+    }
+    const double s = tree32(v);
+    if (threadIdx.x == 0) seg[(size_t)row * ((nx + 31) / 32) + blockIdx.x] = s;
   }
-  const double s = tree32(v);
-  if (threadIdx.x == 0) seg[(size_t)row * ((nx + 31) / 32) + blockIdx.x] = s;
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static inline dim3 row_grid(int nx, int rows) {
-  return dim3((unsigned)((nx + 31) / 32), (unsigned)((rows + 7) / 8));
+  return dim3((unsigned)((nx + 31) / 32), row_grid((size_t)rows));
 }
 
 class VCycle final : public Pc {
@@ -297,8 +234,13 @@ class VCycle final : public Pc {
     require(nx >= 2 && (dims < 2 || ey >= 2) && (dims < 3 || ez >= 2), MLSQR_EDIM,
             "grid extents must be at least 2");
     require(h > 0.0, MLSQR_EINVAL, "grid spacing must be positive");
-    require(levels >= 1 && levels <= 16 && nu_pre >= 1 && nu_post >= 0 && kc >= 1, MLSQR_EINVAL,
-            "V-cycle needs levels >= 1, nu_pre >= 1, nu_post >= 0, coarse sweeps >= 1");
+    require(levels >= 1 && levels <= 16 && nu_pre >= 1 && kc >= 1, MLSQR_EINVAL,
+            "V-cycle needs levels >= 1, nu_pre >= 1, coarse sweeps >= 1");
+    // the SpdMap contract (spdsolve.hpp:11-14): M^-1 must be a fixed SYMMETRIC positive definite
+    // map, which a V-cycle with omega-Jacobi smoothing is only when the post-smoother mirrors the
+    // pre-smoother; an asymmetric cycle would silently break the bidiagonalization
+    require(nu_post == nu_pre, MLSQR_EINVAL,
+            "V-cycle SpdMap needs nu_post == nu_pre (a symmetric map, spdsolve.hpp:11-14)");
     const size_t f = (size_t)1 << (levels - 1);
     require(nx % f == 0 && nx / f >= 2 && (dims < 2 || (ey % f == 0 && ey / f >= 2)) &&
                 (dims < 3 || (ez % f == 0 && ez / f >= 2)),
@@ -333,7 +275,6 @@ class VCycle final : public Pc {
     eps_.alloc((size_t)levels);
     maxd_.alloc(1);
     if (const char* e = getenv("MLSQR_FN_SWEEPS")) fn_enabled_ = e[0] != '0';
-    if (const char* e = getenv("MLSQR_PN_SWEEPS")) pn_enabled_ = e[0] != '0';
     MLSQR_CUDA(cudaMemsetAsync(eps_.p, 0, sizeof(double) * levels, c->stream));
     if (c->sharded()) setup_agglomeration(nu_pre, nu_post, omega, kc);
   }
@@ -370,7 +311,6 @@ class VCycle final : public Pc {
     coarse_ = new VCycle(cctx_, dims_, (size_t)A.nx, (size_t)A.ny, (size_t)nzg_l(la_), h_ * (double)(1 << la_),
                          (int)lv_.size() - la_, nu_pre, nu_post, omega, kc);
     coarse_->fn_enabled_ = fn_enabled_;
-    coarse_->pn_enabled_ = pn_enabled_;
     cb_.alloc(coarse_->n);
   }
 
@@ -596,20 +536,11 @@ class VCycle final : public Pc {
     restrict_to(l, cur, b, gate);
     const bool agg = coarse_ && l + 1 == la_;
     const double* xc = agg ? coarse_solve(C.b.p, gate) : level(l + 1, C.b.p, nullptr, nullptr, gate);
-    if (nu_post_ == 0) {
-      double* dst = out ? out : bufs[nb];
-      sweep<kProlongOnly>(l, cur, xc, b, dst, out ? seg : nullptr, gate);
-      return dst;
-    }
     for (int s = 0; s < nu_post_; ++s) {
-      const bool ppair = s == 0 && pn_ok(l);  // sweeps 3 + 4 in one kernel, x3 on chip
-      const bool last = s + (ppair ? 2 : 1) == nu_post_;
+      const bool last = s + 1 == nu_post_;
       double* dst = (last && out) ? out : bufs[nb];
       double* sg = (last && out) ? seg : nullptr;
-      if (ppair) {
-        sweep_pn(l, cur, xc, b, dst, sg, gate);
-        ++s;
-      } else if (s == 0) {
+      if (s == 0) {
         hx(l, cur);
         if (!agg) hx(l + 1, xc);  // an agglomerated correction is whole: its neighbour planes are real
         sweep<kProlong>(l, cur, xc, b, dst, sg, gate);
@@ -632,27 +563,6 @@ class VCycle final : public Pc {
     return lv_[(size_t)l].nz >= 2 && (l > 0 || in_guarded);
   }
 
-  // prolongation + post-sweeps 3 and 4 in one kernel (3D, whole grids: on a z slab sweep 4
-  // would need x3 on the ghost planes, which the unfused path exchanges)
-  bool pn_ok(int) const { return pn_enabled_ && dims_ == 3 && !ctx->sharded() && nu_post_ >= 2; }
-
-  void sweep_pn(int l, const double* x, const double* xc, const double* b, double* out, double* seg,
-                const int* gate) {
-    const Level& L = lv_[(size_t)l];
-    const Level& C = lv_[(size_t)l + 1];
-    TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
-    const int zc = fn_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
-    dim3 grd((unsigned)((L.nx + pn::TX - 1) / pn::TX), (unsigned)((L.ny + pn::TY - 1) / pn::TY),
-             (unsigned)((L.nz + zc - 1) / zc));
-    if (fits_i32(L))
-      sweep_pn_kernel<int><<<grd, dim3(32, pn::WARPS), 0, ctx->stream>>>(view(l), x, xc, C.nx, C.ny, b, out,
-                                                                          omega_, seg, gate, zc);
-    else
-      sweep_pn_kernel<long><<<grd, dim3(32, pn::WARPS), 0, ctx->stream>>>(view(l), x, xc, C.nx, C.ny, b, out,
-                                                                           omega_, seg, gate, zc);
-    ctx->count();
-  }
-
   void sweep_fn(int l, const double* b, double* out, double* seg, const int* gate) {
     const Level& L = lv_[(size_t)l];
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
@@ -671,7 +581,6 @@ class VCycle final : public Pc {
 
  public:
   bool fn_enabled_ = true;
-  bool pn_enabled_ = false;  // sweep_pn measured slower (sweep_pn.cuh)
 
  private:
 

@@ -15,21 +15,23 @@ __global__ void seg_dot_kernel(const double* __restrict__ x, const double* __res
                                size_t len, size_t rows, size_t chunks, double* __restrict__ seg,
                                const int* gate) {
   if (gate && *gate == 0) return;
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;  // whole warp leaves together (warp == one row segment)
-  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
-  double v = 0.0;
-  if (xi < len) {
-    const size_t i = row * len + xi;
-    v = x[i] * y[i];
+  // row-stride loop: gridDim.y is capped at 65535 (row_grid); a warp is one row segment, so
+  // every lane of a warp takes the same trip count
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += (size_t)gridDim.y * blockDim.y) {
+    const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+    double v = 0.0;
+    if (xi < len) {
+      const size_t i = row * len + xi;
+      v = x[i] * y[i];
+    }
+    v = tree32(v);
+    if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
   }
-  v = tree32(v);
-  if (threadIdx.x == 0) seg[row * chunks + blockIdx.x] = v;
 }
 
 void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, const int* gate) {
   if (s.n() == 0) return;
-  dim3 blk(32, 8), grd((unsigned)s.chunks(), (unsigned)((s.rows + 7) / 8));
+  dim3 blk(32, 8), grd((unsigned)s.chunks(), row_grid(s.rows));
   seg_dot_kernel<<<grd, blk, 0, c->stream>>>(x, y, s.len, s.rows, s.chunks(), seg, gate);
   c->count();
   c->check_launch();
@@ -41,26 +43,26 @@ void seg_dot(Ctx* c, const double* x, const double* y, RowShape s, double* seg, 
 __global__ void axpby_epi_kernel(const double* __restrict__ x, double* __restrict__ out,
                                  size_t len, size_t rows, size_t chunks, EpiArgs e) {
   if (e.gate && *e.gate == 0) return;
-  const size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y;
-  if (row >= rows) return;
-  const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
-  double v = 0.0;
-  if (xi < len) {
-    const size_t i = row * len + xi;
-    double a = x[i];
-    if (e.sx) a = a * *e.sx;
-    v = epilogue(a, e, i);
-    out[i] = v;
-  }
-  if (e.seg) {
-    const double s = tree32(v * v);
-    if (threadIdx.x == 0) e.seg[row * chunks + blockIdx.x] = s;
+  for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += (size_t)gridDim.y * blockDim.y) {
+    const size_t xi = (size_t)blockIdx.x * 32 + threadIdx.x;
+    double v = 0.0;
+    if (xi < len) {
+      const size_t i = row * len + xi;
+      double a = x[i];
+      if (e.sx) a = a * *e.sx;
+      v = epilogue(a, e, i);
+      out[i] = v;
+    }
+    if (e.seg) {
+      const double s = tree32(v * v);
+      if (threadIdx.x == 0) e.seg[row * chunks + blockIdx.x] = s;
+    }
   }
 }
 
 void axpby_epi(Ctx* c, const double* x, double* out, RowShape s, const Epi& e) {
   if (s.n() == 0) return;
-  dim3 blk(32, 8), grd((unsigned)s.chunks(), (unsigned)((s.rows + 7) / 8));
+  dim3 blk(32, 8), grd((unsigned)s.chunks(), row_grid(s.rows));
   axpby_epi_kernel<<<grd, blk, 0, c->stream>>>(x, out, s.len, s.rows, s.chunks(), to_args(e));
   c->count();
   c->check_launch();

@@ -347,7 +347,9 @@ SolverConfig parse_solver(const json& obj) {  // config.cpp:180-259
       reject_unknown(spd, "spd", {"mode", "levels", "nu_pre", "nu_post", "coarse_sweeps", "omega"});
       if (spd.contains("levels")) s.mg_levels = as_positive_int(spd["levels"], "levels");
       if (spd.contains("nu_pre")) s.nu_pre = as_positive_int(spd["nu_pre"], "nu_pre");
-      if (spd.contains("nu_post")) s.nu_post = static_cast<int>(as_count(spd["nu_post"], "nu_post"));
+      if (spd.contains("nu_post")) s.nu_post = as_positive_int(spd["nu_post"], "nu_post");
+      // M^-1 must be a symmetric map (spdsolve.hpp:11-14): the post-smoother mirrors the pre-smoother
+      if (s.nu_post != s.nu_pre) throw ConfigError("keys 'nu_pre' and 'nu_post' must be equal (a symmetric V-cycle)");
       if (spd.contains("coarse_sweeps")) s.coarse_sweeps = as_positive_int(spd["coarse_sweeps"], "coarse_sweeps");
       if (spd.contains("omega")) {
         s.omega = as_number(spd["omega"], "omega");

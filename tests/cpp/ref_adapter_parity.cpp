@@ -173,6 +173,44 @@ int main() {
     EXPECT(fthrew);
   }
 
+  // BreakdownError(iteration) with iteration > 0 crosses the boundary with the iteration the
+  // reference reports (krylov.cpp:401-406): a map that is the identity for its first 6 calls and
+  // -I afterwards, once as a reference SpdMap and once as a device-loop host plug-in
+  {
+    struct LateFlip final : SpdMap {
+      std::size_t n;
+      mutable int calls = 0;
+      explicit LateFlip(std::size_t n_) : n(n_) {}
+      std::size_t dimension() const override { return n; }
+      using SpdMap::solve;
+      void solve(std::span<const double> p, std::span<double> v) const override {
+        const double s = calls++ < 6 ? 1.0 : -1.0;
+        for (std::size_t i = 0; i < n; ++i) v[i] = s * p[i];
+      }
+    };
+    LateFlip cpu_flip(nx * nx), dev_flip(nx * nx);
+    auto fn = [](void* user, const double* p, double* v) -> int {
+      auto* m = static_cast<LateFlip*>(user);
+      m->solve(std::span<const double>(p, m->n), std::span<double>(v, m->n));
+      return 0;
+    };
+    auto gflip = mlsqr_b200::GpuSpdMap::callback(ctx, nx * nx, fn, &dev_flip);
+    int it_ref = -1, it_dev = -1;
+    try {
+      (void)mlsqr::mlsqr(cpu_op, cpu_flip, bundle.g, 1e-2, stop);
+    } catch (const BreakdownError& e) {
+      it_ref = e.iteration();
+    }
+    try {
+      (void)mlsqr_b200::gpu_mlsqr(gpu_op, gflip, bundle.g, 1e-2, stop);
+    } catch (const BreakdownError& e) {
+      it_dev = e.iteration();
+    }
+    std::printf("late breakdown: reference iteration %d, device loop iteration %d\n", it_ref, it_dev);
+    EXPECT(it_ref > 0);
+    EXPECT(it_dev == it_ref);
+  }
+
   // a non-square grid: the reference operator's two factors on the device, bit for bit
   {
     const SeparableGaussianBlur2D ref2(40, 24, 0.04);

@@ -156,7 +156,7 @@ def test_vcycle_explicit_coefficients_and_variants(ctx, dev):
     rng = np.random.default_rng(7)
     f = rng.standard_normal(1024)
     cx, cy, cz = dev.edge_coeffs(grid, f, "tv", 0.1)
-    for levels, pre, post, kc in [(1, 2, 2, 5), (2, 1, 0, 1), (3, 3, 1, 2), (4, 2, 2, 4)]:
+    for levels, pre, post, kc in [(1, 2, 2, 5), (2, 1, 1, 1), (3, 3, 3, 2), (4, 2, 2, 4)]:
         vc = mb.VCycleMap(shape, h, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
         vc.set_coefficients(cx, cy, None, 1e-3)
         om = dev.vcycle(grid, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
@@ -165,19 +165,19 @@ def test_vcycle_explicit_coefficients_and_variants(ctx, dev):
         assert np.array_equal(vc.solve(x), om.solve(x)), (levels, pre, post, kc)
 
 
-@pytest.mark.parametrize("pn", ["1", "0"])
-def test_vcycle_3d_variants_fused_and_unfused(ctx, dev, monkeypatch, pn):
-    """3D V-cycles through the fused post-sweep kernel (sweep_pn: prolongation + sweeps 3, 4)
-    and, with MLSQR_PN_SWEEPS=0, through two sweep_zm launches: both bit-equal to the oracle,
-    on a grid whose x/y extents are not tile multiples, for several (pre, post, coarse) counts."""
-    monkeypatch.setenv("MLSQR_PN_SWEEPS", pn)
+@pytest.mark.parametrize("fn", ["1", "0"])
+def test_vcycle_3d_variants_fused_and_unfused(ctx, dev, monkeypatch, fn):
+    """3D V-cycles with the first two pre-sweeps fused (sweep_fn, default) and, with
+    MLSQR_FN_SWEEPS=0, as two sweep_zm launches: both bit-equal to the oracle, on a grid whose
+    x/y extents are not tile multiples, for several (nu, coarse sweeps) counts."""
+    monkeypatch.setenv("MLSQR_FN_SWEEPS", fn)
     shape, h = (40, 24, 12), 1 / 40
     n = 40 * 24 * 12
     grid = dev.grid(3, shape, h)
     rng = np.random.default_rng(17)
     f = rng.standard_normal(n)
     cx, cy, cz = dev.edge_coeffs(grid, f, "tv", 0.2)
-    for levels, pre, post, kc in [(3, 2, 2, 4), (3, 1, 3, 2), (2, 2, 1, 3), (3, 3, 4, 1), (1, 2, 2, 5)]:
+    for levels, pre, post, kc in [(3, 2, 2, 4), (3, 1, 1, 2), (2, 3, 3, 3), (3, 4, 4, 1), (1, 2, 2, 5)]:
         vc = mb.VCycleMap(shape, h, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
         vc.set_coefficients(cx, cy, cz, 1e-3)
         om = dev.vcycle(grid, levels, nu_pre=pre, nu_post=post, coarse_sweeps=kc)
@@ -186,12 +186,10 @@ def test_vcycle_3d_variants_fused_and_unfused(ctx, dev, monkeypatch, pn):
         assert np.array_equal(vc.solve(x), om.solve(x)), (levels, pre, post, kc)
 
 
-@pytest.mark.parametrize("levels,pn", [(1, "0"), (2, "0"), (2, "1")])
-def test_mlsqr_3d_ragged_tiles_bit_exact(ctx, dev, monkeypatch, levels, pn):
+@pytest.mark.parametrize("levels", [1, 2])
+def test_mlsqr_3d_ragged_tiles_bit_exact(ctx, dev, levels):
     """y extent 20 (not a multiple of the 16-row fused-sweep tile) with the <v, p> partials
-    written by the last sweep: the 1-level case ends in sweep_fn, the 2-level one in sweep_zm
-    or (MLSQR_PN_SWEEPS=1) sweep_pn."""
-    monkeypatch.setenv("MLSQR_PN_SWEEPS", pn)
+    written by the last sweep: the 1-level case ends in sweep_fn, the 2-level one in sweep_zm."""
     shape = (24, 20, 16)
     taps, f, g, o = deblur_problem(dev, shape, 1.5, 4, seed=21, noise=0.02)
     h = 1 / 24
@@ -211,6 +209,11 @@ def test_vcycle_rejects_bad_hierarchy(ctx):
         mb.VCycleMap((24, 24), 1 / 24, 5)  # 24 does not halve 4 times
     with pytest.raises(mb.DimensionError):
         mb.VCycleMap((1, 8), 1.0, 1)
+    # an asymmetric cycle is not a symmetric map (spdsolve.hpp:11-14): rejected, not run
+    with pytest.raises(ValueError):
+        mb.VCycleMap((32, 32), 1 / 32, 3, nu_pre=2, nu_post=1)
+    with pytest.raises(ValueError):
+        mb.VCycleMap((32, 32), 1 / 32, 3, nu_pre=2, nu_post=0)
 
 
 @pytest.mark.parametrize("dims,shape,pen,T", [(2, (64, 64), "tv", 0.01), (3, (16, 16, 16), "pm_log", 0.05),
@@ -253,6 +256,36 @@ def compare_solves(gres, ores, exact=True):
     assert rel(gres.alphas, ores.alphas) <= TOL_AB
     assert rel(gres.betas, ores.betas) <= TOL_AB
     assert rel(gres.solution, ores.f) <= TOL_AB
+
+
+def test_blur_rejects_asymmetric_taps(ctx):
+    """adjoint() is the forward pass (A = A^T, linop.cpp:168-170): only symmetric taps qualify."""
+    with pytest.raises(ValueError):
+        mb.SeparableGaussianBlur((32, 32), taps=[0.1, 0.5, 0.3])
+    with pytest.raises(ValueError):
+        mb.SeparableGaussianBlur((16, 16, 16), taps=[0.2, 0.3, 0.6, 0.3, 0.1])
+
+
+def test_mlsqr_rows_beyond_grid_y_limit_bit_exact(ctx, dev):
+    """ny * nz = 532,480 rows: more than 65535 blocks of 8 rows, so every row-shaped kernel (segment
+    dots, axpby epilogues, the Krylov init, the M / V-cycle kernels) runs its row-stride loop."""
+    shape = (32, 1024, 520)
+    n = int(np.prod(shape))
+    taps = dev.taps(32, 1.0 / 32, radius=2)
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal(n)
+    h = 1 / 32
+    grid = dev.grid(3, shape, h)
+    vc = mb.VCycleMap(shape, h, 1, coarse_sweeps=2)
+    eps = vc.update(np.zeros(n), mb.PenaltySpec.tikhonov())
+    cx, cy, cz = dev.edge_coeffs(grid, np.zeros(n), "tikhonov", 1.0)
+    om = dev.vcycle(grid, 1, coarse_sweeps=2)
+    om.set(cx, cy, cz, eps)
+    st = gstop(3)
+    compare_solves(mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), vc, g, 1e-2, st),
+                   dev.mlsqr(dev.blur(3, shape, taps), om, g, 1e-2, ostop_from(st)))
+    x = rng.uniform(-1, 1, n)
+    assert np.array_equal(vc.m_apply(x), dev.m_apply(grid, cx, cy, cz, eps, x))
 
 
 @pytest.mark.parametrize("tau", [0.0, 1e-2, 1.0])
