@@ -90,7 +90,13 @@ int mlsqr_ctx_get_timing(mlsqr_ctx* ctx, int cls, double* ms, uint64_t* launches
 #define MLSQR_TCLASS_MG 3      /* whole V-cycle (all levels)                    */
 #define MLSQR_TCLASS_UPDATE 4  /* LSQR vector update (f, w, q) + w.q           */
 #define MLSQR_TCLASS_ITER 5    /* whole LSQR iteration                          */
-#define MLSQR_TCLASS_COUNT 6
+#define MLSQR_TCLASS_SWEEP_FN 6       /* level-0 pre-sweeps 1+2 (one fused kernel)    */
+#define MLSQR_TCLASS_SWEEP_PROLONG 7  /* level-0 prolongation + post-sweep 1          */
+#define MLSQR_TCLASS_SWEEP_LAST 8     /* level-0 plain sweep (last post-sweep)        */
+#define MLSQR_TCLASS_RESTRICT 9       /* level-0 residual + restriction               */
+#define MLSQR_TCLASS_HALO 10          /* z-slab ghost-plane exchanges (any stream)    */
+#define MLSQR_TCLASS_COLL 11          /* allgathers / allreduces of the decomposition */
+#define MLSQR_TCLASS_COUNT 12
 
 /* ---- z-slab decomposition (multi-GPU) ----------------------
  * A context can own a slab of a global 3D grid: every grid object created on it with z
@@ -311,6 +317,10 @@ int mlsqr_outer_create(mlsqr_op* op, int dims, size_t nx, size_t ny, size_t nz, 
                        const mlsqr_outer_cfg* cfg, mlsqr_outer** out);
 int mlsqr_outer_advance(mlsqr_outer* o, const double* g, const double* f_prev, double* f_out,
                      mlsqr_outer_step* step, int ptr_kind);
+/* the bidiagonalization of the last advanced step (BidiagEntries, krylov.hpp:62-67): alpha_1..,
+ * beta_1.. into host buffers of capacity cap_a / cap_b (NULL: count only) */
+int mlsqr_outer_last_bidiag(mlsqr_outer* o, double* alphas, size_t cap_a, double* betas, size_t cap_b,
+                            int* n_alphas, int* n_betas);
 int mlsqr_outer_destroy(mlsqr_outer* o);
 
 /* ---- R(f) (diffusion.cpp:89-101) on the device --------------------------- */

@@ -185,6 +185,8 @@ SIGNATURES = {
                                      C.c_double, C.POINTER(_OuterCfg), C.POINTER(C.c_void_p)]),
     "mlsqr_outer_advance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.POINTER(_OuterStep), C.c_int]),
+    "mlsqr_outer_last_bidiag": (C.c_int, [C.c_void_p, dp, C.c_size_t, dp, C.c_size_t, C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int)]),
     "mlsqr_outer_destroy": (C.c_int, [C.c_void_p]),
     "mlsqr_penalty_functional": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
                                            C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_double, dp]),
@@ -347,7 +349,8 @@ class LoopGroup:
             pass
 
 
-TCLASS = {"blur": 0, "dense": 1, "smooth": 2, "mg": 3, "update": 4, "iter": 5}
+TCLASS = {"blur": 0, "dense": 1, "smooth": 2, "mg": 3, "update": 4, "iter": 5, "sweep_fn": 6,
+          "sweep_prolong": 7, "sweep_last": 8, "restrict": 9, "halo": 10, "coll": 11}
 _default: Optional[Context] = None
 
 
@@ -959,8 +962,12 @@ class OuterSolver:
             op_ = C.c_void_p(f_out.ctypes.data)
         s = _OuterStep()
         _check(lib().mlsqr_outer_advance(self.h, gp, pp, op_, C.byref(s), kind))
+        cap = self._cfg.inner_cap + 2
+        al, be = np.zeros(cap), np.zeros(cap)
+        na, nb = C.c_int(), C.c_int()
+        _check(lib().mlsqr_outer_last_bidiag(self.h, _ptr(al), cap, _ptr(be), cap, C.byref(na), C.byref(nb)))
         return OuterStep(s.k, s.penalty_value, s.inner_iterations, s.final_residual,
-                         STOP_NAMES[s.inner_stop], s.eps_used, np.zeros(0), np.zeros(0))
+                         STOP_NAMES[s.inner_stop], s.eps_used, al[:na.value].copy(), be[:nb.value].copy())
 
     def __del__(self):
         try:

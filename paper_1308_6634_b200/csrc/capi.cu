@@ -754,6 +754,20 @@ int mlsqr_outer_advance(mlsqr_outer* o, const double* g, const double* f_prev, d
   });
 }
 
+int mlsqr_outer_last_bidiag(mlsqr_outer* o, double* alphas, size_t cap_a, double* betas, size_t cap_b,
+                            int* n_alphas, int* n_betas) {
+  return guard([&] {
+    require(o && n_alphas && n_betas, MLSQR_EINVAL, "outer_last_bidiag: null argument");
+    const OuterSolver& s = *o->impl;
+    const size_t na = (size_t)s.last_info.n_alphas, nb = (size_t)s.last_info.n_betas;
+    require((!alphas || cap_a >= na) && (!betas || cap_b >= nb), MLSQR_EDIM, "outer_last_bidiag: buffer too short");
+    if (alphas) std::memcpy(alphas, s.al_.data(), sizeof(double) * na);
+    if (betas) std::memcpy(betas, s.be_.data(), sizeof(double) * nb);
+    *n_alphas = (int)na;
+    *n_betas = (int)nb;
+  });
+}
+
 int mlsqr_outer_destroy(mlsqr_outer* o) {
   return guard([&] { delete o; });
 }

@@ -278,7 +278,10 @@ class DenseOp final : public Op {
       const int local = 8 / ctx->comm->size;
       gemvt_part_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, ctx->stream>>>(a_.p, y, rows, cols, part_.p, e.sx,
                                                                                  e.gate, local);
-      ctx->comm->allgather(part_.p, (size_t)local * cols, gath_.p, ctx->stream);
+      {
+        TimedRegion tc(ctx, MLSQR_TCLASS_COLL);
+        ctx->comm->allgather(part_.p, (size_t)local * cols, gath_.p, ctx->stream);
+      }
       gemvt_combine_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, ctx->stream>>>(gath_.p, cols, 8, x, a);
       ctx->count(2);
     } else {

@@ -280,15 +280,15 @@ struct Ctx {
 // scoped timing of one kernel class (CUDA events on the context stream)
 class TimedRegion {
  public:
-  TimedRegion(Ctx* c, int cls) : c_(c), cls_(cls) {
+  TimedRegion(Ctx* c, int cls, cudaStream_t s = nullptr) : c_(c), cls_(cls), s_(s ? s : c->stream) {
     if (!c_->timing || cls_ < 0) return;
     cudaEventCreate(&a_);
     cudaEventCreate(&b_);
-    cudaEventRecord(a_, c_->stream);
+    cudaEventRecord(a_, s_);
   }
   ~TimedRegion() {
     if (!c_->timing || cls_ < 0) return;
-    cudaEventRecord(b_, c_->stream);
+    cudaEventRecord(b_, s_);
     pending().push_back({a_, b_, cls_});
   }
   struct Pending {
@@ -302,9 +302,9 @@ class TimedRegion {
   static void collect(Ctx* c) {
     auto& p = pending();
     if (p.empty()) return;
-    cudaEventSynchronize(p.back().b);
     for (auto& e : p) {
       float ms = 0.f;
+      cudaEventSynchronize(e.b);  // (regions may sit on the side stream too)
       cudaEventElapsedTime(&ms, e.a, e.b);
       c->t_ms[e.cls] += ms;
       c->t_n[e.cls] += 1;
@@ -317,6 +317,7 @@ class TimedRegion {
  private:
   Ctx* c_;
   int cls_;
+  cudaStream_t s_;
   cudaEvent_t a_{}, b_{};
 };
 

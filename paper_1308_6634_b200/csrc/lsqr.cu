@@ -20,6 +20,8 @@
 //   K_U   f += phi/rho w; w <- v - theta/rho w; q <- p - theta/rho q + w.q segments
 //   [K_R  |g - A f| when S4 needs the exact residual (krylov.cpp:142-144)]
 //   F_i   trace row + stopping                                        (krylov.cpp:131-180)
+#include <cstdlib>
+
 #include "internal.cuh"
 #include "vec.cuh"
 
@@ -684,7 +686,12 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
 
   Runner r{op, pc, ws, tau, stop, ws->st.p, c, basis_dev, left_dev, snap_dev};
   const bool host_cb = pc && pc->host_callback();
-  const bool graph = use_graph && !host_cb && !c->timing && (!c->comm || c->comm->capturable());
+  // MLSQR_NO_GRAPH=1 replays the same launches eagerly (bisects a capture failure on a new path)
+  static const bool no_graph = [] {
+    const char* e = getenv("MLSQR_NO_GRAPH");
+    return e && e[0] && e[0] != '0';
+  }();
+  const bool graph = use_graph && !no_graph && !host_cb && !c->timing && (!c->comm || c->comm->capturable());
   r.init(g_dev);
   if (graph) {
     cudaGraph_t gr = nullptr;

@@ -47,7 +47,7 @@ OuterSolver::OuterSolver(Op* o, int dims, size_t nx, size_t ny, size_t nz, doubl
     vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, cfg.mg_levels, cfg.nu_pre, cfg.nu_post, cfg.omega,
                       cfg.coarse_sweeps);
   else  // a one-level V-cycle is the device holder of M; the SpdSolver is rebuilt from it per step
-    vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, 1, 1, 0, 1.0, 1);
+    vc_ = make_vcycle(o->ctx, dims, nx, ny, nz, h, 1, 1, 1, 1.0, 1);
   ws_ = workspace_new(o->ctx, o->rows, o->cols, o->data_shape, o->sol_shape, inner_.max_iters, op_guard(o));
   RowShape s{nx, ey * ez};
   const size_t J = s.segments(), G = dist_gather_size(o->ctx, J);

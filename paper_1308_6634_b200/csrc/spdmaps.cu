@@ -322,7 +322,7 @@ class InnerCgMap final : public Pc {
     n = (size_t)nx * ny * nz;
     S_ = RowShape{(size_t)nx, n / (size_t)nx};
     // snapshot of M (the reference moves the matrix into the solver, spdsolve.cpp:77-85)
-    m_ = make_vcycle(ctx, dims, (size_t)nx, (size_t)ny, (size_t)nz, h, 1, 1, 0, 1.0, 1);
+    m_ = make_vcycle(ctx, dims, (size_t)nx, (size_t)ny, (size_t)nz, h, 1, 1, 1, 1.0, 1);
     double e = 0.0;
     MLSQR_CUDA(cudaMemcpyAsync(&e, eps, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
     MLSQR_CUDA(cudaStreamSynchronize(ctx->stream));

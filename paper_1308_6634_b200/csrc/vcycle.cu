@@ -342,7 +342,10 @@ class VCycle final : public Pc {
       max_diag_kernel<<<grd, dim3(32, 8), 0, ctx->stream>>>(view(0), maxd_.p);
     }
     ctx->count();
-    if (ctx->sharded()) ctx->comm->allreduce_max_u64(maxd_.p, ctx->stream);  // order-free max
+    if (ctx->sharded()) {
+      TimedRegion tc(ctx, MLSQR_TCLASS_COLL);
+      ctx->comm->allreduce_max_u64(maxd_.p, ctx->stream);  // order-free max
+    }
     set_eps_kernel<<<1, 1, 0, ctx->stream>>>(maxd_.p, eps_cfg, mult(), (int)lv_.size(), eps_.p);
     ctx->count();
     coarsen_all();
@@ -474,6 +477,8 @@ class VCycle final : public Pc {
       cny = lv_[(size_t)l + 1].ny;
     }
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    TimedRegion tk(ctx, l != 0 ? -1 : MODE == kProlong ? MLSQR_TCLASS_SWEEP_PROLONG
+                                     : MODE == kNormal ? MLSQR_TCLASS_SWEEP_LAST : MLSQR_TCLASS_SWEEP_FN);
     const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
     if (dims_ == 3 && fits_i32(L))
@@ -490,6 +495,7 @@ class VCycle final : public Pc {
   void restrict_to(int l, const double* x, const double* b, const int* gate) {
     const Level& L = lv_[(size_t)l];
     Level& C = lv_[(size_t)l + 1];
+    TimedRegion tk(ctx, l == 0 ? MLSQR_TCLASS_RESTRICT : -1);
     const int zc = zm_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)((L.nz + zc - 1) / zc));
     if (dims_ == 3 && fits_i32(L))
@@ -566,6 +572,7 @@ class VCycle final : public Pc {
   void sweep_fn(int l, const double* b, double* out, double* seg, const int* gate) {
     const Level& L = lv_[(size_t)l];
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
+    TimedRegion tk(ctx, l == 0 ? MLSQR_TCLASS_SWEEP_FN : -1);
     if (dims_ == 2) {
       sweep_fn2d_kernel<<<row_grid(L.nx, L.ny), dim3(32, 8), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate);
       ctx->count();
@@ -603,7 +610,10 @@ class VCycle final : public Pc {
   // on the whole coarse grid, return this rank's slab of the (guarded, whole) coarse correction
   const double* coarse_solve(const double* b_local, const int* gate) {
     const Level& A = lv_[(size_t)la_];
-    ctx->comm->allgather(b_local, A.n, cb_.p, ctx->stream);
+    {
+      TimedRegion tc(ctx, MLSQR_TCLASS_COLL);
+      ctx->comm->allgather(b_local, A.n, cb_.p, ctx->stream);
+    }
     const double* xfull = coarse_->level(0, cb_.p, nullptr, nullptr, gate);
     ctx->count((int)cctx_->launches);  // the coarse kernels are this library's launches too
     cctx_->launches = 0;

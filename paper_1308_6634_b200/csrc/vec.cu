@@ -163,6 +163,7 @@ void halo_planes(Ctx* c, double* v, size_t plane, long nz_loc, int k, cudaStream
   if (!c->sharded() || k <= 0) return;
   require(nz_loc >= k, MLSQR_EDIM, "z slab thinner than the halo it must provide");
   const size_t cnt = plane * (size_t)k;
+  TimedRegion th(c, MLSQR_TCLASS_HALO, s);
   c->comm->halo(v, v + (size_t)(nz_loc - k) * plane, v - cnt, v + (size_t)nz_loc * plane, cnt, s);
 }
 
@@ -189,10 +190,16 @@ void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratc
     reduce3_kernel<<<(unsigned)K, 1024, 0, c->stream>>>(seg, nseg, scratch, gate);
     c->count();
     c->check_launch();
-    c->comm->allgather(scratch, K, gathered, c->stream);
+    {
+      TimedRegion tc(c, MLSQR_TCLASS_COLL);
+      c->comm->allgather(scratch, K, gathered, c->stream);
+    }
     reduce_segments(c, gathered, K * P, scratch, out, gate);
   } else {
-    c->comm->allgather(seg, nseg, gathered, c->stream);
+    {
+      TimedRegion tc(c, MLSQR_TCLASS_COLL);
+      c->comm->allgather(seg, nseg, gathered, c->stream);
+    }
     reduce_segments(c, gathered, nseg * P, scratch, out, gate);
   }
 }

@@ -794,7 +794,7 @@ RunSummary run_experiment(const ExperimentConfig& cfg, const fs::path& out_overr
     } else if (s.tau > 0.0) {
       // SparseSpd::identity: a holder with no edges and unit shift is I
       Pc m;
-      check(mlsqr_vcycle_create(ctx.h, b.dims, b.nx, b.ny, 1, b.h, 1, 1, 0, 1.0, 1, &m.h));
+      check(mlsqr_vcycle_create(ctx.h, b.dims, b.nx, b.ny, 1, b.h, 1, 1, 1, 1.0, 1, &m.h));
       check(mlsqr_vcycle_set_coefficients(m.h, zeros.data(), b.dims >= 2 ? zeros.data() : nullptr, nullptr, 1.0,
                                           MLSQR_HOST));
       check(mlsqr_krylov_basis(b.op.h, nullptr, m.h, s.tau, b.g.data(), k, vec.data(), &count, &exhausted,
