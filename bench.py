@@ -89,24 +89,42 @@ def canonical_bytes_per_iter(cfg) -> float:
 
 
 def class_bytes(cfg, world=1):
-    """Algorithmic bytes per launch of each timed kernel class (level-0 vectors, 8 B words)."""
+    """Algorithmic bytes per launch of each timed kernel class (level-0 vectors, 8 B words).
+    Single kernels: blur (K_A / K_B), dense (A x / A^T y), sweep_fn (pre-sweeps 1+2 fused),
+    sweep_prolong (prolongation + post-sweep 1), sweep_last (post-sweep 2 + <v, p> partials),
+    restrict (residual + restriction), update (K_U).  "smooth" is the class aggregate of the
+    three level-0 smoothing kernels (their mean bytes per launch)."""
     d = cfg["dims"]
     n = float(cfg["n"] ** d)
     r = 2.0 ** -d
-    if d >= 2:  # (z slabs fuse them too: the Krylov p the V-cycle receives is guarded)
-        # level-0 smoothing launches per V(2,2): fused first+second sweep (b + d coefficient arrays
-        # -> x), prolong+sweep (x, x_c, b, coefficients -> x), last sweep (x, b, coefficients -> x)
-        sweep_words = [(1 + d) + 1, (3 + d + r), (3 + d)]
-    else:
-        # 1D: first-from-zero, normal, prolong+sweep, normal
-        sweep_words = [(2 + d), (3 + d), (3 + d + r), (3 + d)]
     m = float(cfg["ns"] * cfg["nd"]) if cfg.get("kind") == "fdot" else n
+    fn = (1 + d) + 1          # b + d coefficient arrays -> x
+    pro = 3 + d + r           # x, x_c, b, coefficients -> x
+    last = 3 + d              # x, b, coefficients -> x
     return {
         "dense": 8.0 * (m * n + n + 2 * m),        # A x (or A^T y): the matrix once + the vectors
         "blur": 8.0 * 3 * n,                       # read x, read old, write out (m = n)
-        "smooth": 8.0 * n * sum(sweep_words) / len(sweep_words),  # average per level-0 launch
+        "sweep_fn": 8.0 * n * fn,
+        "sweep_prolong": 8.0 * n * pro,
+        "sweep_last": 8.0 * n * last,
+        "restrict": 8.0 * n * (2 + d + r),         # x, b, coefficients -> b_c
+        "smooth": 8.0 * n * (fn + pro + last) / 3,
         "update": 8.0 * 8 * n,                     # read f w q v p, write f w q
     }
+
+
+SINGLE_KERNELS = ("dense", "blur", "sweep_fn", "sweep_prolong", "sweep_last", "restrict", "update")
+
+
+def measured_dram_per_iter():
+    """DRAM bytes per LSQR iteration (dram__bytes_read.sum + dram__bytes_write.sum summed over a
+    bench launch list, divided by its iterations) from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "dram_per_iter.json")) as fh:
+            t = json.load(fh)
+        return t["bytes_per_iter"], t["source"]
+    except Exception:
+        return None, None
 
 
 def measured_traffic(kernel_class):
@@ -333,7 +351,9 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for torch's input set-up, the library and the timing events
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ctx = mb.Context(local, stream=stream.cuda_stream)
     n = cfg["n"]
     h = 1.0 / n
@@ -419,7 +439,7 @@ def main():
     # strong scaling: all ranks iterate the same global problem, count it once
     value = iters / (ms / 1000.0)
 
-    # ---- instrumented step: per-kernel-class CUDA-event durations (eager launches)
+    # ---- instrumented step: per-kernel CUDA-event durations (eager launches, same stream)
     ctx.set_timing(True)
     one_step()
     torch.cuda.synchronize()
@@ -428,17 +448,44 @@ def main():
     # this rank's share: z slabs split everything; row shards split only the dense operator
     cb = {k: v / world if (not dense or k == "dense") else v for k, v in class_bytes(cfg, world).items()}
     peak, peak_src = peaks()
-    cands = {k: cls_ms[k] for k in ("dense", "blur", "smooth", "update") if cls_ms[k][1] > 0}
+    # roofline: the single kernel with the largest summed time in the step (not a class average)
+    cands = {k: cls_ms[k] for k in SINGLE_KERNELS if cls_ms[k][1] > 0}
     dom = max(cands, key=lambda k: cands[k][0])
     dms, dn = cands[dom]
     achieved = cb[dom] * dn / (dms / 1000.0) / 1e9 if dms > 0 else None
-    it_ms = cls_ms["iter"][0] / max(1, cls_ms["iter"][1])
+    n_iter = max(1, cls_ms["iter"][1])
+    it_ms = cls_ms["iter"][0] / n_iter
     traffic, traffic_src = measured_traffic(dom) if world == 1 and args.config == "c5" else (None, None)
-    per_class = {k: {"ms_per_launch": v[0] / v[1], "algorithmic_bytes": cb[k],
-                     "achieved_gbs": cb[k] / (v[0] / v[1] / 1e3) / 1e9,
+    per_class = {k: {"ms_per_launch": v[0] / v[1], "launches": v[1], "share_of_iter": v[0] / max(cls_ms["iter"][0], 1e-9),
+                     "algorithmic_bytes": cb[k], "achieved_gbs": cb[k] / (v[0] / v[1] / 1e3) / 1e9,
                      "frac": cb[k] / (v[0] / v[1] / 1e3) / 1e9 / peak}
-                 for k, v in cands.items() if v[1] > 0}
+                 for k, v in cls_ms.items() if k in cb and v[1] > 0}
+    comm = {k: {"ms_per_iter": cls_ms[k][0] / n_iter, "calls_per_iter": cls_ms[k][1] / n_iter}
+            for k in ("halo", "coll")} if world > 1 else None
     b_iter = canonical_bytes_per_iter(cfg)
+    dram_iter, dram_src = measured_dram_per_iter() if world == 1 and args.config == "c5" else (None, None)
+
+    # ---- cross-N fingerprint: outer step 1 from f^0 = 0 (the step tests/golden/config_<cfg>.npz pins
+    #      against the oracle), bitwise digest of alpha / beta and the whole f (slabs gathered)
+    from paper_1308_6634_b200 import dist as pdist
+    f0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    f1 = torch.empty_like(f0)
+    s1 = solver.step(g_d, f0, f1)
+    torch.cuda.synchronize()
+    digest = pdist.step_digest(dist, f1, s1.alphas, s1.betas, rank, world, row_shards=dense)
+    del f0, f1
+    if digest is not None:
+        fx = os.path.join(ROOT, "tests", "golden", f"config_{args.config}.npz")
+        if os.path.exists(fx):
+            import hashlib
+            z = np.load(fx)
+            digest["oracle_fixture"] = os.path.relpath(fx, ROOT)
+            digest["matches_oracle_fixture"] = bool(
+                str(z["s0_f_sha256"]) == digest["f_sha256"]
+                and hashlib.sha256(np.ascontiguousarray(z["s0_alphas"], "<f8").tobytes()).hexdigest()
+                == digest["alphas_sha256"]
+                and hashlib.sha256(np.ascontiguousarray(z["s0_betas"], "<f8").tobytes()).hexdigest()
+                == digest["betas_sha256"])
 
     # ---- e2e through the public API with host (pinned) buffers
     e2e = None
@@ -476,7 +523,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_rate(cfg, 1, 0, "1 thread (the reference is single-threaded)")
+            # N >= 3 timed iterations after one warm-up iteration
+            r = cpu_reference_rate(cfg, 3, 1, "1 thread (the reference is single-threaded)")
             cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "reference", "sample": r["sample"]}
         except Exception as e:  # never fail the bench line on the baseline leg
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
@@ -501,12 +549,18 @@ def main():
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": cb[dom], "traffic_source": traffic_src,
                          "peak_source": peak_src,
-                         "note": "algorithmic bytes per launch / mean CUDA-event launch time, instrumented step"},
+                         "note": "the single kernel with the largest summed time in an instrumented step: "
+                                 "algorithmic bytes per launch / mean CUDA-event launch time"},
             "iteration_roofline": {"bytes_per_iter": b_iter, "model": "SURVEY.md 8d canonical B_iter",
                                    "achieved_gbs": b_iter * value / world / 1e9,
-                                   "frac": b_iter * value / world / 1e9 / peak},
+                                   "frac": b_iter * value / world / 1e9 / peak,
+                                   "measured_dram_bytes_per_iter": dram_iter,
+                                   "measured_dram_frac": (dram_iter * value / world / 1e9 / peak) if dram_iter else None,
+                                   "measured_dram_source": dram_src},
             "kernel_classes_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in cls_ms.items()},
             "class_rooflines": per_class,
+            "comm": comm,
+            "digest_outer_step1": digest,
             "instrumented_ms_per_iter": it_ms,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -252,6 +252,7 @@ int mlsqr_ctx_set_slab(mlsqr_ctx* ctx, size_t nz_global, size_t z_offset) {
   return guard([&] {
     require(z_offset < nz_global, MLSQR_EINVAL, "slab offset outside the global grid");
     ctx->impl.row_mode = false;
+    ctx->impl.decomposed = true;
     ctx->impl.nzg = (long)nz_global;
     ctx->impl.zoff = (long)z_offset;
   });
@@ -261,6 +262,7 @@ int mlsqr_ctx_set_row_shard(mlsqr_ctx* ctx, size_t rows_global, size_t row_offse
   return guard([&] {
     require(row_offset < rows_global, MLSQR_EINVAL, "row shard offset outside the data space");
     ctx->impl.row_mode = true;
+    ctx->impl.decomposed = true;
     ctx->impl.rows_g = (long)rows_global;
     ctx->impl.row0 = (long)row_offset;
   });

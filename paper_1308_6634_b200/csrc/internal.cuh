@@ -231,10 +231,15 @@ struct Ctx {
   // preconditioner are replicated (so sharded() -- the z-slab predicate -- is false)
   bool row_mode = false;
   long row0 = 0, rows_g = 0;
-  bool sharded() const { return comm != nullptr && comm->size > 1 && !row_mode; }
-  bool row_sharded() const { return comm != nullptr && comm->size > 1 && row_mode; }
+  // an explicit mlsqr_ctx_set_slab / _set_row_shard runs the decomposed code path even on a
+  // one-rank communicator (ghost exchanges with no neighbours, one-rank collectives): that is
+  // how the NCCL transport and the sharded graph are exercised on a single GPU
+  bool decomposed = false;
+  bool multi() const { return comm != nullptr && (comm->size > 1 || decomposed); }
+  bool sharded() const { return multi() && !row_mode; }
+  bool row_sharded() const { return multi() && row_mode; }
   // data-space reductions span ranks in both decompositions
-  bool data_distributed() const { return comm != nullptr && comm->size > 1; }
+  bool data_distributed() const { return multi(); }
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   uint64_t launches = 0;

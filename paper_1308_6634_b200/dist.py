@@ -42,14 +42,49 @@ def broadcast_unique_id(dist, rank: int) -> bytes:
 
 def sharded_context(device: int, rank: int, world: int, nz_global: int, unique_id: bytes,
                     stream=None):
-    """Context of rank `rank` owning its slab of a global grid with nz_global planes."""
+    """Context of rank `rank` owning its slab of a global grid with nz_global planes, over NCCL.
+    At world 1 the slab is the whole grid, and the decomposed code path still runs (ghost
+    exchanges without neighbours, one-rank NCCL collectives inside the captured graph)."""
     import paper_1308_6634_b200 as mb
     ctx = mb.Context(device, stream=stream)
     z0, _ = slab_plan(nz_global, world)[rank]
-    if world > 1:
-        ctx.set_comm_nccl(unique_id, rank, world)
-        ctx.set_slab(nz_global, z0)
+    ctx.set_comm_nccl(unique_id, rank, world)
+    ctx.set_slab(nz_global, z0)
     return ctx
+
+
+def step_digest(dist, f_local, alphas, betas, rank: int, world: int, row_shards: bool = False) -> dict | None:
+    """Bitwise fingerprint of one outer step, comparable across GPU counts (bench.py prints it
+    at every N, so N = 1 vs N = 8 equality can be read from the driver's records).
+
+    f_local: this rank's slab of the iterate (a torch tensor; z slabs are equal-sized and
+    concatenate in rank order) or, with row shards, the replicated solution (rank 0's copy
+    is hashed).  alphas / betas are replicated on every rank.  Returns the digest on rank 0,
+    None elsewhere."""
+    import hashlib
+
+    import torch
+
+    if dist is not None and world > 1 and not row_shards:
+        if f_local.is_cuda:  # NCCL: all_gather into rank-ordered slabs
+            parts = [torch.empty_like(f_local) for _ in range(world)]
+            dist.all_gather(parts, f_local)
+        else:  # gloo
+            parts = [torch.empty_like(f_local) for _ in range(world)] if rank == 0 else None
+            dist.gather(f_local, parts, dst=0)
+        if rank != 0:
+            return None
+        f = torch.cat(parts)
+    else:
+        if rank != 0:
+            return None
+        f = f_local
+    fh = np.ascontiguousarray(f.detach().cpu().numpy(), dtype="<f8")
+    a = np.ascontiguousarray(alphas, dtype="<f8")
+    b = np.ascontiguousarray(betas, dtype="<f8")
+    return {"f_sha256": hashlib.sha256(fh.tobytes()).hexdigest(), "f_l2": float(np.sqrt(np.dot(fh, fh))),
+            "alphas_sha256": hashlib.sha256(a.tobytes()).hexdigest(),
+            "betas_sha256": hashlib.sha256(b.tobytes()).hexdigest(), "n_alphas": int(a.size)}
 
 
 # ---------------------------------------------------------------------------

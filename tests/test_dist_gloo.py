@@ -76,6 +76,15 @@ def _worker(rank, world, port, q):
             sl = slice(rank * L * rows_loc, (rank + 1) * L * rows_loc)
             segs = pdist.segments(xg[sl], yg[sl], L)
             res[name] = (pdist.dist_reduce(segs, allgather), xg.tobytes(), yg.tobytes(), L)
+        # 5. the bench's cross-N fingerprint: slabs gathered in rank order hash like the whole
+        #    vector, and alpha / beta hash identically on every rank
+        import torch
+        whole = np.random.default_rng(5).standard_normal(world * 1000)
+        ab = np.random.default_rng(6).standard_normal(51)
+        dg = pdist.step_digest(dist, torch.from_numpy(whole[rank * 1000:(rank + 1) * 1000].copy()), ab[:50], ab,
+                               rank, world)
+        res["digest"] = dg
+        res["digest_whole"] = pdist.step_digest(None, torch.from_numpy(whole), ab[:50], ab, 0, 1)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -95,6 +104,10 @@ def test_world2_gloo(orc):
     for r in range(2):
         res = out[r]
         assert res["plans_equal"] and res["covered"] and res["uid_ok"] and res["halo_ok"]
+        if r == 0:
+            assert res["digest"] == res["digest_whole"]
+        else:
+            assert res["digest"] is None
         for name in ("unaligned", "aligned"):
             val, xb, yb, L = res[name]
             x = np.frombuffer(xb)

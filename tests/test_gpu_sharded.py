@@ -145,22 +145,56 @@ def test_block_aligned_reduction_path_bit_exact():
     assert np.array_equal(np.concatenate([o.solution for o in out]), ref.solution)
 
 
-def test_nccl_world1_transport_loads_and_solves():
+def test_nccl_world1_transport_runs_the_sharded_graph():
     """The NCCL transport on one GPU: dlopen + ncclGetUniqueId + ncclCommInitRank through the
-    C-ABI, then a solve on that context (world 1 = unsharded, so results equal the plain
-    context's).  N > 1 needs one GPU per rank; the loopback tests above run the same
-    Comm-interface call sequence bit-exact."""
+    C-ABI, then the DECOMPOSED code path on a one-rank communicator (mlsqr_ctx_set_slab makes the
+    context sharded even at P = 1): guarded vectors, ghost exchanges (NCCL group calls with no
+    peers), reduce3 + ncclAllGather of the tree partials, ncclAllReduce(max) for eps, coarse-level
+    agglomeration -- all inside the captured CUDA graph.  The result must equal the plain
+    context's bit for bit.  N > 1 needs one GPU per rank (tools/nccl_parity.py)."""
     from paper_1308_6634_b200 import dist as pdist
     uid = mb.nccl_unique_id()
     assert isinstance(uid, bytes) and len(uid) == 128
-    ctx = pdist.sharded_context(0, 0, 1, 32, uid)
-    shape = (32, 32, 32)
-    taps = mb.gaussian_taps(32, 2.0 / 32, 4)
-    g = np.random.default_rng(1).uniform(-1, 1, 32 ** 3)
-    st = mb.StoppingConfig.max_iterations(5)
-    a = mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps, ctx=ctx), mb.IdentityMap(g.size, ctx=ctx), g, 1e-2, st)
-    b = mb.mlsqr(mb.SeparableGaussianBlur(shape, taps=taps), mb.IdentityMap(g.size), g, 1e-2, st)
+    n = 32
+    shape = (n, n, n)
+    ctx = pdist.sharded_context(0, 0, 1, n, uid)
+    taps = mb.gaussian_taps(n, 2.0 / n, 4)
+    rng = np.random.default_rng(1)
+    g = rng.uniform(-1, 1, n ** 3)
+    cfg = mb.OuterConfig(tau=5e-3, penalty=mb.PenaltySpec("tv", 0.05), inner_stop=mb.StoppingConfig.max_iterations(8),
+                         inner_cap=8, rel_decrease_threshold=0.0, max_outer=2, mg_levels=3)
+    ctx.set_timing(True)
+    a = mb.solve_nonlinear(mb.SeparableGaussianBlur(shape, taps=taps, ctx=ctx), g, shape, 1.0 / n, cfg)
+    halo, coll = ctx.timing(mb.TCLASS["halo"]), ctx.timing(mb.TCLASS["coll"])
+    ctx.set_timing(False)
+    b = mb.solve_nonlinear(mb.SeparableGaussianBlur(shape, taps=taps), g, shape, 1.0 / n, cfg)
+    assert halo[1] > 0 and coll[1] > 0, (halo, coll)  # the exchanges and collectives really ran
     assert np.array_equal(a.solution, b.solution)
+    for sa, sb in zip(a.steps, b.steps):
+        assert np.array_equal(sa.alphas, sb.alphas) and sa.eps_used == sb.eps_used
+    # and with graph capture (timing off): the same bits
+    c = mb.solve_nonlinear(mb.SeparableGaussianBlur(shape, taps=taps, ctx=ctx), g, shape, 1.0 / n, cfg)
+    assert np.array_equal(c.solution, b.solution)
+
+
+def test_nccl_world1_row_shard_dense():
+    """C4's row-shard path on a one-rank NCCL communicator: A^T u allgathers the canonical chunk
+    partials through ncclAllGather; bit-identical to the plain context."""
+    uid = mb.nccl_unique_id()
+    ctx = mb.Context(0)
+    ctx.set_comm_nccl(uid, 0, 1)
+    m, n = 256, 8 ** 3
+    ctx.set_row_shard(m, 0)
+    a = np.random.default_rng(4).standard_normal((m, n))
+    g = a @ np.random.default_rng(5).standard_normal(n)
+    vc_s = mb.VCycleMap((8, 8, 8), 1 / 8, 2, ctx=ctx)
+    vc_s.update(np.zeros(n), mb.PenaltySpec.tikhonov())
+    vc = mb.VCycleMap((8, 8, 8), 1 / 8, 2)
+    vc.update(np.zeros(n), mb.PenaltySpec.tikhonov())
+    st = mb.StoppingConfig.max_iterations(10)
+    r1 = mb.mlsqr(mb.DenseOperator(a, sol_row_len=8, ctx=ctx), vc_s, g, 1e-3, st)
+    r2 = mb.mlsqr(mb.DenseOperator(a, sol_row_len=8), vc, g, 1e-3, st)
+    assert np.array_equal(r1.solution, r2.solution) and np.array_equal(r1.betas, r2.betas)
 
 
 # ---------------------------------------------------------------------------
