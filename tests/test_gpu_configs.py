@@ -1,11 +1,13 @@
 """BASELINE.json configurations at their real sizes.
 
 * C1 (128^2, 1 x 50): the whole configuration, bit-exact against the oracle.
-* C2 (1024^2) and C3 (128^3): the first lagged-diffusivity outer step, bit-exact
-  (the oracle takes seconds per outer step there).
+* C2 (1024^2, 5 x 30) and C3 (128^3, 5 x 40): every outer step of the whole configuration, bit-exact
+  against the oracle run here.
 * C4 (fDOT 64^3, 4096 rows = 8.6 GB) and C5 (512^3): size-independent properties at
   full size -- adjointness, a symmetric positive V-cycle, constants annihilated by M,
-  bitwise determinism, a monotone damped residual -- plus a reduced C4 bit-exact run.
+  bitwise determinism, a monotone damped residual -- plus a reduced C4 bit-exact run, and
+  the full-size runs bit-exact against offline oracle fixtures (tests/golden/config_c4.npz:
+  all 8 outer steps; config_c5.npz: the first 2 outer steps).
 """
 import numpy as np
 import pytest
@@ -164,3 +166,91 @@ def test_c5_full_size_properties(ctx):
     assert torch.equal(r1.solution, r2.solution) and np.array_equal(r1.betas, r2.betas)
     res = [t.res_damped for t in r1.trace]
     assert all(res[i + 1] <= res[i] * (1 + 1e-12) for i in range(len(res) - 1))
+
+
+# ---------------------------------------------------------------------------
+# C4 / C5 at their BASELINE sizes against offline oracle fixtures
+# (tests/golden/make_config_golden.py: the oracle's device-order restatement of the fixed-count
+#  lagged-diffusivity loop, outer.cpp:58-96 with krylov.cpp:335-440 inside, on bench.py's inputs)
+# ---------------------------------------------------------------------------
+def _fixture(name):
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", f"config_{name}.npz")
+    if not os.path.exists(p):
+        pytest.fail(f"missing fixture {p}: run tests/golden/make_config_golden.py {name}")
+    return np.load(p)
+
+
+def _sha(v):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(v, dtype="<f8").tobytes()).hexdigest()
+
+
+def _check_steps(torch, solver, g, N, z, K):
+    """K outer steps from f^0 = 0 through OuterSolver; each must equal the fixture bit for bit."""
+    I = int(z["inner"])
+    fa = torch.zeros(N, dtype=torch.float64, device="cuda")
+    fb = torch.empty_like(fa)
+    for k in range(K):
+        s = solver.step(g, fa, fb)
+        fa, fb = fb, fa
+        assert s.inner_iterations == int(z[f"s{k}_iters"]) == I, (k, s.inner_iterations)
+        assert s.eps_used == float(z[f"s{k}_eps"]), (k, s.eps_used, float(z[f"s{k}_eps"]))
+        assert np.array_equal(s.alphas[:I], z[f"s{k}_alphas"]), f"step {k}: alpha sequence differs"
+        assert np.array_equal(s.betas[:I + 1], z[f"s{k}_betas"]), f"step {k}: beta sequence differs"
+        assert s.penalty_value == float(z[f"s{k}_R"]), (k, s.penalty_value, float(z[f"s{k}_R"]))
+        fh = fa.cpu().numpy()
+        stride = int(z[f"s{k}_f_stride"])
+        assert np.array_equal(fh[::stride][:z[f"s{k}_f_samples"].size], z[f"s{k}_f_samples"]), f"step {k}: f samples"
+        assert _sha(fh) == str(z[f"s{k}_f_sha256"]), f"step {k}: iterate digest differs"
+        del fh
+
+
+def test_c5_first_outer_steps_bit_exact(ctx):
+    """C5 (512^3, the north-star gate config) at full size: the first outer steps x 50 MLSQR
+    iterations -- eps, R(f), alpha[50], beta[51] and the whole iterate -- bit-exact against the
+    oracle fixture.  Exercises the size-dependent schedule only 512^3 has: the blur's persistent
+    item split, the z-march chunking and the 64-bit element-index paths."""
+    torch = pytest.importorskip("torch")
+    from bench import CONFIGS, make_problem
+    z = _fixture("c5")
+    cfg = CONFIGS["c5"]
+    shape, taps, f_true, zn = make_problem(mb, cfg)
+    N = int(np.prod(shape))
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    af = op.apply(torch.from_numpy(f_true).cuda())
+    del f_true
+    g = af + cfg["noise"] * float(af.abs().max()) * torch.from_numpy(zn).cuda()
+    del af, zn
+    assert _sha(g.cpu().numpy()) == str(z["g_sha256"]), "input g differs from the fixture's"
+    ocfg = mb.OuterConfig(tau=cfg["tau"], penalty=mb.PenaltySpec(cfg["pen"], cfg["T"]),
+                          inner_stop=mb.StoppingConfig.max_iterations(cfg["I"]), inner_cap=cfg["I"],
+                          rel_decrease_threshold=0.0, max_outer=cfg["K"], mg_levels=cfg["levels"])
+    solver = mb.OuterSolver(op, shape, 1.0 / cfg["n"], ocfg)
+    _check_steps(torch, solver, g, N, z, int(z["outer_steps"]))
+
+
+def test_c4_full_config_bit_exact(ctx):
+    """C4 (fDOT 64^3 x 4096 rows, 8.6 GB matrix formed on the device) at full size: every outer
+    step of the fixture bit-exact against the oracle."""
+    torch = pytest.importorskip("torch")
+    from bench import CONFIGS
+    z = _fixture("c4")
+    cfg = CONFIGS["c4"]
+    n = cfg["n"]
+    shape = (n, n, n)
+    N = n ** 3
+    lo, hi = cfg["semi"]
+    vlo, vhi = cfg["vals"]
+    f_true = mb.phantom_ellipsoids3d(n, n, n, cfg["count"], lo, hi, vlo, vhi, cfg["seed"])
+    op = mb.FdotOperator(n, cfg["ns"], cfg["nd"], mu=cfg["mu"], seed=cfg["seed"])
+    m = cfg["ns"] * cfg["nd"]
+    af = op.apply(torch.from_numpy(f_true).cuda())
+    zn = mb.gaussian_noise(cfg["seed"] + 1000, m, 1.0)
+    g = af + cfg["noise"] * float(af.abs().max()) * torch.from_numpy(zn).cuda()
+    assert _sha(g.cpu().numpy()) == str(z["g_sha256"]), "input g differs from the fixture's"
+    ocfg = mb.OuterConfig(tau=cfg["tau"], penalty=mb.PenaltySpec(cfg["pen"], cfg["T"]),
+                          inner_stop=mb.StoppingConfig.max_iterations(cfg["I"]), inner_cap=cfg["I"],
+                          rel_decrease_threshold=0.0, max_outer=cfg["K"], mg_levels=cfg["levels"])
+    solver = mb.OuterSolver(op, shape, 1.0 / n, ocfg)
+    _check_steps(torch, solver, g, N, z, int(z["outer_steps"]))

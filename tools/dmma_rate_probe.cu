@@ -18,8 +18,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // DF: DFMA instructions per DMMA issued by the same warp (independent chains)
 template <int CH, int LD, int DF>
 __global__ void probe(double* out, long long* cyc, double s) {
-  __shared__ double sm[8192];
-  for (int i = threadIdx.x; i < 8192; i += blockDim.x) sm[i] = 1.0 + 1e-9 * i;
+  __shared__ double sm[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = 1.0 + 1e-9 * i;
   __syncthreads();
   double d[2 * CH];
 #pragma unroll
@@ -32,7 +32,7 @@ __global__ void probe(double* out, long long* cyc, double s) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       double a = a0;
-      if (LD == 1 || (LD == 2 && (c & 1) == 0)) a = p[((it * CH + c) * 256) & 8191];
+      if (LD == 1 || (LD == 2 && (c & 1) == 0)) a = p[((it * CH + c) * 256) & 4095];
       dmma(d[2 * c], d[2 * c + 1], a, s);
 #pragma unroll
       for (int q = 0; q < DF; ++q) f[q & 3] = fma(f[q & 3], s, 1e-12);
