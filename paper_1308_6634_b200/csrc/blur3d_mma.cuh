@@ -32,6 +32,13 @@
 // Shared-memory pitches are chosen for conflict-free 8-byte fragment loads: a half-warp reads
 // 4 rows x 4 (x pass) or 4 rows x 4 columns (y pass), so row pitches are = 4 (mod 16) doubles.
 
+#ifndef MLSQR_B3M_NIN
+#define MLSQR_B3M_NIN 4
+#endif
+#ifndef MLSQR_B3M_NXS
+#define MLSQR_B3M_NXS 3
+#endif
+
 template <int R>
 struct B3M {
   static constexpr int NT = 2 * R + 1;
@@ -49,26 +56,18 @@ struct B3M {
   static constexpr int KS = (8 + 2 * R + 3) / 4;               // k-steps per 8x8 tile
   static constexpr int MT = (H + 7) / 8;                       // x-pass row tiles (per x warp)
   static constexpr int XP = 36;                                // xs pitch (= 4 mod 16)
-  static constexpr int SQP = 34;
-  static constexpr int OP = 32;
-  static constexpr int NIN = 4;    // input-plane ring (TMA, x warps)
-  static constexpr int NOLD = 4;   // old-tile ring (TMA, y warps)
-  static constexpr int NXS = 3;    // x-result ring (x warps -> y warps)
-  static constexpr int TREE_WARP = XWARPS + YWARPS - 1;
+  static constexpr int NIN = MLSQR_B3M_NIN;  // input-plane ring (TMA, x warps)
+  static constexpr int NXS = MLSQR_B3M_NXS;  // x-result ring (x warps -> y warps)
   // the x pass of the last row tile reads up to 8 * MT - H rows past the tile: keep them inside
   static constexpr int IN_SLOT = ((8 * MT) * P + 15) / 16 * 16;
-  static constexpr int OLD_DOUBLES = TX * TY;
   static constexpr int XS_DOUBLES = H * XP;
-  static constexpr int SQ_DOUBLES = TY * SQP;
-  static constexpr int NBARS = NIN + NOLD + 2 * NXS;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)NIN * IN_SLOT + (size_t)NOLD * OLD_DOUBLES +
-                                                   (size_t)NXS * XS_DOUBLES + 2 * SQ_DOUBLES) +
-                                 NBARS * sizeof(unsigned long long);
+  static constexpr int NBARS = NIN + 2 * NXS;
+  static constexpr size_t SMEM =
+      sizeof(double) * ((size_t)NIN * IN_SLOT + (size_t)NXS * XS_DOUBLES) + NBARS * sizeof(unsigned long long);
   static constexpr unsigned IN_BYTES = H * P * 8u;
-  static constexpr unsigned OLD_BYTES = TX * TY * 8u;
   static_assert(P % 2 == 0 && P >= W + XOFF && P <= 256, "TMA box width");
   static_assert(XOFF + 24 + 4 * KS <= P, "x-pass window inside the row");
-  static_assert(8 * 3 + 4 * KS <= H, "y-pass window inside the x results (even R)");
+  static_assert(TY == 4 * YWARPS && TX == 32, "y warps: lane = tile column, 4 tile rows per warp");
   static_assert(MT <= 6, "x-pass chains per x warp");
   static_assert(XREGS * 32 * XWARPS + YREGS * 32 * YWARPS <= (65536 / THREADS / 8 * 8) * THREADS, "register split");
 };
@@ -132,26 +131,21 @@ template <int R, bool OLD, bool SEG>
 __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
     blur3d_mma(const double* __restrict__ in, double* __restrict__ out, int nx, int ny, int nz, int tiles_x,
                int tiles, int zchunk, int items, int zoff, int nzg, int zshift, Taps taps, EpiArgs e,
-               const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_old) {
+               const __grid_constant__ CUtensorMap map_in) {
   using C = B3M<R>;
   if (e.gate && *e.gate == 0) return;
   if ((int)blockIdx.x >= items) return;
   extern __shared__ __align__(128) double sm[];
   double* tin = sm;                                // [NIN][IN_SLOT]  rows of pitch P
-  double* olds = tin + C::NIN * C::IN_SLOT;        // [NOLD][TY][TX]
-  double* xs = olds + C::NOLD * C::OLD_DOUBLES;    // [NXS][H][XP]
-  double* sq = xs + C::NXS * C::XS_DOUBLES;        // [2][TY][SQP]
-  unsigned long long* tfull = reinterpret_cast<unsigned long long*>(sq + 2 * C::SQ_DOUBLES);
-  unsigned long long* ofull = tfull + C::NIN;
-  unsigned long long* xfull = ofull + C::NOLD;
+  double* xs = tin + C::NIN * C::IN_SLOT;          // [NXS][H][XP]
+  unsigned long long* tfull = reinterpret_cast<unsigned long long*>(xs + C::NXS * C::XS_DOUBLES);
+  unsigned long long* xfull = tfull + C::NIN;
   unsigned long long* xempty = xfull + C::NXS;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < C::NIN; ++s) mbar_init(tfull + s, 1);
-#pragma unroll
-    for (int s = 0; s < C::NOLD; ++s) mbar_init(ofull + s, 1);
 #pragma unroll
     for (int s = 0; s < C::NXS; ++s) {
       mbar_init(xfull + s, 32 * C::XWARPS);
@@ -175,7 +169,7 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
     const int xa_off = (lane >> 2) * C::P + C::XOFF + 8 * warp + (lane & 3);
     const int xd_off = (lane >> 2) * C::XP + 8 * warp + 2 * (lane & 3);
     // input-plane issue cursor (warp 0, lane 0's issues take effect)
-    B3Cursor ic;
+    B3Cursor ic{};
     unsigned issued = 0;
     auto issue_in = [&]() {
       if (ic.item >= items) return;
@@ -202,17 +196,17 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
 #pragma unroll 1
       for (int s = 0; s < C::NIN; ++s) issue_in();
     }
-    unsigned k = 0;  // planes done (input slots and x-result buffers, in sequence)
+    unsigned si = 0, pi = 0, sb = 0, pb = 1;  // ring positions (slot, parity) of the next plane; x-result
+                                              // slots start free (parity 1 passes on a fresh barrier)
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
       it.set(item, tiles, tiles_x, zchunk, nz);
       const int nplanes = it.z1 - it.z0 + 2 * R;
 #pragma unroll 1
-      for (int j = 0; j < nplanes; ++j, ++k) {
-        const unsigned si = k % C::NIN, sb = k % C::NXS;
-        mbar_wait(tfull + si, (k / C::NIN) & 1u);
-        mbar_wait(xempty + sb, ((k / C::NXS) & 1u) ^ 1u);  // first pass: free
+      for (int j = 0; j < nplanes; ++j) {
+        mbar_wait(tfull + si, pi);
+        mbar_wait(xempty + sb, pb);
         const double* tile = tin + si * C::IN_SLOT + xa_off;
         double d[C::MT][2];
 #pragma unroll
@@ -230,101 +224,84 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
         for (int i = 0; i < C::MT; ++i)
           if (8 * i + (lane >> 2) < C::H) *reinterpret_cast<double2*>(xw + 8 * i * C::XP) = make_double2(d[i][0], d[i][1]);
         mbar_arrive(xfull + sb);
-        named_bar(1, 32 * C::XWARPS);  // every x warp is done with input slot si
+        if (++si == C::NIN) {
+          si = 0;
+          pi ^= 1u;
+        }
+        if (++sb == C::NXS) {
+          sb = 0;
+          pb ^= 1u;
+        }
+        named_bar(1, 32 * C::XWARPS);  // every x warp is done with the input slot
         if (warp == 0) issue_in();
       }
     }
   } else {
-    // =================== y warps: Y = T' X, z accumulators, epilogue, |out|^2 partials
+    // =================== y warps: lane = tile column, warp yw = tile rows 4 yw .. 4 yw + 3
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::YREGS));
     const int yw = warp - C::XWARPS;
     const size_t nxy = (size_t)nx * ny;
     const size_t chunks = (size_t)(nx + 31) / 32;
     const double so = OLD && e.so ? *e.so : 1.0;
     const double coef = OLD ? *e.coef : 0.0;
-    // y tiles of warp yw: row tile yw/2, column tiles 2 (yw%2) + {0, 1}; this thread's outputs are
-    // row yr, columns yc + {0, 1} and yc + 8 + {0, 1}
-    const int yr = 8 * (yw >> 1) + (lane >> 2), yc = 16 * (yw & 1) + 2 * (lane & 3);
-    const int yb_off = (8 * (yw >> 1) + (lane & 3)) * C::XP + 16 * (yw & 1) + (lane >> 2);
-    // old-tile issue cursor over the CTA's outputs (y warp 0, lane 0)
-    B3Cursor oc;
-    unsigned oissued = 0;
-    auto issue_old = [&]() {
-      if (!OLD || oc.item >= items) return;
-      const unsigned st = oissued % C::NOLD;
-      tma_issue_pred(lane == 0, ofull + st, C::OLD_BYTES, olds + st * C::OLD_DOUBLES, &map_old, oc.it.x0, oc.it.y0,
-                     oc.q);
-      ++oissued;
-      if (++oc.q > oc.hi) {
-        oc.item += gridDim.x;
-        if (oc.item < items) {
-          oc.it.set(oc.item, tiles, tiles_x, zchunk, nz);
-          oc.q = oc.it.z0;
-          oc.hi = oc.it.z1 - 1;
-        }
-      }
-    };
-    if (OLD && yw == 0) {
-      oc.item = blockIdx.x;
-      oc.it.set(oc.item, tiles, tiles_x, zchunk, nz);
-      oc.q = oc.it.z0;
-      oc.hi = oc.it.z1 - 1;
-#pragma unroll 1
-      for (int s = 0; s < C::NOLD; ++s) issue_old();
-    }
+    const int r0 = 4 * yw;
+    // butterfly row-segment tree (SEG): the row this lane's final value belongs to
+    const int trow = r0 + ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1);
     double acc[4][C::NT];
-    unsigned k = 0;   // planes consumed (x-result buffers)
-    unsigned ko = 0;  // outputs emitted (old-tile slots)
+    unsigned sb = 0, ph = 0;  // x-result ring position (slot, parity) of the next plane
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
       it.set(item, tiles, tiles_x, zchunk, nz);
       const int z0 = it.z0, z1 = it.z1;
       const int zlo = z0 - R, zhi = z1 + R - 1;
-      const int gx = it.x0 + yc, gy = it.y0 + yr;
-      const bool rowok = gy < ny;
-      const bool ok0 = rowok && gx < nx, ok1 = rowok && gx + 1 < nx, ok2 = rowok && gx + 8 < nx,
-                 ok3 = rowok && gx + 9 < nx;
-      double* const obase = out + (size_t)gy * nx + gx;
-      auto tree = [&](int zt) {  // canonical segment partials of output plane zt (tree warp)
-        const int gyt = it.y0 + lane;
-        if (gyt < ny) {
-          const double* rr = sq + (zt & 1) * C::SQ_DOUBLES + lane * C::SQP;
-          double v[32];
+      const int gx = it.x0 + lane, gy = it.y0 + r0;
+      const bool colok = gx < nx;
+      bool ok[4];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const double2 qv = *reinterpret_cast<const double2*>(rr + 2 * j);
-            v[2 * j] = qv.x;
-            v[2 * j + 1] = qv.y;
-          }
-          e.seg[((size_t)zt * ny + gyt) * chunks + it.bx] = tree32_serial(v);
-        }
+      for (int c = 0; c < 4; ++c) ok[c] = colok && gy + c < ny;
+      // running pointers: the next output plane's row gy, the next old plane to load, the next
+      // segment partial of this lane's tree row
+      const size_t first = ((size_t)z0 * ny + gy) * nx + gx;
+      double* orow = out + first;
+      const double* oold = OLD ? e.old + first : nullptr;
+      double* segp = SEG ? e.seg + ((size_t)z0 * ny + it.y0 + trow) * chunks + it.bx : nullptr;
+      const size_t segstep = (size_t)ny * chunks;
+      const bool segok = it.y0 + trow < ny && (lane & 7) == 0;
+      // old-vector values of the next output plane, loaded one plane ahead
+      double on[4] = {0.0, 0.0, 0.0, 0.0};
+      auto load_old = [&]() {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (ok[c]) on[c] = __ldcg(oold + (size_t)c * nx);
+        oold += nxy;
       };
+      if (OLD) load_old();
 #pragma unroll 1
       for (int pb = zlo; pb <= zhi; pb += C::NT) {
 #pragma unroll
         for (int u = 0; u < C::NT; ++u) {
           const int p = pb + u;
-          if (p <= zhi) {  // block-uniform
-            const unsigned sb = k % C::NXS;
-            mbar_wait(xfull + sb, (k / C::NXS) & 1u);
-            const double* xb = xs + sb * C::XS_DOUBLES + yb_off;
-            double b0[C::KS], b1[C::KS];
+          if (p <= zhi) {  // warp-uniform
+            mbar_wait(xfull + sb, ph);
+            const double* xb = xs + sb * C::XS_DOUBLES + r0 * C::XP + lane;
+            double b[4 + 2 * R];
 #pragma unroll
-            for (int q = 0; q < C::KS; ++q) {
-              b0[q] = xb[4 * q * C::XP];
-              b1[q] = xb[4 * q * C::XP + 8];
+            for (int j = 0; j < 4 + 2 * R; ++j) b[j] = xb[j * C::XP];
+            mbar_arrive(xempty + sb);  // the x results are in registers
+            if (++sb == C::NXS) {
+              sb = 0;
+              ph ^= 1u;
             }
-            double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+            // ---- y pass: ascending fma chain over the 2R+1 rows of each output
+            double yv[4];
 #pragma unroll
-            for (int q = 0; q < C::KS; ++q) {
-              dmma8844(y0, y1, tq[q], b0[q]);
-              dmma8844(y2, y3, tq[q], b1[q]);
+            for (int c = 0; c < 4; ++c) {
+              yv[c] = 0.0;
+#pragma unroll
+              for (int s = 0; s < C::NT; ++s) yv[c] = fma(taps.t[s <= R ? s : 2 * R - s], b[c + s], yv[c]);
             }
-            mbar_arrive(xempty + sb);  // the fragments are consumed (the DMMAs read them)
-            ++k;
             // ---- z pass: output zo' = p - R + j takes tap 2R - j; slot (u + j) % NT
-            const double yv[4] = {y0, y1, y2, y3};
 #pragma unroll
             for (int j = 0; j < C::NT; ++j) {
               const int s = (u + j) % C::NT;
@@ -333,48 +310,42 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
               for (int c = 0; c < 4; ++c) acc[c][s] = fma(t, yv[c], j == C::NT - 1 ? 0.0 : acc[c][s]);
             }
             const int zo = p - R;
-            const bool emit = zo >= z0;  // (zo <= zhi - R = z1 - 1 always)
-            if (emit) {
-              double v0 = ok0 ? acc[0][u] : 0.0, v1 = ok1 ? acc[1][u] : 0.0;
-              double v2 = ok2 ? acc[2][u] : 0.0, v3 = ok3 ? acc[3][u] : 0.0;
+            if (zo >= z0) {  // (zo <= zhi - R = z1 - 1 always)
+              double v[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) v[c] = ok[c] ? acc[c][u] : 0.0;
               if (OLD) {
-                const unsigned so_ = ko % C::NOLD;
-                mbar_wait(ofull + so_, (ko / C::NOLD) & 1u);
-                const double* po = olds + so_ * C::OLD_DOUBLES + yr * C::OP + yc;
-                const double2 o0 = *reinterpret_cast<const double2*>(po);
-                const double2 o1 = *reinterpret_cast<const double2*>(po + 8);
-                if (ok0) v0 = v0 + coef * (o0.x * so);
-                if (ok1) v1 = v1 + coef * (o0.y * so);
-                if (ok2) v2 = v2 + coef * (o1.x * so);
-                if (ok3) v3 = v3 + coef * (o1.y * so);
+                double o[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) o[c] = on[c];
+                if (zo + 1 < z1) load_old();
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                  if (ok[c]) v[c] = v[c] + coef * (o[c] * so);
               }
-              ++ko;
-              double* orow = obase + (size_t)zo * nxy;
-              if (ok1) {
-                *reinterpret_cast<double2*>(orow) = make_double2(v0, v1);
-              } else if (ok0) {
-                orow[0] = v0;
-              }
-              if (ok3) {
-                *reinterpret_cast<double2*>(orow + 8) = make_double2(v2, v3);
-              } else if (ok2) {
-                orow[8] = v2;
-              }
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                if (ok[c]) orow[(size_t)c * nx] = v[c];
+              orow += nxy;
               if (SEG) {
-                double* ps = sq + (zo & 1) * C::SQ_DOUBLES + yr * C::SQP + yc;
-                *reinterpret_cast<double2*>(ps) = make_double2(v0 * v0, v1 * v1);
-                *reinterpret_cast<double2*>(ps + 8) = make_double2(v2 * v2, v3 * v3);
+                // tree32 of each row's 32 squares (v[l] += v[l + off], off = 16 .. 1) as a
+                // butterfly: every level halves the live values per lane, the pairs are tree32's
+                const bool hi16 = lane & 16, hi8 = lane & 8;
+                const double q0 = v[0] * v[0], q1 = v[1] * v[1], q2 = v[2] * v[2], q3 = v[3] * v[3];
+                // level 16: lanes < 16 keep rows 0 / 2, lanes >= 16 rows 1 / 3
+                const double a = (hi16 ? q1 : q0) + __shfl_xor_sync(0xffffffffu, hi16 ? q0 : q1, 16);
+                const double c2 = (hi16 ? q3 : q2) + __shfl_xor_sync(0xffffffffu, hi16 ? q2 : q3, 16);
+                // level 8: lanes with bit 3 clear keep a's row, the others c2's row
+                double w = (hi8 ? c2 : a) + __shfl_xor_sync(0xffffffffu, hi8 ? a : c2, 8);
+                w = w + __shfl_xor_sync(0xffffffffu, w, 4);
+                w = w + __shfl_xor_sync(0xffffffffu, w, 2);
+                w = w + __shfl_xor_sync(0xffffffffu, w, 1);
+                if (segok) *segp = w;
+                segp += segstep;
               }
             }
-            if (SEG && warp == C::TREE_WARP && zo - 1 >= z0) tree(zo - 1);
-            if (SEG || OLD) named_bar(2, 32 * C::YWARPS);  // |out|^2 of zo published; old slot free
-            if (OLD && emit && yw == 0) issue_old();
           }
         }
-      }
-      if (SEG) {  // the last output plane's partials
-        if (warp == C::TREE_WARP) tree(z1 - 1);
-        named_bar(2, 32 * C::YWARPS);
       }
     }
   }
@@ -410,14 +381,12 @@ static bool launch_b3m(Ctx* c, const double* in, double* out, int nx, int ny, in
   const bool sh = c->sharded();
   const int zoff = sh ? (int)c->zoff : 0, nzg = sh ? (int)c->nzg : nz;
   const int zshift = sh ? R : 0;
-  CUtensorMap mi{}, mo{};
-  bool tma = tensor_map3d(&mi, in - (size_t)zshift * nx * ny, nx, ny, nz + 2 * zshift, C::P, C::H);
-  if (tma && a.old) tma = tensor_map3d(&mo, a.old, nx, ny, nz, C::TX, C::TY);
-  if (!tma) return false;
+  CUtensorMap mi{};
+  if (!tensor_map3d(&mi, in - (size_t)zshift * nx * ny, nx, ny, nz + 2 * zshift, C::P, C::H)) return false;
   auto k = a.old ? (a.seg ? blur3d_mma<R, true, true> : blur3d_mma<R, true, false>)
                  : (a.seg ? blur3d_mma<R, false, true> : blur3d_mma<R, false, false>);
   k<<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, tiles, zck, items, zoff, nzg, zshift, t, a,
-                                              mi, mo);
+                                              mi);
   c->count();
   return true;
 }
