@@ -1,54 +1,56 @@
-// blur3d_mma.cuh -- the fused 3D blur with its x and y passes on the FP64 tensor cores
-// (included by blur.cu after blur3d_pipe.cuh, whose TMA / mbarrier helpers it reuses).
+// blur3d_mma.cuh -- the fused 3D blur: x pass on the FP64 tensor cores, y / z passes and the
+// LSQR epilogue on the FP64 CUDA cores (included by blur.cu after blur3d_pipe.cuh, whose TMA /
+// mbarrier helpers it reuses).
 //
-// Same canonical DEVICE order as blur3d_pipe (per output an ascending fma chain along x, then y,
-// then z), but the x and y passes are banded-Toeplitz GEMMs issued as `mma.sync.m8n8k4.f64`:
-// tools/dmma_probe.cu shows the FP64 MMA rounds exactly like fma(a3,b3,fma(a2,b2,fma(a1,b1,
-// fma(a0,b0,c)))), i.e. an ascending fma chain over k, so a k-loop over the source window in
-// ascending order reproduces the scalar chain bit for bit (taps outside an output's band are
-// zero: fma(0, x, acc) == acc, up to the sign of an exact zero).
+// Canonical DEVICE order (the oracle's): per output an ascending fma chain along x, then y, then z.
+//  x pass: banded-Toeplitz GEMM X[r][o] = sum_s In[r][s] T[s][o], T[s][o] = t[s - o], issued as
+//    `mma.sync.m8n8k4.f64` with tap fragments tq[q] = t[4q + lane%4 - lane/4] (zero outside [0, 2R]);
+//    tools/dmma_probe.cu shows the FP64 MMA rounds exactly like an ascending fma chain over k, so
+//    the k-loop over the source window reproduces the scalar chain bit for bit.
+//  y pass: 2R+1-long DFMA chains down a column (lane = tile column), the DMMA's band would waste a
+//    third of the pipe there;  z pass: 2R+1 running accumulators per output (independent DFMAs).
 //
-//  x pass (plane p+1):  X[r][o] = sum_s In[r][s] T[s][o],   T[s][o] = t[s - o]   (H x 32 outputs)
-//  y pass (plane p):    Y[r][o] = sum_u T'[r][u] X[u][o],   T'[r][u] = t[u - r]  (32 x 32 outputs)
-// Both use the same per-lane tap fragments tq[q] = t[4q + (lane & 3) - (lane >> 2)] (zero
-// outside [0, 2R]).  An m8n8 output tile takes ceil((8 + 2R) / 4) k-steps.
-//  z pass: running accumulators; each thread owns the two outputs of its y-pass fragment,
-//  Y[r0 + lane/4][o0 + 2 (lane % 4) + {0, 1}], of warp w's tile (r0, o0) = (8 (w / 4), 8 (w % 4)),
-//  so every value stays in the registers of the thread that sums it.
-//
-// Schedule (FP64-pipe and shared-memory bound, tools/dmma_mix_probe.cu: DMMA and DFMA share one
-// 64 FMA/cycle/SM pipe; a DMMA holds it 4 SM cycles):
-//  * a continuous TMA ring over all of a CTA's items: ring slot r holds input plane q (the r-th of
-//    the CTA's plane sequence) and the old-vector tile of output plane q - R - 1, so the phase that
-//    runs the x pass of q also emits that output and frees the whole slot.  Slot r is issued right
-//    after the barrier that ends the phase consuming slot r - NSTAGE, i.e. NSTAGE - 1 phases ahead
-//    of its use, across item boundaries.  One predicated thread issues it (no branch, so no reconvergence
-//    barrier in the other warps); the z coordinate of a plane outside the (global) grid is moved
-//    out of the tensor map's bounds, so the hardware zero-fills it and no pass tests planes;
-//  * phase p loads the y-pass fragments of plane p (published by the last barrier) before it
-//    writes the x-pass results of plane p+1, so the y chain and the x chains interleave;
-//  * every thread waits on the slot's mbarrier itself (no single-warp poll + broadcast);
-//  * the epilogue variants (old vector / |out|^2 partials) are template parameters.
+// Warp roles (tools/dmma_mix_probe.cu: DMMA and DFMA share one 64 FMA/cycle/SM pipe, so the
+// roles are sized to keep it fed from every SMSP):
+//  * x warps, XG groups of four taking alternate planes: TMA ring of input planes (TMA zero-fills
+//    the box outside the grid; a plane outside the global grid is loaded from far outside the
+//    tensor map), DMMA x pass into an x-result ring (full / empty mbarriers).  Group warp w does
+//    row tiles MTH (w / 2) + {0 .. MTH-1} and column tiles 2 (w % 2) + {0, 1}, whose A fragments
+//    overlap in KS - 2 of KS k-steps;
+//  * y warps (4 tile rows each): y pass and z accumulators; each z-complete output plane goes to an
+//    output ring;
+//  * epilogue warps (8 tile rows each): out = v + coef (old so) with the old vector streamed into
+//    each thread's own shared-memory slots by cp.async three planes ahead, the stores, and the
+//    |out|^2 row-segment partials as a register butterfly (tree32's pairs, no shared memory).
+// Only the rings couple the roles, so a role waits for another only when a ring runs empty / full.
 // Shared-memory pitches are chosen for conflict-free 8-byte fragment loads: a half-warp reads
-// 4 rows x 4 (x pass) or 4 rows x 4 columns (y pass), so row pitches are = 4 (mod 16) doubles.
+// 4 rows x 4 doubles (x pass), so the input row pitch is = 4 (mod 16) doubles.
 
+#ifndef MLSQR_B3M_XG
+#define MLSQR_B3M_XG 2
+#endif
 #ifndef MLSQR_B3M_NIN
 #define MLSQR_B3M_NIN 4
 #endif
 #ifndef MLSQR_B3M_NXS
-#define MLSQR_B3M_NXS 3
+#define MLSQR_B3M_NXS 4
 #endif
 
 template <int R>
 struct B3M {
   static constexpr int NT = 2 * R + 1;
   static constexpr int TX = 32, TY = 32;
-  static constexpr int XWARPS = 4;                 // warpgroup 0: x pass (producer)
-  static constexpr int YWARPS = 8;                 // warpgroups 1-2: y / z passes + epilogue (consumers)
-  static constexpr int THREADS = 32 * (XWARPS + YWARPS);
-  // setmaxnreg split of the launch allocation (384 x 168 = 64512): 128 x 88 + 256 x 208 = 64512 --
-  // an increase beyond what the decrease released would block forever
-  static constexpr int XREGS = 88, YREGS = 208;
+  static constexpr int XG = MLSQR_B3M_XG;          // x groups (4 warps each) taking alternate planes
+  static constexpr int XWARPS = 4 * XG;            // x pass
+  static constexpr int YR = 4;                     // tile rows per y warp (outputs per y thread)
+  static constexpr int YWARPS = TY / YR;           // y and z passes
+  static constexpr int ER = 8;                     // tile rows per epilogue warp
+  static constexpr int EWARPS = TY / ER;           // epilogue: old vector, stores, |out|^2 segment trees
+  static constexpr int THREADS = 32 * (XWARPS + YWARPS + EWARPS);
+  // setmaxnreg split of the launch allocation (XG 1: 512 x 128 = 65536, XG 2: 640 x 96 = 61440):
+  // an increase beyond what the decreases released would block forever
+  static constexpr int XREGS = XG == 1 ? 88 : 80, EREGS = XG == 1 ? 80 : 72;
+  static constexpr int YREGS = XG == 1 ? 168 : 120;
   static constexpr int W = TX + 2 * R;
   static constexpr int H = TY + 2 * R;
   static constexpr int XOFF = R & 1;           // TMA boxes start at an even x (see B3P)
@@ -61,15 +63,21 @@ struct B3M {
   // the x pass of the last row tile reads up to 8 * MT - H rows past the tile: keep them inside
   static constexpr int IN_SLOT = ((8 * MT) * P + 15) / 16 * 16;
   static constexpr int XS_DOUBLES = H * XP;
-  static constexpr int NBARS = NIN + 2 * NXS;
-  static constexpr size_t SMEM =
-      sizeof(double) * ((size_t)NIN * IN_SLOT + (size_t)NXS * XS_DOUBLES) + NBARS * sizeof(unsigned long long);
+  static constexpr int NV = 4;                                 // z-complete output ring (y -> epilogue warps)
+  static constexpr int V_DOUBLES = TY * TX;
+  static constexpr int NOLD = 4;  // epilogue threads' own old-vector slots (cp.async, NOLD - 1 planes ahead)
+  static constexpr int OLD_DOUBLES = NOLD * TY * TX;
+  static constexpr int NBARS = NIN + 2 * NXS + 2 * NV;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)NIN * IN_SLOT + (size_t)NXS * XS_DOUBLES +
+                                                   (size_t)NV * V_DOUBLES + OLD_DOUBLES) +
+                                 NBARS * sizeof(unsigned long long);
   static constexpr unsigned IN_BYTES = H * P * 8u;
   static_assert(P % 2 == 0 && P >= W + XOFF && P <= 256, "TMA box width");
   static_assert(XOFF + 24 + 4 * KS <= P, "x-pass window inside the row");
-  static_assert(TY == 4 * YWARPS && TX == 32, "y warps: lane = tile column, 4 tile rows per warp");
-  static_assert(MT <= 6, "x-pass chains per x warp");
-  static_assert(XREGS * 32 * XWARPS + YREGS * 32 * YWARPS <= (65536 / THREADS / 8 * 8) * THREADS, "register split");
+  static_assert((XG == 1 || (XG == 2 && NIN % 2 == 0 && NXS % 2 == 0)) && TX == 32 && TY == 32, "roles");
+  static_assert(MT <= 6 && KS + 2 <= 7, "x-pass chains and A fragments per x warp");
+  static_assert(XREGS * 32 * XWARPS + YREGS * 32 * YWARPS + EREGS * 32 * EWARPS <= (65536 / THREADS / 8 * 8) * THREADS,
+                "register split");
 };
 
 // (not volatile: a pure function of its operands, so independent chains may interleave)
@@ -138,9 +146,13 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
   extern __shared__ __align__(128) double sm[];
   double* tin = sm;                                // [NIN][IN_SLOT]  rows of pitch P
   double* xs = tin + C::NIN * C::IN_SLOT;          // [NXS][H][XP]
-  unsigned long long* tfull = reinterpret_cast<unsigned long long*>(xs + C::NXS * C::XS_DOUBLES);
+  double* vs = xs + C::NXS * C::XS_DOUBLES;        // [NV][TY][TX]  z-complete outputs
+  double* olds = vs + C::NV * C::V_DOUBLES;        // [NOLD][ER][EWARPS * 32]  old vector, per thread
+  unsigned long long* tfull = reinterpret_cast<unsigned long long*>(olds + C::OLD_DOUBLES);
   unsigned long long* xfull = tfull + C::NIN;
   unsigned long long* xempty = xfull + C::NXS;
+  unsigned long long* vfull = xempty + C::NXS;
+  unsigned long long* vempty = vfull + C::NV;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -148,8 +160,13 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
     for (int s = 0; s < C::NIN; ++s) mbar_init(tfull + s, 1);
 #pragma unroll
     for (int s = 0; s < C::NXS; ++s) {
-      mbar_init(xfull + s, 32 * C::XWARPS);
+      mbar_init(xfull + s, 128);  // one x group writes a plane
       mbar_init(xempty + s, 32 * C::YWARPS);
+    }
+#pragma unroll
+    for (int s = 0; s < C::NV; ++s) {
+      mbar_init(vfull + s, 32 * C::YWARPS);
+      mbar_init(vempty + s, 32 * C::EWARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -166,19 +183,18 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
     // =================== x warps: X[r][o] for all H rows of column tile `warp`
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::XREGS));
     const double sx = e.sx ? *e.sx : 1.0;  // x * 1.0 == x: no scale is exact
-    const int xa_off = (lane >> 2) * C::P + C::XOFF + 8 * warp + (lane & 3);
-    const int xd_off = (lane >> 2) * C::XP + 8 * warp + 2 * (lane & 3);
-    // input-plane issue cursor (warp 0, lane 0's issues take effect)
+    // x warp w: row tiles MTH (w / 2) + {0 .. MTH-1}, column tiles 2 (w % 2) + {0, 1}; the two column
+    // tiles share the A fragments of KS - 2 of their KS k-steps (KP = KS + 2 loads per row tile)
+    constexpr int MTH = (C::MT + 1) / 2, KP = C::KS + 2;
+    const int grp = warp >> 2, role = warp & 3;  // x group, and the warp's tiles within the plane
+    const int xg = role >> 1, xh = role & 1;
+    const int xa_off = (8 * MTH * xg + (lane >> 2)) * C::P + C::XOFF + 16 * xh + (lane & 3);
+    const int xd_off = (8 * MTH * xg + (lane >> 2)) * C::XP + 16 * xh + 2 * (lane & 3);
+    // the CTA's plane sequence (all items, planes z0 - R .. z1 + R - 1 each); x group grp runs the
+    // planes k = grp (mod XG), its role-0 warp refills their input slots (lane 0's issues take effect)
     B3Cursor ic{};
-    unsigned issued = 0;
-    auto issue_in = [&]() {
+    auto advance = [&]() {
       if (ic.item >= items) return;
-      const int q = ic.q;
-      const bool real = q + zoff >= 0 && q + zoff < nzg;
-      const unsigned st = issued % C::NIN;
-      tma_issue_pred(lane == 0, tfull + st, C::IN_BYTES, tin + st * C::IN_SLOT, &map_in, ic.it.x0 - R - C::XOFF,
-                     ic.it.y0 - R, real ? q + zshift : -(1 << 20));
-      ++issued;
       if (++ic.q > ic.hi) {
         ic.item += gridDim.x;
         if (ic.item < items) {
@@ -188,95 +204,92 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
         }
       }
     };
-    if (warp == 0) {
+    auto issue_in = [&](unsigned kq) {  // the cursor's plane, sequence index kq
+      if (ic.item >= items) return;
+      const int q = ic.q;
+      const bool real = q + zoff >= 0 && q + zoff < nzg;
+      const unsigned st = kq % C::NIN;
+      tma_issue_pred(lane == 0, tfull + st, C::IN_BYTES, tin + st * C::IN_SLOT, &map_in, ic.it.x0 - R - C::XOFF,
+                     ic.it.y0 - R, real ? q + zshift : -(1 << 20));
+    };
+    unsigned kis = grp;  // sequence index of the next plane this group issues
+    if (role == 0) {
       ic.item = blockIdx.x;
       ic.it.set(ic.item, tiles, tiles_x, zchunk, nz);
       ic.q = ic.it.z0 - R;
       ic.hi = ic.it.z1 + R - 1;
+      if (C::XG == 2 && grp) advance();
 #pragma unroll 1
-      for (int s = 0; s < C::NIN; ++s) issue_in();
+      for (int s = 0; s < C::NIN / C::XG; ++s) {
+        issue_in(kis);
+        kis += C::XG;
+#pragma unroll
+        for (int g = 0; g < C::XG; ++g) advance();
+      }
     }
-    unsigned si = 0, pi = 0, sb = 0, pb = 1;  // ring positions (slot, parity) of the next plane; x-result
-                                              // slots start free (parity 1 passes on a fresh barrier)
+    unsigned k = 0;  // sequence index of the current plane
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
       it.set(item, tiles, tiles_x, zchunk, nz);
       const int nplanes = it.z1 - it.z0 + 2 * R;
 #pragma unroll 1
-      for (int j = 0; j < nplanes; ++j) {
-        mbar_wait(tfull + si, pi);
-        mbar_wait(xempty + sb, pb);
+      for (int j = 0; j < nplanes; ++j, ++k) {
+        if (C::XG == 2 && (int)(k & 1u) != grp) continue;
+        const unsigned si = k % C::NIN, sb = k % C::NXS;
+        mbar_wait(tfull + si, (k / C::NIN) & 1u);
+        mbar_wait(xempty + sb, ((k / C::NXS) & 1u) ^ 1u);  // x-result slots start free
         const double* tile = tin + si * C::IN_SLOT + xa_off;
-        double d[C::MT][2];
+        auto live = [&](int i) { return C::MT % 2 == 0 || MTH * xg + i < C::MT; };  // warp-uniform
+        double a[MTH][KP];
 #pragma unroll
-        for (int i = 0; i < C::MT; ++i) d[i][0] = d[i][1] = 0.0;
+        for (int i = 0; i < MTH; ++i)
+          if (live(i)) {
 #pragma unroll
-        for (int q = 0; q < C::KS; ++q) {
-          double a[C::MT];
+            for (int q = 0; q < KP; ++q) a[i][q] = tile[8 * i * C::P + 4 * q] * sx;
+          }
+        double d[MTH][2][2];
 #pragma unroll
-          for (int i = 0; i < C::MT; ++i) a[i] = tile[8 * i * C::P + 4 * q] * sx;
+        for (int i = 0; i < MTH; ++i) d[i][0][0] = d[i][0][1] = d[i][1][0] = d[i][1][1] = 0.0;
 #pragma unroll
-          for (int i = 0; i < C::MT; ++i) dmma8844(d[i][0], d[i][1], a[i], tq[q]);
-        }
+        for (int q = 0; q < C::KS; ++q)
+#pragma unroll
+          for (int i = 0; i < MTH; ++i)
+            if (live(i)) {
+              dmma8844(d[i][0][0], d[i][0][1], a[i][q], tq[q]);
+              dmma8844(d[i][1][0], d[i][1][1], a[i][q + 2], tq[q]);
+            }
         double* xw = xs + sb * C::XS_DOUBLES + xd_off;
 #pragma unroll
-        for (int i = 0; i < C::MT; ++i)
-          if (8 * i + (lane >> 2) < C::H) *reinterpret_cast<double2*>(xw + 8 * i * C::XP) = make_double2(d[i][0], d[i][1]);
+        for (int i = 0; i < MTH; ++i)
+          if (live(i) && 8 * (MTH * xg + i) + (lane >> 2) < C::H) {
+            *reinterpret_cast<double2*>(xw + 8 * i * C::XP) = make_double2(d[i][0][0], d[i][0][1]);
+            *reinterpret_cast<double2*>(xw + 8 * i * C::XP + 8) = make_double2(d[i][1][0], d[i][1][1]);
+          }
         mbar_arrive(xfull + sb);
-        if (++si == C::NIN) {
-          si = 0;
-          pi ^= 1u;
+        named_bar(1 + grp, 128);  // the group's four warps are done with the input slot
+        if (role == 0) {
+          issue_in(kis);
+          kis += C::XG;
+#pragma unroll
+          for (int g = 0; g < C::XG; ++g) advance();
         }
-        if (++sb == C::NXS) {
-          sb = 0;
-          pb ^= 1u;
-        }
-        named_bar(1, 32 * C::XWARPS);  // every x warp is done with the input slot
-        if (warp == 0) issue_in();
       }
     }
-  } else {
+  } else if (warp < C::XWARPS + C::YWARPS) {
     // =================== y warps: lane = tile column, warp yw = tile rows 4 yw .. 4 yw + 3
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::YREGS));
-    const int yw = warp - C::XWARPS;
-    const size_t nxy = (size_t)nx * ny;
-    const size_t chunks = (size_t)(nx + 31) / 32;
-    const double so = OLD && e.so ? *e.so : 1.0;
-    const double coef = OLD ? *e.coef : 0.0;
-    const int r0 = 4 * yw;
-    // butterfly row-segment tree (SEG): the row this lane's final value belongs to
-    const int trow = r0 + ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1);
-    double acc[4][C::NT];
+    constexpr int YR = C::YR;
+    const int r0 = YR * (warp - C::XWARPS);
+    double acc[YR][C::NT];
     unsigned sb = 0, ph = 0;  // x-result ring position (slot, parity) of the next plane
+    unsigned vb = 0, vp = 1;  // output ring position of the next output plane (slots start free)
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
       it.set(item, tiles, tiles_x, zchunk, nz);
       const int z0 = it.z0, z1 = it.z1;
       const int zlo = z0 - R, zhi = z1 + R - 1;
-      const int gx = it.x0 + lane, gy = it.y0 + r0;
-      const bool colok = gx < nx;
-      bool ok[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) ok[c] = colok && gy + c < ny;
-      // running pointers: the next output plane's row gy, the next old plane to load, the next
-      // segment partial of this lane's tree row
-      const size_t first = ((size_t)z0 * ny + gy) * nx + gx;
-      double* orow = out + first;
-      const double* oold = OLD ? e.old + first : nullptr;
-      double* segp = SEG ? e.seg + ((size_t)z0 * ny + it.y0 + trow) * chunks + it.bx : nullptr;
-      const size_t segstep = (size_t)ny * chunks;
-      const bool segok = it.y0 + trow < ny && (lane & 7) == 0;
-      // old-vector values of the next output plane, loaded one plane ahead
-      double on[4] = {0.0, 0.0, 0.0, 0.0};
-      auto load_old = [&]() {
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (ok[c]) on[c] = __ldcg(oold + (size_t)c * nx);
-        oold += nxy;
-      };
-      if (OLD) load_old();
 #pragma unroll 1
       for (int pb = zlo; pb <= zhi; pb += C::NT) {
 #pragma unroll
@@ -285,18 +298,18 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
           if (p <= zhi) {  // warp-uniform
             mbar_wait(xfull + sb, ph);
             const double* xb = xs + sb * C::XS_DOUBLES + r0 * C::XP + lane;
-            double b[4 + 2 * R];
+            double b[YR + 2 * R];
 #pragma unroll
-            for (int j = 0; j < 4 + 2 * R; ++j) b[j] = xb[j * C::XP];
+            for (int j = 0; j < YR + 2 * R; ++j) b[j] = xb[j * C::XP];
             mbar_arrive(xempty + sb);  // the x results are in registers
             if (++sb == C::NXS) {
               sb = 0;
               ph ^= 1u;
             }
             // ---- y pass: ascending fma chain over the 2R+1 rows of each output
-            double yv[4];
+            double yv[YR];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < YR; ++c) {
               yv[c] = 0.0;
 #pragma unroll
               for (int s = 0; s < C::NT; ++s) yv[c] = fma(taps.t[s <= R ? s : 2 * R - s], b[c + s], yv[c]);
@@ -307,44 +320,128 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
               const int s = (u + j) % C::NT;
               const double t = taps.t[(2 * R - j) <= R ? 2 * R - j : j];
 #pragma unroll
-              for (int c = 0; c < 4; ++c) acc[c][s] = fma(t, yv[c], j == C::NT - 1 ? 0.0 : acc[c][s]);
+              for (int c = 0; c < YR; ++c) acc[c][s] = fma(t, yv[c], j == C::NT - 1 ? 0.0 : acc[c][s]);
             }
-            const int zo = p - R;
-            if (zo >= z0) {  // (zo <= zhi - R = z1 - 1 always)
-              double v[4];
+            if (p - R >= z0) {  // output p - R is complete (p - R <= z1 - 1 always): hand it over
+              mbar_wait(vempty + vb, vp);
+              double* vw = vs + vb * C::V_DOUBLES + r0 * C::TX + lane;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) v[c] = ok[c] ? acc[c][u] : 0.0;
-              if (OLD) {
-                double o[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) o[c] = on[c];
-                if (zo + 1 < z1) load_old();
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                  if (ok[c]) v[c] = v[c] + coef * (o[c] * so);
-              }
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (ok[c]) orow[(size_t)c * nx] = v[c];
-              orow += nxy;
-              if (SEG) {
-                // tree32 of each row's 32 squares (v[l] += v[l + off], off = 16 .. 1) as a
-                // butterfly: every level halves the live values per lane, the pairs are tree32's
-                const bool hi16 = lane & 16, hi8 = lane & 8;
-                const double q0 = v[0] * v[0], q1 = v[1] * v[1], q2 = v[2] * v[2], q3 = v[3] * v[3];
-                // level 16: lanes < 16 keep rows 0 / 2, lanes >= 16 rows 1 / 3
-                const double a = (hi16 ? q1 : q0) + __shfl_xor_sync(0xffffffffu, hi16 ? q0 : q1, 16);
-                const double c2 = (hi16 ? q3 : q2) + __shfl_xor_sync(0xffffffffu, hi16 ? q2 : q3, 16);
-                // level 8: lanes with bit 3 clear keep a's row, the others c2's row
-                double w = (hi8 ? c2 : a) + __shfl_xor_sync(0xffffffffu, hi8 ? a : c2, 8);
-                w = w + __shfl_xor_sync(0xffffffffu, w, 4);
-                w = w + __shfl_xor_sync(0xffffffffu, w, 2);
-                w = w + __shfl_xor_sync(0xffffffffu, w, 1);
-                if (segok) *segp = w;
-                segp += segstep;
+              for (int c = 0; c < YR; ++c) vw[c * C::TX] = acc[c][u];
+              mbar_arrive(vfull + vb);
+              if (++vb == C::NV) {
+                vb = 0;
+                vp ^= 1u;
               }
             }
           }
+        }
+      }
+    }
+  } else {
+    // =================== epilogue warps: lane = tile column, warp ew = tile rows 8 ew .. 8 ew + 7
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::EREGS));
+    constexpr int ER = C::ER;
+    const int r0 = ER * (warp - C::XWARPS - C::YWARPS);
+    const size_t nxy = (size_t)nx * ny;
+    const size_t chunks = (size_t)(nx + 31) / 32;
+    const double so = OLD && e.so ? *e.so : 1.0;
+    const double coef = OLD ? *e.coef : 0.0;
+    // butterfly row-segment tree (SEG): lane 4m ends with the sum of row r0 + trow, m = lane / 4
+    const int m = lane >> 2;
+    const int trow = r0 + 2 * (2 * (m & 1) + ((m >> 1) & 1)) + ((m >> 2) & 1);
+    unsigned vb = 0, vp = 0;  // output ring position of the next output plane
+    constexpr int ET = 32 * C::EWARPS;
+    double* const omine = olds + (tid - 32 * (C::XWARPS + C::YWARPS));  // slot s, row c: [(s ER + c) ET]
+    unsigned os = 0;  // old slot of the next output plane
+#pragma unroll 1
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      B3Item it;
+      it.set(item, tiles, tiles_x, zchunk, nz);
+      const int z0 = it.z0, z1 = it.z1;
+      const int gx = it.x0 + lane, gy = it.y0 + r0;
+      const bool colok = gx < nx;
+      bool ok[ER];
+#pragma unroll
+      for (int c = 0; c < ER; ++c) ok[c] = colok && gy + c < ny;
+      // running pointers: the next output plane's row gy, the next old plane to load, the next
+      // segment partial of this lane's tree row
+      const size_t first = ((size_t)z0 * ny + gy) * nx + gx;
+      double* orow = out + first;
+      const double* oold = OLD ? e.old + first : nullptr;
+      double* segp = SEG ? e.seg + ((size_t)z0 * ny + it.y0 + trow) * chunks + it.bx : nullptr;
+      const size_t segstep = (size_t)ny * chunks;
+      const bool segok = it.y0 + trow < ny && (lane & 3) == 0;
+      // old-vector values NOLD - 1 planes ahead: cp.async into this thread's own slots, one commit
+      // group per output plane (empty past z1), so wait_group<NOLD - 1> completes the current one
+      int zl = z0;
+      const unsigned os0 = os;
+      auto load_old = [&]() {
+        if (zl < z1) {
+          double* dst = omine + ((os0 + (unsigned)(zl - z0)) % C::NOLD) * ER * ET;
+#pragma unroll
+          for (int c = 0; c < ER; ++c)
+            if (ok[c]) cp_async8(dst + c * ET, oold + (size_t)c * nx, true);
+          oold += nxy;
+        }
+        ++zl;
+        cp_async_commit();
+      };
+      if (OLD)
+#pragma unroll
+        for (int j = 0; j < C::NOLD - 1; ++j) load_old();
+#pragma unroll 1
+      for (int zo = z0; zo < z1; ++zo) {
+        double o[ER];
+        if (OLD) {
+          load_old();  // plane zo + NOLD - 1
+          cp_async_wait<C::NOLD - 1>();
+          const double* src = omine + (os % C::NOLD) * ER * ET;
+#pragma unroll
+          for (int c = 0; c < ER; ++c) o[c] = src[c * ET];
+          ++os;
+        }
+        mbar_wait(vfull + vb, vp);
+        const double* vr = vs + vb * C::V_DOUBLES + r0 * C::TX + lane;
+        double v[ER];
+#pragma unroll
+        for (int c = 0; c < ER; ++c) v[c] = vr[c * C::TX];
+        mbar_arrive(vempty + vb);
+        if (++vb == C::NV) {
+          vb = 0;
+          vp ^= 1u;
+        }
+#pragma unroll
+        for (int c = 0; c < ER; ++c) {
+          v[c] = ok[c] ? v[c] : 0.0;
+          if (OLD && ok[c]) v[c] = v[c] + coef * (o[c] * so);
+        }
+#pragma unroll
+        for (int c = 0; c < ER; ++c)
+          if (ok[c]) orow[(size_t)c * nx] = v[c];
+        orow += nxy;
+        if (SEG) {
+          // tree32 of each row's 32 squares (v[l] += v[l + off], off = 16 .. 1) as a butterfly:
+          // every level pairs tree32's elements and halves the live values per lane
+          const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+          double q[ER];
+#pragma unroll
+          for (int c = 0; c < ER; ++c) q[c] = v[c] * v[c];
+          // level 16: lanes < 16 keep the even rows, lanes >= 16 the odd ones
+          double a[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            a[j] = (h16 ? q[2 * j + 1] : q[2 * j]) + __shfl_xor_sync(0xffffffffu, h16 ? q[2 * j] : q[2 * j + 1], 16);
+          // level 8: bit 3 clear keeps a[0] / a[2], set keeps a[1] / a[3]
+          double b2[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            b2[j] = (h8 ? a[2 * j + 1] : a[2 * j]) + __shfl_xor_sync(0xffffffffu, h8 ? a[2 * j] : a[2 * j + 1], 8);
+          // level 4: bit 2 clear keeps b2[0], set keeps b2[1]
+          double w = (h4 ? b2[1] : b2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? b2[0] : b2[1], 4);
+          w = w + __shfl_xor_sync(0xffffffffu, w, 2);
+          w = w + __shfl_xor_sync(0xffffffffu, w, 1);
+          if (segok) *segp = w;
+          segp += segstep;
         }
       }
     }
