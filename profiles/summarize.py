@@ -2,6 +2,7 @@
 
     python profiles/summarize.py launches <launches.csv> <out.md>
     python profiles/summarize.py full <report.ncu-rep> <out.md>
+    python profiles/summarize.py dram_iter <launches.csv> <out.json>
 """
 import collections
 import csv
@@ -111,5 +112,38 @@ def traffic(tag, out):
     print(json.dumps(doc, indent=1))
 
 
+def dram_iter(path, out):
+    """profiles/dram_per_iter.json: DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one
+    LSQR iteration, from a bench launch list: every launch from one update_kernel (K_U, the last
+    kernel of an iteration) to the next is one whole iteration; the mean over the complete ones."""
+    import json
+    rows = list(csv.reader(open(path)))
+    hdr = next(r for r in rows if r and r[0] == "ID")
+    ik, im, iv, iu, iid = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
+                           hdr.index("Metric Unit"), hdr.index("ID"))
+    per = collections.defaultdict(dict)
+    names = {}
+    for r in rows:
+        if not r or not r[0].isdigit():
+            continue
+        per[int(r[iid])][r[im]] = (r[iv], r[iu])
+        names[int(r[iid])] = r[ik].split("(")[0].replace("void ", "")
+    ids = sorted(per)
+    ends = [i for i in ids if "update_kernel" in names[i]]
+    iters = []
+    for a, b in zip(ends[:-1], ends[1:]):
+        gb = sum(to_gb(*per[i]["dram__bytes_read.sum"]) + to_gb(*per[i]["dram__bytes_write.sum"])
+                 for i in ids if a < i <= b)
+        ms = sum(to_ms(*per[i]["gpu__time_duration.sum"]) for i in ids if a < i <= b)
+        iters.append((gb, ms, b - a))
+    gb = sum(x[0] for x in iters) / len(iters)
+    doc = {"source": f"ncu launch list {path}: launches between consecutive update_kernel launches, "
+                     f"mean over {len(iters)} whole iterations",
+           "bytes_per_iter": gb * 1e9, "launches_per_iter": iters[0][2],
+           "serialised_ms_per_iter": sum(x[1] for x in iters) / len(iters)}
+    open(out, "w").write(json.dumps(doc, indent=1) + "\n")
+    print(json.dumps(doc, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "traffic": traffic, "dram_iter": dram_iter}[sys.argv[1]](sys.argv[2], sys.argv[3])
