@@ -93,6 +93,104 @@ __global__ void __launch_bounds__(256) blur2d_tile_kernel(const double* __restri
   }
 }
 
+// 2D blur for the radii of the taps-by-value path (R <= 12), same order as blur2d_tile_kernel
+// (reference scalar SeparableGaussianBlur2D, linop.cpp:151-162: rows then columns, acc + t * v):
+// compile-time R, the x pass two outputs per thread from LDS.128 windows, the y pass four rows per
+// thread from a register window, and the |out|^2 row-segment partials as a register butterfly
+// (tree32's pairs) instead of a shuffle tree per row.
+template <int R>
+__global__ void __launch_bounds__(256) blur2d_reg_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                         int nx, int ny, int nz, Taps taps, EpiArgs e) {
+  if (e.gate && *e.gate == 0) return;
+  constexpr int W = 32 + 2 * R, H = 32 + 2 * R, P = (W + 1) & ~1, NT = 2 * R + 1;
+  __shared__ __align__(16) double tin[H * P];
+  __shared__ __align__(16) double txs[H * 32];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, z = blockIdx.z;
+  const size_t plane = (size_t)z * nx * ny;
+  const int tid = threadIdx.y * 32 + threadIdx.x, lane = threadIdx.x, w = threadIdx.y;
+  const double sx = e.sx ? *e.sx : 1.0;
+  for (int k = tid; k < H * W; k += 256) {
+    const int ly = k / W, lx = k - ly * W;
+    const int gx = x0 + lx - R, gy = y0 + ly - R;
+    double v = 0.0;
+    if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
+      v = in[plane + (size_t)gy * nx + gx];
+      if (e.sx) v = v * sx;
+    }
+    tin[ly * P + lx] = v;
+  }
+  __syncthreads();
+  // x pass: row r, outputs 2g, 2g + 1
+  for (int t = tid; t < H * 16; t += 256) {
+    const int r = t >> 4, g = t & 15;
+    const double2* row = reinterpret_cast<const double2*>(tin + r * P + 2 * g);
+    double wv[2 * R + 2];
+#pragma unroll
+    for (int j = 0; j < R + 1; ++j) {
+      const double2 q = row[j];
+      wv[2 * j] = q.x;
+      wv[2 * j + 1] = q.y;
+    }
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      a0 = a0 + taps.t[k] * wv[k];
+      a1 = a1 + taps.t[k] * wv[k + 1];
+    }
+    *reinterpret_cast<double2*>(txs + r * 32 + 2 * g) = make_double2(a0, a1);
+  }
+  __syncthreads();
+  // y pass: column `lane`, rows 4w .. 4w + 3
+  double c[4 + 2 * R];
+#pragma unroll
+  for (int j = 0; j < 4 + 2 * R; ++j) c[j] = txs[(4 * w + j) * 32 + lane];
+  const int gx = x0 + lane;
+  double v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) acc = acc + taps.t[k] * c[i + k];
+    const int gy = y0 + 4 * w + i;
+    v[i] = 0.0;
+    if (gx < nx && gy < ny) {
+      const size_t idx = plane + (size_t)gy * nx + gx;
+      v[i] = epilogue(acc, e, idx);
+      out[idx] = v[i];
+    }
+  }
+  if (e.seg) {
+    // tree32 of each row's 32 squares as a butterfly (rows 0/2 on lanes < 16, 1/3 on lanes >= 16)
+    const bool h16 = lane & 16, h8 = lane & 8;
+    double q[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = v[i] * v[i];
+    const double a = (h16 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, h16 ? q[0] : q[1], 16);
+    const double b = (h16 ? q[3] : q[2]) + __shfl_xor_sync(0xffffffffu, h16 ? q[2] : q[3], 16);
+    double s = (h8 ? b : a) + __shfl_xor_sync(0xffffffffu, h8 ? a : b, 8);
+    s = s + __shfl_xor_sync(0xffffffffu, s, 4);
+    s = s + __shfl_xor_sync(0xffffffffu, s, 2);
+    s = s + __shfl_xor_sync(0xffffffffu, s, 1);
+    const int gy = y0 + 4 * w + ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1);
+    if ((lane & 7) == 0 && gy < ny) e.seg[((size_t)z * ny + gy) * ((nx + 31) / 32) + blockIdx.x] = s;
+  }
+}
+
+static bool launch_blur2d_reg(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
+                              const EpiArgs& a) {
+  const dim3 blk(32, 8), grd((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)nz);
+  switch (t.R) {
+#define MLSQR_B2R(RR) \
+  case RR: blur2d_reg_kernel<RR><<<grd, blk, 0, c->stream>>>(in, out, nx, ny, nz, t, a); break;
+    MLSQR_B2R(1) MLSQR_B2R(2) MLSQR_B2R(3) MLSQR_B2R(4) MLSQR_B2R(5) MLSQR_B2R(6)
+    MLSQR_B2R(7) MLSQR_B2R(8) MLSQR_B2R(9) MLSQR_B2R(10) MLSQR_B2R(11) MLSQR_B2R(12)
+#undef MLSQR_B2R
+    default: return false;
+  }
+  c->count();
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // generic single-axis pass (1D operator; z pass of the generic 3D path)
 // ---------------------------------------------------------------------------
@@ -314,8 +412,10 @@ class BlurOp final : public Op {
                                                                           true);
         ctx->count(2);
       } else if (dims_ == 2) {
-        blur2d_tile_kernel<kTY, false><<<g2, blk, smem_, ctx->stream>>>(in, out, (int)nx_, (int)ny_, (int)nz_, taps_, a);
-        ctx->count();
+        if (nz_ > 65535 || !launch_blur2d_reg(ctx, in, out, (int)nx_, (int)ny_, (int)nz_, taps_, a)) {
+          blur2d_tile_kernel<kTY, false><<<g2, blk, smem_, ctx->stream>>>(in, out, (int)nx_, (int)ny_, (int)nz_, taps_, a);
+          ctx->count();
+        }
       } else {
         EpiArgs first = a;
         first.old = nullptr;
