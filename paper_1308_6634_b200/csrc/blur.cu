@@ -371,8 +371,40 @@ class BlurOp final : public Op {
   size_t plane_size() const override { return nx_ * ny_; }
 
  private:
+  // z slabs, guarded input whose ghost planes are not filled yet (K_B's u, produced by K_A right
+  // before): the R ghost planes per side travel on the side stream while the slab interior
+  // (outputs R .. nz-R-1, which read no ghost plane) is blurred; then the two boundary bands.
+  // Per output the arithmetic is unchanged, so the split is bit-identical to one launch.
+  bool run_split(double* in, double* out, const Epi& e) {
+    const int R = taps_.R;
+    if (!(fused_ && dims_ == 3 && e.in_guarded && (R == 4 || R == 6) && blur_mma_enabled() &&
+          nz_ > (size_t)(4 * R)))
+      return false;
+    const int nx = (int)nx_, ny = (int)ny_, nz = (int)nz_;
+    const EpiArgs a = to_args(e);
+    auto band = [&](int zb, int ze) {
+      return R == 4 ? launch_b3m_range<4>(ctx, in, out, nx, ny, nz, zb, ze, taps_, a)
+                    : launch_b3m_range<6>(ctx, in, out, nx, ny, nz, zb, ze, taps_, a);
+    };
+    cudaStream_t s = ctx->side_stream();
+    MLSQR_CUDA(cudaEventRecord(ctx->ev_fork2, ctx->stream));
+    MLSQR_CUDA(cudaStreamWaitEvent(s, ctx->ev_fork2, 0));
+    halo_planes(ctx, in, nx_ * ny_, (long)nz_, R, s);
+    MLSQR_CUDA(cudaEventRecord(ctx->ev_join2, s));
+    const bool ok = band(R, nz - R);  // the TMA map covers the guarded slab: fails for all bands or none
+    MLSQR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join2, 0));
+    if (!ok) return false;
+    band(0, R);
+    band(nz - R, nz);
+    ctx->check_launch();
+    return true;
+  }
+
   void run(const double* in, double* out, const Epi& e) {
     TimedRegion tr(ctx, MLSQR_TCLASS_BLUR);
+    if (ctx->sharded() && !(e.in_guarded && e.ghosts_ready) && !split_off_ &&
+        run_split(const_cast<double*>(in), out, e))
+      return;
     if (ctx->sharded() && !(e.in_guarded && e.ghosts_ready)) {
       // fill the ghost planes: in place for guarded solver vectors, else via a staging copy
       const size_t plane = nx_ * ny_, g = (size_t)taps_.R * plane;
@@ -431,6 +463,7 @@ class BlurOp final : public Op {
   }
 
   static constexpr int kTY = 32;
+  const bool split_off_ = getenv("MLSQR_BLUR_SPLIT") && getenv("MLSQR_BLUR_SPLIT")[0] == '0';
   DevBuf<double> gin_;  // guarded staging input (z-sharded, unguarded callers)
   int dims_;
   size_t nx_, ny_, nz_;

@@ -110,10 +110,11 @@ __device__ __forceinline__ void tma_issue_pred(bool on, unsigned long long* bar,
 // a persistent CTA's work item: z chunk item / tiles of column tile item % tiles
 struct B3Item {
   int z0, z1, x0, y0, bx;
-  __device__ __forceinline__ void set(int item, int tiles, int tiles_x, int zchunk, int nz) {
+  // outputs z0 .. z1-1 of the range zb .. ze-1 (ze - zb planes split into zchunk-plane items)
+  __device__ __forceinline__ void set(int item, int tiles, int tiles_x, int zchunk, int zb, int ze) {
     const int t = item % tiles;
-    z0 = (item / tiles) * zchunk;
-    z1 = min(nz, z0 + zchunk);
+    z0 = zb + (item / tiles) * zchunk;
+    z1 = min(ze, z0 + zchunk);
     bx = t % tiles_x;
     x0 = bx * 32;
     y0 = (t / tiles_x) * 32;
@@ -137,7 +138,7 @@ struct B3Cursor {
 // far outside the tensor map: the hardware zero-fills the box.
 template <int R, bool OLD, bool SEG>
 __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
-    blur3d_mma(const double* __restrict__ in, double* __restrict__ out, int nx, int ny, int nz, int tiles_x,
+    blur3d_mma(const double* __restrict__ in, double* __restrict__ out, int nx, int ny, int zb, int ze, int tiles_x,
                int tiles, int zchunk, int items, int zoff, int nzg, int zshift, Taps taps, EpiArgs e,
                const __grid_constant__ CUtensorMap map_in) {
   using C = B3M<R>;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
       if (++ic.q > ic.hi) {
         ic.item += gridDim.x;
         if (ic.item < items) {
-          ic.it.set(ic.item, tiles, tiles_x, zchunk, nz);
+          ic.it.set(ic.item, tiles, tiles_x, zchunk, zb, ze);
           ic.q = ic.it.z0 - R;
           ic.hi = ic.it.z1 + R - 1;
         }
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
     unsigned kis = grp;  // sequence index of the next plane this group issues
     if (role == 0) {
       ic.item = blockIdx.x;
-      ic.it.set(ic.item, tiles, tiles_x, zchunk, nz);
+      ic.it.set(ic.item, tiles, tiles_x, zchunk, zb, ze);
       ic.q = ic.it.z0 - R;
       ic.hi = ic.it.z1 + R - 1;
       if (C::XG == 2 && grp) advance();
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
-      it.set(item, tiles, tiles_x, zchunk, nz);
+      it.set(item, tiles, tiles_x, zchunk, zb, ze);
       const int nplanes = it.z1 - it.z0 + 2 * R;
 #pragma unroll 1
       for (int j = 0; j < nplanes; ++j, ++k) {
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
-      it.set(item, tiles, tiles_x, zchunk, nz);
+      it.set(item, tiles, tiles_x, zchunk, zb, ze);
       const int z0 = it.z0, z1 = it.z1;
       const int zlo = z0 - R, zhi = z1 + R - 1;
 #pragma unroll 1
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       B3Item it;
-      it.set(item, tiles, tiles_x, zchunk, nz);
+      it.set(item, tiles, tiles_x, zchunk, zb, ze);
       const int z0 = it.z0, z1 = it.z1;
       const int gx = it.x0 + lane, gy = it.y0 + r0;
       const bool colok = gx < nx;
@@ -448,10 +449,19 @@ __global__ void __launch_bounds__(B3M<R>::THREADS, 1)
   }
 }
 
-// MMA variant of launch_b3 (same persistent schedule); false when TMA cannot address the grid
+// MMA variant of launch_b3 (same persistent schedule); false when TMA cannot address the grid.
+// Outputs zb .. ze-1 of the (local) nz-plane grid; inputs zb-R .. ze+R-1 (ghost planes past the slab)
+template <int R>
+static bool launch_b3m_range(Ctx* c, const double* in, double* out, int nx, int ny, int nz, int zb, int ze,
+                             const Taps& t, const EpiArgs& a);
 template <int R>
 static bool launch_b3m(Ctx* c, const double* in, double* out, int nx, int ny, int nz, const Taps& t,
                        const EpiArgs& a) {
+  return launch_b3m_range<R>(c, in, out, nx, ny, nz, 0, nz, t, a);
+}
+template <int R>
+static bool launch_b3m_range(Ctx* c, const double* in, double* out, int nx, int ny, int nz, int zb, int ze,
+                             const Taps& t, const EpiArgs& a) {
   using C = B3M<R>;
   static std::once_flag attr;
   std::call_once(attr, [] {
@@ -462,10 +472,11 @@ static bool launch_b3m(Ctx* c, const double* in, double* out, int nx, int ny, in
   });
   const int tiles_x = (nx + C::TX - 1) / C::TX, tiles_y = (ny + C::TY - 1) / C::TY;
   const int tiles = tiles_x * tiles_y;
-  int zck = nz;
+  const int nzr = ze - zb;
+  int zck = nzr;
   long best = -1;
-  for (int zc = 1; zc <= nz; ++zc) {
-    const long items = (long)tiles * ((nz + zc - 1) / zc);
+  for (int zc = 1; zc <= nzr; ++zc) {
+    const long items = (long)tiles * ((nzr + zc - 1) / zc);
     const long g = items < c->sm_count ? items : c->sm_count;
     const long cost = (items + g - 1) / g * (zc + 2 * R);
     if (best < 0 || cost < best) {
@@ -473,7 +484,7 @@ static bool launch_b3m(Ctx* c, const double* in, double* out, int nx, int ny, in
       zck = zc;
     }
   }
-  const int items = tiles * ((nz + zck - 1) / zck);
+  const int items = tiles * ((nzr + zck - 1) / zck);
   const unsigned grid = (unsigned)(items < c->sm_count ? items : c->sm_count);
   const bool sh = c->sharded();
   const int zoff = sh ? (int)c->zoff : 0, nzg = sh ? (int)c->nzg : nz;
@@ -482,7 +493,7 @@ static bool launch_b3m(Ctx* c, const double* in, double* out, int nx, int ny, in
   if (!tensor_map3d(&mi, in - (size_t)zshift * nx * ny, nx, ny, nz + 2 * zshift, C::P, C::H)) return false;
   auto k = a.old ? (a.seg ? blur3d_mma<R, true, true> : blur3d_mma<R, true, false>)
                  : (a.seg ? blur3d_mma<R, false, true> : blur3d_mma<R, false, false>);
-  k<<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, nz, tiles_x, tiles, zck, items, zoff, nzg, zshift, t, a,
+  k<<<grid, C::THREADS, C::SMEM, c->stream>>>(in, out, nx, ny, zb, ze, tiles_x, tiles, zck, items, zoff, nzg, zshift, t, a,
                                               mi);
   c->count();
   return true;

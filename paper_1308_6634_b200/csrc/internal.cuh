@@ -209,12 +209,15 @@ struct Ctx {
   long zoff = 0, nzg = 0;
   // side stream + fork/join events for exchanges overlapped with main-stream work
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;    // the Krylov loop's vtilde exchange
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;  // an operator's own input exchange
   cudaStream_t side_stream() {
     if (!side) {
       MLSQR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
       MLSQR_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       MLSQR_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      MLSQR_CUDA(cudaEventCreateWithFlags(&ev_fork2, cudaEventDisableTiming));
+      MLSQR_CUDA(cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming));
     }
     return side;
   }
@@ -223,6 +226,8 @@ struct Ctx {
       cudaStreamDestroy(side);
       cudaEventDestroy(ev_fork);
       cudaEventDestroy(ev_join);
+      cudaEventDestroy(ev_fork2);
+      cudaEventDestroy(ev_join2);
       side = nullptr;
     }
   }
