@@ -392,6 +392,10 @@ void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratc
                           double* out, const int* gate, bool dist);
 void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
                           double* out, const int* gate);
+// the distributed reductions' first half: this rank's block-aligned level-3 partials (or its raw
+// segments), allgathered in rank order; returns the gathered list and its length
+const double* dist_gather_partials(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                                   const int* gate, size_t* count);
 // scratch sizes of reduce_segments_dist
 size_t dist_gather_size(Ctx* c, size_t nseg);
 

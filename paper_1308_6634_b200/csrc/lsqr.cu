@@ -415,10 +415,6 @@ void validate_stop(const mlsqr_stop& s) {  // StoppingConfig::validate (krylov.c
   require(s.atol >= 0.0 && s.btol >= 0.0, MLSQR_EINVAL, "tolerances must be >= 0");
 }
 
-__global__ void fin_beta_kernel(DevState* s) { fin_beta_dev(s); }
-__global__ void fin_p_kernel(DevState* s) { fin_p_dev(s); }
-__global__ void fin_alpha_kernel(DevState* s, double* alphas, double* betas) { fin_alpha_dev(s, alphas, betas); }
-__global__ void fin_iter_kernel(DevState* s, mlsqr_iter_rec* trace, mlsqr_stop stop) { fin_iter_dev(s, trace, stop); }
 
 // the same scalar steps as epilogues of the final reduction pass (vec.cuh reduce_final_fin)
 struct FinBeta {
@@ -490,17 +486,18 @@ struct Runner {
                          data ? c->data_distributed() : c->sharded());
   }
 
-  // reduce, then the scalar step F: one fused final pass when the partials are local, else the
-  // distributed reduction followed by the separate scalar kernel
-  template <class F, class K>
-  void reduce_fin(double* seg, size_t nseg, double* out, const int* gate, bool data, F fin, K kernel) {
-    const bool dist = data ? c->data_distributed() : c->sharded();
+  // reduce, then the scalar step F in the same final one-warp pass; z slabs / row shards first
+  // allgather the block-aligned tree partials (every rank finishes the canonical tree identically)
+  template <class F>
+  void reduce_fin(double* seg, size_t nseg, double* out, const int* gate, bool data, F fin) {
+    const bool dist = (data ? c->data_distributed() : c->sharded()) && c->data_distributed();
     if (!dist) {
       reduce_segments_fin(c, seg, nseg, ws->scratch.p, out, gate, fin);
-    } else {
-      reduce(seg, nseg, out, gate, data);
-      kernel();
+      return;
     }
+    size_t J = 0;
+    const double* g = dist_gather_partials(c, seg, nseg, ws->scratch.p, ws->gathered.p, gate, &J);
+    reduce_segments_fin(c, g, J, ws->scratch.p, out, gate, fin);
   }
 
   double* vbuf() const { return pc ? ws->v.p : ws->p.p; }
@@ -535,11 +532,7 @@ struct Runner {
       reduce(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false);
       return;
     }
-    reduce_fin(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false, FinAlpha{st, ws->alphas.p, ws->betas.p},
-               [&] {
-                 fin_alpha_kernel<<<1, 1, 0, c->stream>>>(st, ws->alphas.p, ws->betas.p);
-                 c->count();
-               });
+    reduce_fin(ws->seg_vp.p, ws->sol.segments(), &st->red_vp, gate, false, FinAlpha{st, ws->alphas.p, ws->betas.p});
   }
 
   void init(const double* g) {
@@ -589,8 +582,7 @@ struct Runner {
     ea.in_guarded = true;
     ea.ghosts_ready = vghost_async();
     op->apply(vbuf(), ws->u.p, ea);
-    reduce_fin(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true, FinBeta{st},
-               [&] { fin_beta_kernel<<<1, 1, 0, c->stream>>>(st); c->count(); });
+    reduce_fin(ws->seg_u.p, ws->data.segments(), &st->red_u, gate_active(), true, FinBeta{st});
     store_left(1);
     // K_B: p_s <- A^T(u_s*su) + (-beta)(p_s*sv)
     Epi eb;
@@ -602,8 +594,7 @@ struct Runner {
     eb.gate = flag(1);
     eb.in_guarded = true;
     op->adjoint(ws->u.p, ws->p.p, eb);
-    reduce_fin(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1), false, FinP{st},
-               [&] { fin_p_kernel<<<1, 1, 0, c->stream>>>(st); c->count(); });
+    reduce_fin(ws->seg_p.p, ws->sol.segments(), &st->red_p, flag(1), false, FinP{st});
     // M^{-1}
     precond(flag(2), true);  // + F_a
     fork_vghost();
@@ -618,10 +609,6 @@ struct Runner {
                                                  ws->sol.len, ws->sol.rows, ws->seg_wq.p);
     }
     store_snapshot();  // f is final after K_U; F_i (which advances iter / flags) runs last
-    auto fin_iter = [&] {
-      fin_iter_kernel<<<1, 1, 0, c->stream>>>(st, ws->trace.p, stop);
-      c->count();
-    };
     if (tau != 0.0 && stop.use_s4) {
       reduce(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false);
       // exact data residual |g - A f| (krylov.cpp:142-144): (A f - g)^2 partials
@@ -632,10 +619,9 @@ struct Runner {
       er.gate = gate_active();
       op->apply(ws->f.p, ws->tmp_rows.p, er);
       reduce_fin(ws->seg_res.p, ws->data.segments(), &st->red_res, gate_active(), true,
-                 FinIter{st, ws->trace.p, stop}, fin_iter);
+                 FinIter{st, ws->trace.p, stop});
     } else {
-      reduce_fin(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false, FinIter{st, ws->trace.p, stop},
-                 fin_iter);
+      reduce_fin(ws->seg_wq.p, ws->sol.segments(), &st->red_wq, flag(3), false, FinIter{st, ws->trace.p, stop});
     }
     join_vghost();
     c->count(1);  // update_kernel

@@ -177,12 +177,8 @@ void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratc
   reduce_segments_dist(c, seg, nseg, scratch, gathered, out, gate, c->sharded());
 }
 
-void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
-                          double* out, const int* gate, bool dist) {
-  if (!dist || !c->data_distributed()) {
-    reduce_segments(c, seg, nseg, scratch, out, gate);
-    return;
-  }
+const double* dist_gather_partials(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                                   const int* gate, size_t* count) {
   const size_t P = (size_t)c->comm->size;
   if (nseg % 32768 == 0) {
     // this rank's segments are whole 32768-blocks of the global list: levels 1-3 locally
@@ -194,14 +190,26 @@ void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratc
       TimedRegion tc(c, MLSQR_TCLASS_COLL);
       c->comm->allgather(scratch, K, gathered, c->stream);
     }
-    reduce_segments(c, gathered, K * P, scratch, out, gate);
+    *count = K * P;
   } else {
     {
       TimedRegion tc(c, MLSQR_TCLASS_COLL);
       c->comm->allgather(seg, nseg, gathered, c->stream);
     }
-    reduce_segments(c, gathered, nseg * P, scratch, out, gate);
+    *count = nseg * P;
   }
+  return gathered;
+}
+
+void reduce_segments_dist(Ctx* c, const double* seg, size_t nseg, double* scratch, double* gathered,
+                          double* out, const int* gate, bool dist) {
+  if (!dist || !c->data_distributed()) {
+    reduce_segments(c, seg, nseg, scratch, out, gate);
+    return;
+  }
+  size_t J = 0;
+  const double* g = dist_gather_partials(c, seg, nseg, scratch, gathered, gate, &J);
+  reduce_segments(c, g, J, scratch, out, gate);
 }
 
 }  // namespace mlsqr_b200
