@@ -57,7 +57,7 @@ struct B3M {
   static constexpr int P = ((W + XOFF + 11) / 16) * 16 + 4;  // smallest pitch >= W + XOFF, = 4 mod 16
   static constexpr int KS = (8 + 2 * R + 3) / 4;               // k-steps per 8x8 tile
   static constexpr int MT = (H + 7) / 8;                       // x-pass row tiles (per x warp)
-  static constexpr int XP = 36;                                // xs pitch (= 4 mod 16)
+  static constexpr int XP = 40;  // xs pitch: = 8 mod 16, so the x warps' STS.128 rows land on disjoint banks
   static constexpr int NIN = MLSQR_B3M_NIN;  // input-plane ring (TMA, x warps)
   static constexpr int NXS = MLSQR_B3M_NXS;  // x-result ring (x warps -> y warps)
   // the x pass of the last row tile reads up to 8 * MT - H rows past the tile: keep them inside

@@ -1,7 +1,8 @@
 #!/bin/bash
 # Round measurement recipe (run on the GPU box via gpurun):  bash tools/profile_round.sh TAG
-#   bench line (+ CPU baseline, e2e), reference arm, ncu launch list of the bench, one
-#   `ncu --set full` capture per hot kernel.  Outputs land in gpurun_out/TAG_*.
+#   bench line (+ CPU baseline, e2e), reference arm, ncu launch list of the bench (with DRAM bytes),
+#   one `ncu --set full` capture per hot kernel, and one bench line per other BASELINE config.
+#   Outputs land in gpurun_out/TAG_*.
 TAG=${1:-r}
 O=gpurun_out
 mkdir -p $O
@@ -10,7 +11,7 @@ tail -1 $O/${TAG}_bench.json
 timeout 900 python bench.py --impl reference > $O/${TAG}_ref.json 2> $O/${TAG}_ref.err; echo "ref rc=$?"
 tail -1 $O/${TAG}_ref.json
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -c 600 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+  -c 700 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
   > $O/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
 # one full capture per hot kernel, aimed at a level-0 launch of the 512^3 driver:
 #   blur: 6th launch (mlsqr iteration 1's K_A, with the xpby/norm epilogue); sweep_fn: 2nd V-cycle's level 0;
@@ -27,8 +28,10 @@ cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2' 3
 cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1' 5
 cap restrict 'restrict_zm_kernel' 4
 cap update 'update_kernel' 0
-# the other BASELINE configs (parity configs; one bench line each, no CPU baseline)
+# the other BASELINE configs (parity configs; one bench line each, no CPU baseline; enough steps for
+# the clock sampler to see the timed region)
+declare -A STEPS=([c1]=300 [c2]=200 [c3]=100 [c4]=5)
 for c in c1 c2 c3 c4; do
-  timeout 600 python bench.py --config $c --no-cpu-baseline --steps 3 --warmup 3 > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err
+  timeout 600 python bench.py --config $c --no-cpu-baseline --steps ${STEPS[$c]} --warmup 3 > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err
   echo "bench $c rc=$?"
 done
