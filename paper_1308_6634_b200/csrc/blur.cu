@@ -242,6 +242,7 @@ __global__ void blur_pass_kernel(const double* __restrict__ in, double* __restri
   }
 }
 
+#include "tma.cuh"
 #include "blur3d_pipe.cuh"
 #include "blur3d_mma.cuh"
 

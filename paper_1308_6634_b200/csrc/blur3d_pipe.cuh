@@ -16,7 +16,7 @@
 //    ... in ascending order;
 //  * |out|^2 goes to shared memory and warp 15 (no x-pass work) forms the
 //    canonical row-segment trees one phase later (tree32_serial == tree32).
-// (included inside namespace mlsqr_b200; blur.cu includes <cudaTypedefs.h> and <mutex>)
+// (included inside namespace mlsqr_b200 after tma.cuh)
 
 template <int R>
 struct B3P {
@@ -48,32 +48,6 @@ struct B3P {
   static constexpr unsigned OLD_BYTES = TX * TY * 8u;
   static_assert(H * XG <= TREE_WARP * 32, "x-pass tasks must leave the tree warp free");
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  unsigned done;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load3d(double* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                           unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // Persistent: gridDim.x CTAs (one per SM) take work items round-robin; item k is column
 // tile k % T of z chunk k / T (zchunk planes).  CTAs running at the same time therefore
@@ -274,34 +248,6 @@ __global__ void __launch_bounds__(512, 1) blur3d_pipe(const double* __restrict__
     qbase += (unsigned)(zhi - zlo + 1);
   }
 #undef TAP
-}
-
-// ---- host side ------------------------------------------------------------
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    (void)cudaGetLastError();
-  });
-  return fn;
-}
-
-// fp64 tensor map of an (nx, ny, nz) grid with a (bx, by, 1) box; false if TMA cannot address it
-static bool tensor_map3d(CUtensorMap* m, const double* base, int nx, int ny, int nz, int bx, int by) {
-  auto enc = tensor_map_encoder();
-  if (!enc || (nx & 1) || (reinterpret_cast<uintptr_t>(base) & 15) || bx > 256 || by > 256) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
-  cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
-  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int R>

@@ -14,6 +14,10 @@
 // Storage: per level the d edge-coefficient arrays (cx, cy, cz), zero where
 // an edge is missing; no CSR is ever built (sparse.cpp's std::map assembly
 // is replaced by one pass over the field).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "internal.cuh"
 #include "vec.cuh"
 
@@ -78,6 +82,7 @@ enum SweepMode { kFirst = 0, kNormal = 1, kProlong = 2 };
 // one omega-Jacobi sweep: out = x + (omega * (b - M x)) / D   (x = 0 for kFirst,
 // x = x + P xc for kProlong); seg (optional) <- partials of out * b  (stencil_zm.cuh)
 #include "stencil_zm.cuh"
+#include "tma.cuh"
 #include "sweep_fn.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
@@ -581,13 +586,39 @@ class VCycle final : public Pc {
     const int zc = fn_chunk(L.nx, L.ny, L.nz, ctx->sm_count);
     dim3 grd((unsigned)((L.nx + fn::TX - 1) / fn::TX), (unsigned)((L.ny + fn::TY - 1) / fn::TY),
              (unsigned)((L.nz + zc - 1) / zc));
+    if (fn_tma_ && sweep_fn_tma(l, b, out, seg, gate, zc, grd)) return;
     sweep_fn_kernel<<<grd, dim3(32, fn::WARPS), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate, zc, zoff_l(l),
                                                                    nzg_l(l));
     ctx->count();
   }
 
+  // the TMA-fed kernel; false (nothing launched) when a stream cannot be tensor-mapped
+  bool sweep_fn_tma(int l, const double* b, double* out, double* seg, const int* gate, int zc, dim3 grd) {
+    const Level& L = lv_[(size_t)l];
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+      MLSQR_CUDA(cudaFuncSetAttribute(sweep_fn_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)fnt::SMEM));
+    });
+    // slabs read the ghost planes (b: one per side; the coefficients: two below for cz, mapped on both sides)
+    const int gb = ctx->sharded() ? 1 : 0, gcz = ctx->sharded() ? 2 : 0;
+    const size_t nxy = (size_t)L.nx * L.ny;
+    CUtensorMap mb{}, mx{}, my{}, mz{};
+    const int nz = L.nz;
+    if (!tensor_map3d(&mb, b - gb * nxy, L.nx, L.ny, nz + 2 * gb, fnt::BX, fnt::BY) ||
+        !tensor_map3d(&mx, L.cx.p - gcz * nxy, L.nx, L.ny, nz + 2 * gcz, fnt::BX, fnt::BY) ||
+        !tensor_map3d(&my, L.cy.p - gcz * nxy, L.nx, L.ny, nz + 2 * gcz, fnt::BX, fnt::BY) ||
+        !tensor_map3d(&mz, L.cz.p - gcz * nxy, L.nx, L.ny, nz + 2 * gcz, fnt::BX, fnt::BY))
+      return false;
+    sweep_fn_tma_kernel<<<grd, dim3(32, fn::WARPS), fnt::SMEM, ctx->stream>>>(
+        view(l), out, omega_, seg, gate, zc, zoff_l(l), nzg_l(l), gb, gcz, mb, mx, my, mz);
+    ctx->count();
+    return true;
+  }
+
  public:
   bool fn_enabled_ = true;
+  const bool fn_tma_ = !(getenv("MLSQR_FN_TMA") && getenv("MLSQR_FN_TMA")[0] == '0');
 
  private:
 
