@@ -375,17 +375,23 @@ void orc_linop_adjoint(const orc_linop* op, const double* y, double* x) {
     case OP_IDENTITY: memcpy(x, y, sizeof(double) * op->rows); break;
     case OP_DENSE:  /* DenseOperator::do_apply_adjoint (linop.cpp:78-84) */
       if (g_device && op->rows % 8 == 0) {
-        /* 8 fixed row chunks, sequential inside, chunk partials summed in order */
+        /* 8 fixed row chunks, sequential inside, chunk partials summed in order:
+         * x[j] = ((0 + acc_0[j]) + acc_1[j]) + ...,  acc_c[j] = (0 + y[i0] a[i0][j]) + y[i0+1] a[i0+1][j] + ...
+         * The loops run row-major (the per-column operation sequence is unchanged), so the
+         * matrix streams once per chunk instead of being walked column by column. */
         const size_t ch = op->rows / 8;
-        for (size_t j = 0; j < op->cols; ++j) {
-          double tot = 0.0;
-          for (size_t c = 0; c < 8; ++c) {
-            double acc = 0.0;
-            for (size_t i = c * ch; i < (c + 1) * ch; ++i) acc += y[i] * op->a[i * op->cols + j];
-            tot += acc;
+        double* acc = (double*)malloc(sizeof(double) * op->cols);
+        for (size_t j = 0; j < op->cols; ++j) x[j] = 0.0;
+        for (size_t c = 0; c < 8; ++c) {
+          for (size_t j = 0; j < op->cols; ++j) acc[j] = 0.0;
+          for (size_t i = c * ch; i < (c + 1) * ch; ++i) {
+            const double yi = y[i];
+            const double* row = op->a + i * op->cols;
+            for (size_t j = 0; j < op->cols; ++j) acc[j] += yi * row[j];
           }
-          x[j] = tot;
+          for (size_t j = 0; j < op->cols; ++j) x[j] += acc[j];
         }
+        free(acc);
         break;
       }
       for (size_t j = 0; j < op->cols; ++j) x[j] = 0.0;
