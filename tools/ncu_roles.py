@@ -57,6 +57,12 @@ def main():
         print(f"== role from SASS line {a} ({seg[0][isrc].strip()[:40]}): {100 * S / tot:.1f}% of samples, "
               f"{I / 1e6:.1f} M instructions")
         print("   " + " ".join(f"{n}={100 * v / max(S, 1):.0f}%" for n, v in st.most_common(7)))
+        ops = collections.Counter()
+        for r in seg:
+            t = r[isrc].split()
+            if t:
+                ops[t[1] if t[0].startswith("@") and len(t) > 1 else t[0]] += f(r, ie)
+        print("   instructions: " + " ".join(f"{o}={v / max(I, 1) * 100:.0f}%" for o, v in ops.most_common(12)))
         for r in sorted(seg, key=lambda r: -f(r, iw))[:top]:
             s3 = sorted(((f(r, i), h[i][6:]) for i in stalls), reverse=True)[:2]
             print(f"   {100 * f(r, iw) / tot:5.2f}%  L{line_of.get(r[ia], ''):>4} {r[isrc].strip()[:48]:48s} " +
