@@ -165,12 +165,14 @@ def test_vcycle_explicit_coefficients_and_variants(ctx, dev):
         assert np.array_equal(vc.solve(x), om.solve(x)), (levels, pre, post, kc)
 
 
-@pytest.mark.parametrize("fn", ["1", "0"])
-def test_vcycle_3d_variants_fused_and_unfused(ctx, dev, monkeypatch, fn):
-    """3D V-cycles with the first two pre-sweeps fused (sweep_fn, default) and, with
-    MLSQR_FN_SWEEPS=0, as two sweep_zm launches: both bit-equal to the oracle, on a grid whose
-    x/y extents are not tile multiples, for several (nu, coarse sweeps) counts."""
+@pytest.mark.parametrize("fn,tma", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_vcycle_3d_variants_fused_and_unfused(ctx, dev, monkeypatch, fn, tma):
+    """3D V-cycles with the first two pre-sweeps fused -- TMA-fed (sweep_fn_tma, default) or, with
+    MLSQR_FN_TMA=0, the plain sweep_fn -- and, with MLSQR_FN_SWEEPS=0, as two sweep_zm launches: all
+    bit-equal to the oracle, on a grid whose x/y extents are not tile multiples (zero-filled TMA
+    boxes), for several (nu, coarse sweeps) counts."""
     monkeypatch.setenv("MLSQR_FN_SWEEPS", fn)
+    monkeypatch.setenv("MLSQR_FN_TMA", tma)
     shape, h = (40, 24, 12), 1 / 40
     n = 40 * 24 * 12
     grid = dev.grid(3, shape, h)
