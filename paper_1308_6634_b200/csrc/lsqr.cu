@@ -66,6 +66,13 @@ struct Workspace {
   DevBuf<double> alphas, betas;
   DevBuf<double> g;  // device copy of host data
   DevBuf<double> f;
+  // the instantiated iteration graph of the last solve on this workspace: the next solve captures
+  // its iteration again and UPDATES this executable (new pointers and scalars, same topology)
+  // instead of instantiating a new one
+  cudaGraphExec_t ge = nullptr;
+  ~Workspace() {
+    if (ge) cudaGraphExecDestroy(ge);
+  }
 };
 
 Workspace* workspace_new(Ctx* c, size_t rows, size_t cols, RowShape data, RowShape sol,
@@ -692,12 +699,24 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
       throw;
     }
     MLSQR_CUDA(cudaStreamEndCapture(c->stream, &gr));
-    MLSQR_CUDA(cudaGraphInstantiate(&ge, gr, 0));
+    if (ws->ge) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(ws->ge, gr, &info) == cudaSuccess) {
+        ge = ws->ge;
+      } else {  // another topology (a different operator / map on this workspace): instantiate anew
+        (void)cudaGetLastError();
+        cudaGraphExecDestroy(ws->ge);
+        ws->ge = nullptr;
+      }
+    }
+    if (!ge) {
+      MLSQR_CUDA(cudaGraphInstantiate(&ge, gr, 0));
+      ws->ge = ge;
+    }
     // every replay launches the captured kernels (gated ones exit at once)
     c->launches += (c->launches - before) * (uint64_t)(stop.max_iters - 1);
     for (int i = 0; i < stop.max_iters; ++i) MLSQR_CUDA(cudaGraphLaunch(ge, c->stream));
     MLSQR_CUDA(cudaStreamSynchronize(c->stream));
-    cudaGraphExecDestroy(ge);
     cudaGraphDestroy(gr);
   } else {
     for (int i = 0; i < stop.max_iters; ++i) {
