@@ -691,8 +691,18 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
     cudaGraphExec_t ge = nullptr;
     MLSQR_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     const uint64_t before = c->launches;
+    // iterations per graph replay: the graph holds `per` gated iterations (fewer replay gaps; the
+    // largest of 5, 4, 2 that divides max_iters; MLSQR_GRAPH_ITERS overrides)
+    static const int per_env = [] {
+      const char* e = getenv("MLSQR_GRAPH_ITERS");
+      return e ? atoi(e) : 0;
+    }();
+    int per = 1;
+    for (int k : {5, 4, 2})
+      if (per == 1 && stop.max_iters % k == 0) per = k;
+    if (per_env >= 1) per = stop.max_iters % per_env == 0 ? per_env : 1;
     try {
-      r.iteration(g_dev);
+      for (int k = 0; k < per; ++k) r.iteration(g_dev);
     } catch (...) {
       cudaStreamEndCapture(c->stream, &gr);
       if (gr) cudaGraphDestroy(gr);
@@ -714,8 +724,8 @@ int solve_mlsqr(Op* op, Pc* pc, const double* g_dev, double tau, const mlsqr_sto
       ws->ge = ge;
     }
     // every replay launches the captured kernels (gated ones exit at once)
-    c->launches += (c->launches - before) * (uint64_t)(stop.max_iters - 1);
-    for (int i = 0; i < stop.max_iters; ++i) MLSQR_CUDA(cudaGraphLaunch(ge, c->stream));
+    c->launches += (c->launches - before) * (uint64_t)(stop.max_iters / per - 1);
+    for (int i = 0; i < stop.max_iters / per; ++i) MLSQR_CUDA(cudaGraphLaunch(ge, c->stream));
     MLSQR_CUDA(cudaStreamSynchronize(c->stream));
     cudaGraphDestroy(gr);
   } else {
