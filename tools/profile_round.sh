@@ -23,7 +23,7 @@ cap() {  # name regex skip
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
 cap blur 'blur3d_(mma|pipe)' 5
-cap sweep_fn 'sweep_fn_kernel' 5
+cap sweep_fn 'sweep_fn(_tma)?_kernel' 5
 cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2' 3
 cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1' 5
 cap restrict 'restrict_zm_kernel' 4
