@@ -95,21 +95,23 @@ __global__ void __launch_bounds__(256) blur2d_tile_kernel(const double* __restri
 
 // 2D blur for the radii of the taps-by-value path (R <= 12), same order as blur2d_tile_kernel
 // (reference scalar SeparableGaussianBlur2D, linop.cpp:151-162: rows then columns, acc + t * v):
-// compile-time R, the x pass two outputs per thread from LDS.128 windows, the y pass four rows per
-// thread from a register window, and the |out|^2 row-segment partials as a register butterfly
-// (tree32's pairs) instead of a shuffle tree per row.
+// compile-time R; the x pass makes two outputs per thread from LDS.128 pairs and the y pass four
+// rows per thread, both STREAMING their input window (each loaded value goes straight into every
+// accumulator it feeds, so each accumulator still sums its taps in ascending order) instead of
+// holding it in registers: 32 registers, 8 resident blocks per SM, so C2's 1024 tiles run as one
+// wave; the |out|^2 row-segment partials are a register butterfly (tree32's pairs).
 template <int R>
-__global__ void __launch_bounds__(256) blur2d_reg_kernel(const double* __restrict__ in, double* __restrict__ out,
-                                                         int nx, int ny, int nz, Taps taps, EpiArgs e) {
+__global__ void __launch_bounds__(256, 8) blur2d_reg_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                            int nx, int ny, int nz, Taps taps, EpiArgs e) {
   if (e.gate && *e.gate == 0) return;
-  constexpr int W = 32 + 2 * R, H = 32 + 2 * R, P = (W + 1) & ~1, NT = 2 * R + 1;
-  __shared__ __align__(16) double tin[H * P];
-  __shared__ __align__(16) double txs[H * 32];
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, z = blockIdx.z;
+  constexpr int TH = 32, NTH = 256;
+  constexpr int W = 32 + 2 * R, H = TH + 2 * R, P = (W + 1) & ~1, NT = 2 * R + 1;
+  __shared__ __align__(16) double tin[H * P];  // input tile; the x results overwrite columns 0..31
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TH, z = blockIdx.z;
   const size_t plane = (size_t)z * nx * ny;
   const int tid = threadIdx.y * 32 + threadIdx.x, lane = threadIdx.x, w = threadIdx.y;
   const double sx = e.sx ? *e.sx : 1.0;
-  for (int k = tid; k < H * W; k += 256) {
+  for (int k = tid; k < H * W; k += NTH) {
     const int ly = k / W, lx = k - ly * W;
     const int gx = x0 + lx - R, gy = y0 + ly - R;
     double v = 0.0;
@@ -120,42 +122,47 @@ __global__ void __launch_bounds__(256) blur2d_reg_kernel(const double* __restric
     tin[ly * P + lx] = v;
   }
   __syncthreads();
-  // x pass: row r, outputs 2g, 2g + 1
-  for (int t = tid; t < H * 16; t += 256) {
+  // x pass: row r, outputs 2g (taps on window positions 0..2R) and 2g + 1 (positions 1..2R+1),
+  // written in place over the row's first 32 columns once every thread of the round (whole rows)
+  // has read its window
+  for (int base = 0; base < H * 16; base += NTH) {
+    const int t = base + tid;
+    const bool act = t < H * 16;
     const int r = t >> 4, g = t & 15;
-    const double2* row = reinterpret_cast<const double2*>(tin + r * P + 2 * g);
-    double wv[2 * R + 2];
-#pragma unroll
-    for (int j = 0; j < R + 1; ++j) {
-      const double2 q = row[j];
-      wv[2 * j] = q.x;
-      wv[2 * j + 1] = q.y;
-    }
     double a0 = 0.0, a1 = 0.0;
+    if (act) {
+      const double2* row = reinterpret_cast<const double2*>(tin + r * P + 2 * g);
 #pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      a0 = a0 + taps.t[k] * wv[k];
-      a1 = a1 + taps.t[k] * wv[k + 1];
+      for (int j = 0; j < R + 1; ++j) {
+        const double2 q = row[j];
+        a0 = a0 + taps.t[2 * j] * q.x;
+        if (j > 0) a1 = a1 + taps.t[2 * j - 1] * q.x;
+        if (j < R) a0 = a0 + taps.t[2 * j + 1] * q.y;
+        a1 = a1 + taps.t[2 * j] * q.y;
+      }
     }
-    *reinterpret_cast<double2*>(txs + r * 32 + 2 * g) = make_double2(a0, a1);
+    __syncthreads();
+    if (act) *reinterpret_cast<double2*>(tin + r * P + 2 * g) = make_double2(a0, a1);
   }
   __syncthreads();
-  // y pass: column `lane`, rows 4w .. 4w + 3
-  double c[4 + 2 * R];
+  // y pass: column `lane`, output rows 4w .. 4w + 3 from x-result rows 4w .. 4w + 3 + 2R
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int j = 0; j < 4 + 2 * R; ++j) c[j] = txs[(4 * w + j) * 32 + lane];
+  for (int j = 0; j < 4 + 2 * R; ++j) {
+    const double c = tin[(4 * w + j) * P + lane];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (j - i >= 0 && j - i < NT) acc[i] = acc[i] + taps.t[j - i] * c;
+  }
   const int gx = x0 + lane;
   double v[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < NT; ++k) acc = acc + taps.t[k] * c[i + k];
     const int gy = y0 + 4 * w + i;
     v[i] = 0.0;
     if (gx < nx && gy < ny) {
       const size_t idx = plane + (size_t)gy * nx + gx;
-      v[i] = epilogue(acc, e, idx);
+      v[i] = epilogue(acc[i], e, idx);
       out[idx] = v[i];
     }
   }

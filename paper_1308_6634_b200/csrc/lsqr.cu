@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(256) update_kernel(const DevState* __restrict_
   const bool upd = s->flags[3] != 0;
   const double sc = s->sc, sv = s->sv, ndc = s->neg_dc;
   const size_t chunks = (len + 31) / 32, rstep = (size_t)gridDim.y * blockDim.y;
+#pragma unroll 4
   for (size_t row = (size_t)blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += rstep) {
     double prod = 0.0;
     if (xi < len) {

@@ -269,9 +269,11 @@ __global__ void zero_boundary_edges_kernel(Lvl L, int zoff, int nzg, double* cx,
 }
 
 // z chunk: enough blocks to fill the GPU a few times; even (restriction pairs fine planes)
+// (MLSQR_ZM_BPS: target blocks per SM, default 24)
 static inline int zm_chunk(int nx, int ny, int nz, int sms) {
+  static const long bps = getenv("MLSQR_ZM_BPS") ? atol(getenv("MLSQR_ZM_BPS")) : 24;
   const long bxy = (long)((nx + 31) / 32) * ((ny + 7) / 8);
-  long chunks = (sms * 24L + bxy - 1) / bxy;
+  long chunks = (sms * bps + bxy - 1) / bxy;
   if (chunks < 1) chunks = 1;
   if (chunks > nz) chunks = nz;
   int zc = (int)((nz + chunks - 1) / chunks);

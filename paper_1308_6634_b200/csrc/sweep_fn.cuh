@@ -24,7 +24,10 @@ constexpr int TX = 32, TY = 16;
 constexpr int ROWS = TY + 2, COLS = TX + 2;
 constexpr int WARPS = ROWS + 1;  // rows y0-1 .. y0+TY, then the x-halo warp
 constexpr int THREADS = 32 * WARPS;
-constexpr int MINB = 1;  // resident blocks per SM (19 warps, 92 registers)
+#ifndef MLSQR_FN_MINB
+#define MLSQR_FN_MINB 1
+#endif
+constexpr int MINB = MLSQR_FN_MINB;  // resident blocks per SM (19 warps, 85-92 registers at 1)
 }  // namespace fn
 
 constexpr int kFnL2Ahead = 1;  // L2 prefetch distance beyond the register prefetch (planes)
@@ -320,14 +323,17 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB)
 // memory (x1 is 0 outside the grid, where it meets exactly-zero boundary coefficients), then the
 // second sweep; D and the row sums in sweep_zm_kernel<2>'s order.  Level-0 traffic 4 + 1 words
 // per point instead of 3 + 5 for the two kernels, and one launch fewer per level.
+// TY = tile rows (8: one row per warp; 32: four rows per warp and a 34 x 34 x1 ring instead of
+// 10 x 34 per 32 x 8 outputs -- 1.13 instead of 1.33 first-sweep points per output, a quarter of
+// the blocks)
+template <int TY>
 __global__ void __launch_bounds__(256) sweep_fn2d_kernel(Lvl L, const double* __restrict__ b,
                                                          double* __restrict__ out, double omega,
                                                          double* __restrict__ seg, const int* gate) {
   if (gate && *gate == 0) return;
-  __shared__ double xs[10][35];
+  __shared__ double xs[TY + 2][35];
   const int nx = L.nx, ny = L.ny;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TY;
   const double eps = *L.eps;
   auto diag = [&](long i) {  // diag_at order: x-, x+, y-, y+ ; then + eps
     double d = 0.0;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(256) sweep_fn2d_kernel(Lvl L, const double* __
     d = d + L.cy[i];
     return d + eps;
   };
-  for (int k = tid; k < 10 * 34; k += 256) {
+  for (int k = threadIdx.y * 32 + threadIdx.x; k < (TY + 2) * 34; k += 256) {
     const int r = k / 34, cc = k - r * 34;
     const int gx = x0 - 1 + cc, gy = y0 - 1 + r;
     double x1 = 0.0;
@@ -348,28 +354,33 @@ __global__ void __launch_bounds__(256) sweep_fn2d_kernel(Lvl L, const double* __
     xs[r][cc] = x1;
   }
   __syncthreads();
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int gx = x0 + tx, gy = y0 + ty;
-  if (gy >= ny) return;  // whole warp (one row segment)
-  double v = 0.0, bi = 0.0;
-  if (gx < nx) {
-    const long i = (long)gy * nx + gx;
-    const double d = diag(i);
-    bi = b[i];
-    const double xc = xs[ty + 1][tx + 1];
-    // m_row order: y-, x-, diag, x+, y+
-    double acc = 0.0;
-    acc = acc + -L.cy[i - nx] * xs[ty][tx + 1];
-    acc = acc + -L.cx[i - 1] * xs[ty + 1][tx];
-    acc = acc + d * xc;
-    acc = acc + -L.cx[i] * xs[ty + 1][tx + 2];
-    acc = acc + -L.cy[i] * xs[ty + 2][tx + 1];
-    v = xc + (omega * (bi - acc)) / d;
-    out[i] = v;
-  }
-  if (seg) {
-    const double s2 = tree32(v * bi);
-    if (tx == 0) seg[(long)gy * ((nx + 31) / 32) + blockIdx.x] = s2;
+  const int tx = threadIdx.x;
+  const int gx = x0 + tx;
+#pragma unroll
+  for (int rr = 0; rr < TY / 8; ++rr) {
+    const int ty = threadIdx.y * (TY / 8) + rr;
+    const int gy = y0 + ty;
+    if (gy >= ny) break;  // whole warp (one row segment)
+    double v = 0.0, bi = 0.0;
+    if (gx < nx) {
+      const long i = (long)gy * nx + gx;
+      const double d = diag(i);
+      bi = b[i];
+      const double xc = xs[ty + 1][tx + 1];
+      // m_row order: y-, x-, diag, x+, y+
+      double acc = 0.0;
+      acc = acc + -L.cy[i - nx] * xs[ty][tx + 1];
+      acc = acc + -L.cx[i - 1] * xs[ty + 1][tx];
+      acc = acc + d * xc;
+      acc = acc + -L.cx[i] * xs[ty + 1][tx + 2];
+      acc = acc + -L.cy[i] * xs[ty + 2][tx + 1];
+      v = xc + (omega * (bi - acc)) / d;
+      out[i] = v;
+    }
+    if (seg) {
+      const double s2 = tree32(v * bi);
+      if (tx == 0) seg[(long)gy * ((nx + 31) / 32) + blockIdx.x] = s2;
+    }
   }
 }
 

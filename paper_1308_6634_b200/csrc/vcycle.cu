@@ -84,6 +84,7 @@ enum SweepMode { kFirst = 0, kNormal = 1, kProlong = 2 };
 #include "stencil_zm.cuh"
 #include "tma.cuh"
 #include "sweep_fn.cuh"
+#include "stencil_ym.cuh"
 
 // y = (M + eps I) x   (tests; penalty_gradient, diffusion.cpp:103-106)
 __global__ void m_apply_kernel(Lvl L, const double* __restrict__ x, double* __restrict__ y) {
@@ -490,7 +491,11 @@ class VCycle final : public Pc {
       sweep_zm_kernel<3, MODE, int><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
     else if (dims_ == 3)
       sweep_zm_kernel<3, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
-    else if (dims_ == 2)
+    else if (dims_ == 2 && ym_ && (long)((L.nx + 31) / 32) * ((L.ny + 7) / 8) > 4L * ctx->sm_count) {
+      const int yc = ym_chunk(L.nx, L.ny, ctx->sm_count, 4);
+      sweep_ym_kernel<MODE><<<dim3((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 8 * yc - 1) / (8 * yc))), dim3(32, 8), 0,
+                              ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, yc);
+    } else if (dims_ == 2)
       sweep_zm_kernel<2, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
     else
       sweep_zm_kernel<1, MODE><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, xc, cnx, cny, b, out, omega_, seg, gate, zc);
@@ -507,7 +512,11 @@ class VCycle final : public Pc {
       restrict_zm_kernel<3, int><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
     else if (dims_ == 3)
       restrict_zm_kernel<3><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
-    else if (dims_ == 2)
+    else if (dims_ == 2 && ym_ && (long)((L.nx + 31) / 32) * ((L.ny + 7) / 8) > 4L * ctx->sm_count) {
+      const int yc = ym_chunk(L.nx, L.ny, ctx->sm_count, 4);
+      restrict_ym_kernel<<<dim3((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 8 * yc - 1) / (8 * yc))), dim3(32, 8), 0,
+                           ctx->stream>>>(view(l), x, b, C.nx, C.b.p, gate, yc);
+    } else if (dims_ == 2)
       restrict_zm_kernel<2><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
     else
       restrict_zm_kernel<1><<<grd, dim3(32, 8), 0, ctx->stream>>>(view(l), x, b, C.nx, C.ny, C.b.p, gate, zc);
@@ -570,6 +579,9 @@ class VCycle final : public Pc {
   // only when the caller's p is guarded) and of the coefficients
   bool fn_ok(int l) const {
     if (!fn_enabled_ || dims_ < 2) return false;
+    // small 3D levels: the fused pair marches each block's planes through one serial TMA / x1 ring
+    // (~9 us from 64^3 down to 8^3) where two z-march launches take ~3 us each
+    if (dims_ == 3 && (long)lv_[(size_t)l].n < fn_min_) return false;
     if (!ctx->sharded()) return true;
     return lv_[(size_t)l].nz >= 2 && (l > 0 || in_guarded);
   }
@@ -579,7 +591,12 @@ class VCycle final : public Pc {
     TimedRegion tr(ctx, l == 0 ? MLSQR_TCLASS_SMOOTH : -1);
     TimedRegion tk(ctx, l == 0 ? MLSQR_TCLASS_SWEEP_FN : -1);
     if (dims_ == 2) {
-      sweep_fn2d_kernel<<<row_grid(L.nx, L.ny), dim3(32, 8), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate);
+      // 32-row tiles where 8-row tiles would take more than a wave (MLSQR_YM=0: 8-row tiles)
+      if (ym_ && (long)((L.nx + 31) / 32) * ((L.ny + 7) / 8) > 8L * ctx->sm_count)
+        sweep_fn2d_kernel<32><<<dim3((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 31) / 32)), dim3(32, 8), 0,
+                                 ctx->stream>>>(view(l), b, out, omega_, seg, gate);
+      else
+        sweep_fn2d_kernel<8><<<row_grid(L.nx, L.ny), dim3(32, 8), 0, ctx->stream>>>(view(l), b, out, omega_, seg, gate);
       ctx->count();
       return;
     }
@@ -619,6 +636,10 @@ class VCycle final : public Pc {
  public:
   bool fn_enabled_ = true;
   const bool fn_tma_ = !(getenv("MLSQR_FN_TMA") && getenv("MLSQR_FN_TMA")[0] == '0');
+  // 2D sweeps / restriction marching rows (stencil_ym.cuh); MLSQR_YM=0: one point per thread
+  const bool ym_ = !(getenv("MLSQR_YM") && getenv("MLSQR_YM")[0] == '0');
+  // the smallest 3D level (points) that runs the fused first sweeps (MLSQR_FN_MIN)
+  const long fn_min_ = getenv("MLSQR_FN_MIN") ? atol(getenv("MLSQR_FN_MIN")) : 262144;
 
  private:
 

@@ -108,6 +108,11 @@ __global__ void __launch_bounds__(256) reduce2_kernel(const double* __restrict__
   if (lane == 0) out[k] = r;
 }
 
+void reduce2_pass(Ctx* c, const double* in, size_t J, size_t K, double* out, const int* gate) {
+  reduce2_kernel<<<(unsigned)((K + 7) / 8), 256, 0, c->stream>>>(in, J, K, out, gate);
+  c->count();
+}
+
 size_t reduce_scratch_size(size_t nseg) {
   size_t tot = 0;
   while (nseg > 1024) {

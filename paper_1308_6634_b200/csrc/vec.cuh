@@ -1,6 +1,8 @@
 // vec.cuh -- device-side pieces shared by the operator / stencil / solver kernels.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace mlsqr_b200 {
@@ -93,9 +95,93 @@ __global__ void __launch_bounds__(32) reduce_final_fin(const double* __restrict_
   if (lane == 0) fin();
 }
 
+// one reduce2_kernel pass (vec.cu): J values -> K = ceil(J / 1024)
+void reduce2_pass(Ctx* c, const double* in, size_t J, size_t K, double* out, const int* gate);
+
+// The last two-level pass, when it leaves at most 64 values (at most 8 blocks of reduce2_kernel),
+// fused with the final one-warp pass in ONE launch: the blocks form a thread-block cluster, each
+// warp's level-2 value goes straight into block 0's shared memory (DSMEM), a cluster barrier
+// (release / acquire), then block 0's first warp runs reduce_final_fin's pass over them and the
+// scalar step.  The same values meet the same trees in the same order, so the result is
+// bit-identical; one launch per reduction fewer (four per LSQR iteration).
+template <class F>
+__global__ void __launch_bounds__(256) reduce2_final_fin(const double* __restrict__ in, size_t J, size_t K,
+                                                         double* __restrict__ out, const int* gate, F fin) {
+  namespace cg = cooperative_groups;
+  __shared__ double part[64];
+  cg::cluster_group cl = cg::this_cluster();
+  const bool live = !(gate && *gate == 0);
+  const int lane = threadIdx.x & 31;
+  const size_t k = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (live && k < K) {  // reduce2_kernel's warp
+    const size_t base = k * 1024 + (size_t)lane * 32;
+    double v[32];
+    if (base + 32 <= J && !(reinterpret_cast<uintptr_t>(in + base) & 15)) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double2 q = *reinterpret_cast<const double2*>(in + base + 2 * j);
+        v[2 * j] = q.x;
+        v[2 * j + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = base + j < J ? in[base + j] : 0.0;
+    }
+    const double r = tree32(tree32_serial(v));
+    if (lane == 0) cl.map_shared_rank(part, 0)[k] = r;
+  }
+  cl.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // reduce_final_fin over the K values
+    if (live) {
+      const size_t base = (size_t)lane * 32;
+      double v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = base + j < K ? part[base + j] : 0.0;
+      const double r = tree32(tree32_serial(v));
+      if (lane == 0) *out = r;
+    }
+    if (lane == 0) fin();
+  }
+}
+
 template <class F>
 void reduce_segments_fin(Ctx* c, const double* seg, size_t nseg, double* scratch, double* out, const int* gate,
                          F fin) {
+  // MLSQR_CLUSTER_FIN=0: the last pass and the final pass as two launches
+  static const bool fused = !(getenv("MLSQR_CLUSTER_FIN") && getenv("MLSQR_CLUSTER_FIN")[0] == '0');
+  if (fused && nseg > 1024) {
+    const double* cur = seg;
+    size_t J = nseg;
+    double* s = scratch;
+    while (J > 64 * 1024) {
+      const size_t K = (J + 1023) / 1024;
+      reduce2_pass(c, cur, J, K, s, gate);
+      cur = s;
+      s += K;
+      J = K;
+    }
+    if (J > 1024) {
+      const size_t K = (J + 1023) / 1024;
+      const unsigned nb = (unsigned)((K + 7) / 8);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(nb);
+      cfg.blockDim = dim3(256);
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = nb;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      MLSQR_CUDA(cudaLaunchKernelEx(&cfg, reduce2_final_fin<F>, cur, J, K, out, gate, fin));
+    } else {
+      reduce_final_fin<F><<<1, 32, 0, c->stream>>>(cur, J, out, gate, fin);
+    }
+    c->count();
+    c->check_launch();
+    return;
+  }
   size_t J = 0;
   const double* cur = reduce_segments_to_warp(c, seg, nseg, scratch, gate, &J);
   reduce_final_fin<F><<<1, 32, 0, c->stream>>>(cur, J, out, gate, fin);
