@@ -35,3 +35,16 @@ for c in c1 c2 c3 c4; do
   timeout 600 python bench.py --config $c --no-cpu-baseline --steps ${STEPS[$c]} --warmup 3 > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err
   echo "bench $c rc=$?"
 done
+# one full capture per hot kernel of the small / dense configs (C2 2D blur + fused first sweeps, C3 128^3 blur,
+# C4 dense A x / A^T y), aimed at launches inside the first timed outer step
+capc() {  # name config regex skip
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k "regex:$3" -s $4 -c 1 -o $O/${TAG}_full_$1 python bench.py --config $2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+    > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
+}
+capc c2_blur2d c2 'blur2d_reg_kernel' 40
+capc c2_sweep_fn2d c2 'sweep_fn2d_kernel<32>' 20
+capc c3_blur c3 'blur3d_(mma|pipe)' 40
+capc c3_sweep_fn c3 'sweep_fn(_tma)?_kernel' 20
+capc c4_gemv c4 'gemv_l1_kernel' 10
+capc c4_gemvt c4 'gemvt_kernel' 10
