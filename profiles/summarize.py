@@ -67,7 +67,9 @@ def full(path, out):
     ik = hdr.index("Kernel Name")
     lines = [f"# ncu --set full summary ({path})", "", "| kernel | " + " | ".join(METRICS) + " |",
              "|" + "---|" * (len(METRICS) + 1)]
-    for row in rows[2:]:
+    # a capture may hold several launches of the kernel (all levels of a V-cycle): keep the longest
+    it, ut = hdr.index("gpu__time_duration.sum"), units[hdr.index("gpu__time_duration.sum")]
+    for row in [max(rows[2:], key=lambda r: to_ms(r[it], ut))]:
         vals = []
         for m in METRICS:
             if m in hdr:
@@ -93,7 +95,9 @@ def traffic(tag, out):
                             "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
                            capture_output=True, text=True).stdout
         rows = list(csv.reader(r.splitlines()))
-        hdr, units, row = rows[0], rows[1], rows[2]
+        hdr, units = rows[0], rows[1]
+        it = hdr.index("gpu__time_duration.sum")
+        row = max(rows[2:], key=lambda r: to_ms(r[it], units[it]))  # the level-0 launch of the capture
         g = lambda m: (row[hdr.index(m)], units[hdr.index(m)])
         per[name] = {"kernel": row[hdr.index("Kernel Name")].split("(")[0].replace("void ", ""),
                      "dram_bytes": 1e9 * (to_gb(*g("dram__bytes_read.sum")) + to_gb(*g("dram__bytes_write.sum"))),

@@ -14,19 +14,18 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   -c 700 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
   > $O/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
 # one full capture per hot kernel, aimed at a level-0 launch of the 512^3 driver:
-#   blur: 6th launch (mlsqr iteration 1's K_A, with the xpby/norm epilogue); sweep_fn: 2nd V-cycle's level 0;
-#   prolong sweep <3,2>: levels 3,2,1,0 -> 4th; normal sweep <3,1>: coarsest x2, levels 3..0 -> 6th;
-#   restrict: 2nd V-cycle's level 0 (5th); update: first.
-cap() {  # name regex skip
+#   blur: 6th launch (mlsqr iteration 1's K_A, with the xpby/norm epilogue); the V-cycle kernels: every
+#   launch of the driver's 2nd V-cycle (all levels), of which summarize.py keeps the longest; update: first.
+cap() {  # name regex skip count   (summarize.py keeps the longest captured launch = level 0)
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:$2" -s $3 -c 1 -o $O/${TAG}_full_$1 python profiles/kernel_driver.py --reps 2 --iters 2 \
+    -k "regex:$2" -s $3 -c ${4:-1} -o $O/${TAG}_full_$1 python profiles/kernel_driver.py --reps 2 --iters 2 \
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
 cap blur 'blur3d_(mma|pipe)' 5
-cap sweep_fn 'sweep_fn(_tma)?_kernel' 5
-cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2' 3
-cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1' 5
-cap restrict 'restrict_zm_kernel' 4
+cap sweep_fn 'sweep_fn(_tma)?_kernel' 4 4
+cap sweep_prolong 'sweep_zm_kernel<.int.3, .int.2' 4 4
+cap sweep_normal 'sweep_zm_kernel<.int.3, .int.1' 7 7
+cap restrict 'restrict_zm_kernel' 4 4
 cap update 'update_kernel' 0
 # the other BASELINE configs (parity configs; one bench line each, no CPU baseline; enough steps for
 # the clock sampler to see the timed region)
@@ -43,7 +42,7 @@ capc() {  # name config regex skip
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
 capc c2_blur2d c2 'blur2d_reg_kernel' 40
-capc c2_sweep_fn2d c2 'sweep_fn2d_kernel<32>' 20
+capc c2_sweep_fn2d c2 'sweep_fn2d_kernel<.int.32' 20
 capc c3_blur c3 'blur3d_(mma|pipe)' 40
 capc c3_sweep_fn c3 'sweep_fn(_tma)?_kernel' 20
 capc c4_gemv c4 'gemv_l1_kernel' 10
