@@ -20,6 +20,18 @@ constexpr bool kZmPrefetch = MLSQR_ZM_PREFETCH;
 #define MLSQR_ZM_AHEAD 3
 #endif
 constexpr int kZmAhead = MLSQR_ZM_AHEAD;  // planes ahead of the z march
+// resident blocks per SM the compiler plans for: 4 (64 registers) for the plain and first sweeps, which
+// otherwise take 76 registers and 3 blocks (last sweep 1.32 -> 1.22 ms per 512^3 launch in the power-capped
+// bench); the prolongation sweep already fits 64 and gets slower under the constraint (1.26 -> 1.36 ms)
+#ifndef MLSQR_ZM_MINB
+#define MLSQR_ZM_MINB 4
+#endif
+#ifndef MLSQR_RZ_MINB
+#define MLSQR_RZ_MINB 0  // restriction: no block target
+#endif
+#ifndef MLSQR_ZM_MINB_P
+#define MLSQR_ZM_MINB_P 0  // 0: no block target (the compiler settles on 64 registers)
+#endif
 
 // iterate value at fine index j (plus the prolongated coarse correction)
 // I: element index type -- int where the level (with guards) fits 2^31 elements: every
@@ -37,7 +49,7 @@ __device__ __forceinline__ double xv_zm(const double* __restrict__ x, const doub
 }
 
 template <int D, int MODE, typename I = long>
-__global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __restrict__ x,
+__global__ void __launch_bounds__(256, MODE == kProlong ? MLSQR_ZM_MINB_P : MLSQR_ZM_MINB) sweep_zm_kernel(Lvl L, const double* __restrict__ x,
                                                        const double* __restrict__ xc, int cnx, int cny,
                                                        const double* __restrict__ b,
                                                        double* __restrict__ out, double omega,
@@ -149,7 +161,7 @@ __global__ void __launch_bounds__(256) sweep_zm_kernel(Lvl L, const double* __re
 // of each 2 x 2 patch accumulates the children in the canonical order across the two
 // fine planes of the coarse cell.
 template <int D, typename I = long>
-__global__ void __launch_bounds__(256) restrict_zm_kernel(Lvl L, const double* __restrict__ x,
+__global__ void __launch_bounds__(256, MLSQR_RZ_MINB) restrict_zm_kernel(Lvl L, const double* __restrict__ x,
                                                           const double* __restrict__ b, int cnx, int cny,
                                                           double* __restrict__ bcoarse, const int* gate,
                                                           int zc) {
