@@ -748,11 +748,33 @@ int mlsqr_outer_advance(mlsqr_outer* o, const double* g, const double* f_prev, d
     Op* op = o->impl->op;
     Ctx* c = op->ctx;
     set_device(c);
-    In gin(c, g, op->rows, kind);
+    if (kind == MLSQR_DEVICE) {
+      o->impl->step(g, f_prev, f_out, step, ++o->k);
+      return;
+    }
+    // HOST buffers: f_prev first on the main stream (the hierarchy build needs only it), then g on
+    // the side stream behind it (the same PCIe direction: no sharing), joined before the solve;
+    // f_out returns on the side stream from inside step(), overlapped with R(f)
     In fin(c, f_prev, op->cols, kind);
-    Out fout(c, f_out, op->cols, kind);
-    o->impl->step(gin.d, fin.d, fout.d, step, ++o->k);
-    fout.finish();
+    double* gd = static_cast<double*>(c->staging(sizeof(double) * op->rows));
+    double* fd = static_cast<double*>(c->staging(sizeof(double) * op->cols));
+    cudaStream_t side = c->side_stream();
+    MLSQR_CUDA(cudaEventRecord(c->ev_copy, c->stream));
+    MLSQR_CUDA(cudaStreamWaitEvent(side, c->ev_copy, 0));
+    MLSQR_CUDA(cudaMemcpyAsync(gd, g, sizeof(double) * op->rows, cudaMemcpyHostToDevice, side));
+    MLSQR_CUDA(cudaEventRecord(c->ev_copy, side));
+    struct Reset {  // also on an error path: no copy may still touch the caller's buffers
+      OuterSolver* s;
+      cudaStream_t side;
+      ~Reset() {
+        s->g_ready = nullptr;
+        s->out_host = nullptr;
+        cudaStreamSynchronize(side);
+      }
+    } reset{o->impl.get(), side};
+    o->impl->g_ready = c->ev_copy;
+    o->impl->out_host = f_out;
+    o->impl->step(gd, fin.d, fd, step, ++o->k);
   });
 }
 

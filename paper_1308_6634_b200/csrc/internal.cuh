@@ -211,6 +211,7 @@ struct Ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;    // the Krylov loop's vtilde exchange
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;  // an operator's own input exchange
+  cudaEvent_t ev_copy = nullptr, ev_copy2 = nullptr;   // HOST-buffer copies overlapped with main-stream work
   cudaStream_t side_stream() {
     if (!side) {
       MLSQR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -218,6 +219,8 @@ struct Ctx {
       MLSQR_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
       MLSQR_CUDA(cudaEventCreateWithFlags(&ev_fork2, cudaEventDisableTiming));
       MLSQR_CUDA(cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming));
+      MLSQR_CUDA(cudaEventCreateWithFlags(&ev_copy, cudaEventDisableTiming));
+      MLSQR_CUDA(cudaEventCreateWithFlags(&ev_copy2, cudaEventDisableTiming));
     }
     return side;
   }
@@ -228,6 +231,8 @@ struct Ctx {
       cudaEventDestroy(ev_join);
       cudaEventDestroy(ev_fork2);
       cudaEventDestroy(ev_join2);
+      cudaEventDestroy(ev_copy);
+      cudaEventDestroy(ev_copy2);
       side = nullptr;
     }
   }
@@ -469,6 +474,11 @@ class OuterSolver {
   OuterSolver(const OuterSolver&) = delete;
   OuterSolver& operator=(const OuterSolver&) = delete;
   void step(const double* g, const double* f_prev, double* f_out, mlsqr_outer_step* st, int k);
+  // HOST-buffer calls (mlsqr_outer_advance): g may still be on its way on the side stream while
+  // the hierarchy is built from f_prev (g_ready, waited for before the solve), and f_out goes
+  // back to out_host on the side stream as soon as the solve is done, next to R(f)
+  cudaEvent_t g_ready = nullptr;
+  double* out_host = nullptr;
   Op* op;
   mlsqr_solve_info last_info{};
   std::vector<double> al_, be_;

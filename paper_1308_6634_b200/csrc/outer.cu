@@ -80,8 +80,15 @@ void OuterSolver::step(const double* g, const double* f_prev, double* f_out, mls
   if (cfg_.spd_mode == MLSQR_SPD_CHOLESKY) solver.reset(make_chol_map(vc_, nullptr));
   if (cfg_.spd_mode == MLSQR_SPD_INNER_CG) solver.reset(make_inner_cg_map(vc_, cfg_.k_inner));
   mlsqr_solve_info info{};
+  if (g_ready) MLSQR_CUDA(cudaStreamWaitEvent(c->stream, g_ready, 0));
   solve_mlsqr(op, solver ? solver.get() : vcycle_as_pc(vc_), g, cfg_.tau, inner_, f_out, trace_.data(), al_.data(),
               be_.data(), &info, ws_);
+  if (out_host) {  // f_out is final: send it home on the side stream while R(f) is evaluated
+    cudaStream_t side = c->side_stream();
+    MLSQR_CUDA(cudaEventRecord(c->ev_copy2, c->stream));
+    MLSQR_CUDA(cudaStreamWaitEvent(side, c->ev_copy2, 0));
+    MLSQR_CUDA(cudaMemcpyAsync(out_host, f_out, sizeof(double) * op->cols, cudaMemcpyDeviceToHost, side));
+  }
   penalty_functional_async(c, dims_, nx_, ny_, nz_, h_, f_out, cfg_.pen_kind, cfg_.T, pseg_.p,
                            pscr_.p, pgat_.p, pfg_.p ? pfg_.p + nx_ * (dims_ >= 2 ? ny_ : 1) : nullptr,
                            pval_.p);
@@ -89,6 +96,7 @@ void OuterSolver::step(const double* g, const double* f_prev, double* f_out, mls
   MLSQR_CUDA(cudaMemcpyAsync(&pv, pval_.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   MLSQR_CUDA(cudaMemcpyAsync(&eps, vcycle_eps_dev(vc_), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   MLSQR_CUDA(cudaStreamSynchronize(c->stream));
+  if (out_host) MLSQR_CUDA(cudaStreamSynchronize(c->side));
   last_info = info;
   if (st) {
     st->k = k;

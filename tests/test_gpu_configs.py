@@ -254,3 +254,41 @@ def test_c4_full_config_bit_exact(ctx):
                           rel_decrease_threshold=0.0, max_outer=cfg["K"], mg_levels=cfg["levels"])
     solver = mb.OuterSolver(op, shape, 1.0 / n, ocfg)
     _check_steps(torch, solver, g, N, z, int(z["outer_steps"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(96, 80), (48, 40, 32)])
+def test_outer_step_host_buffers_match_device(shape):
+    """mlsqr_outer_advance with HOST buffers (pinned or pageable numpy): f_prev goes up first, g
+    follows on the side stream while the hierarchy is built, f comes back on the side stream next
+    to R(f).  Three chained steps must equal the DEVICE-buffer steps bit for bit."""
+    torch = pytest.importorskip("torch")
+    n = shape[0]
+    N = int(np.prod(shape))
+    taps = mb.gaussian_taps(n, 2.0 / n, 3)
+    rng = np.random.default_rng(5)
+    g = rng.random(N)
+    cfg = mb.OuterConfig(tau=5e-3, penalty=mb.PenaltySpec.tv_smoothed(0.05),
+                         inner_stop=mb.StoppingConfig.max_iterations(7), inner_cap=7,
+                         rel_decrease_threshold=0.0, max_outer=3, mg_levels=3)
+    op = mb.SeparableGaussianBlur(shape, taps=taps)
+    sd = mb.OuterSolver(op, shape, 1.0 / n, cfg)
+    gd = torch.from_numpy(g).cuda()
+    fa = torch.zeros(N, dtype=torch.float64, device="cuda")
+    fb = torch.empty_like(fa)
+    dev = []
+    for _ in range(3):
+        st = sd.step(gd, fa, fb)
+        torch.cuda.synchronize()
+        dev.append((st.penalty_value, st.eps_used, st.inner_iterations, st.final_residual, fb.cpu().numpy().copy()))
+        fa, fb = fb, fa
+    sh = mb.OuterSolver(op, shape, 1.0 / n, cfg)
+    gh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    gh.copy_(torch.from_numpy(g))
+    pa = np.zeros(N)  # pageable
+    pb = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
+    for k in range(3):
+        st = sh.step(gh.numpy(), pa, pb)
+        assert (st.penalty_value, st.eps_used, st.inner_iterations, st.final_residual) == dev[k][:4]
+        assert np.array_equal(pb, dev[k][4])
+        pa, pb = pb, pa
