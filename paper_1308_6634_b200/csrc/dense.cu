@@ -7,10 +7,17 @@
 // A^T y: one thread per column, rows in 8 fixed chunks, sequential inside a
 //       chunk (the reference's per-row axpy order, linop.cpp:78-84), chunk
 //       partials added in order -- deterministic and row-shardable.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <mutex>
+
 #include "internal.cuh"
 #include "vec.cuh"
 
 namespace mlsqr_b200 {
+
+#include "tma.cuh"
 
 // ---------------------------------------------------------------------------
 // y = A (x*sx) in the canonical order with ~5 instructions per element instead of ~20:
@@ -91,6 +98,96 @@ __global__ void __launch_bounds__(256, 2) gemv_l1_kernel(const double* __restric
       const double t = tree32(tree32_serial(p));  // segment partial, then level 1 across the group
       if (lane == 0) l1[row * G1 + g] = t;
     }
+  }
+}
+
+// The same level-1 kernel fed by bulk copies (cp.async.bulk into an mbarrier ring): thread 0 issues,
+// per 1024-column group, nine contiguous 8 KB copies (the x slice and the eight row slices) into
+// stage (g mod kBulkStages), kBulkStages - 1 groups ahead of the group being reduced, so the
+// compute warps issue no global loads or staging stores at all.  The slices sit UNPADDED in shared
+// memory; lane l still owns segment l but walks its sixteen double2 pairs rotated by l
+// (pair (jj + l) mod 16 at step jj: conflict-free 16-byte loads).  tree32_serial's pairing is
+// invariant under that rotation -- v[i] meets v[i + 16], then sums i and i + 8 of the sixteen, ...
+// and IEEE addition commutes -- so the pair partners always sit at STATIC register slots (jj and
+// jj - 8, then k and k + 4, ...) and the segment partial is bit-identical to tree32_serial's.
+// Used when the operator has whole 8-row groups and whole 1024-column groups, 16-byte aligned;
+// anything else runs gemv_l1_kernel (MLSQR_GEMV_BULK=0 forces it).
+constexpr int kBulkStages = 3;
+constexpr int kBulkStage = 1024 * (1 + kGemvWarps);  // doubles per stage: x, then the 8 rows
+constexpr size_t kBulkSmem = sizeof(double) * kBulkStages * kBulkStage + 8 * kBulkStages;
+
+__device__ __forceinline__ void bulk_load(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1) gemv_l1_bulk_kernel(const double* __restrict__ A,
+                                                              const double* __restrict__ x, size_t rows,
+                                                              size_t cols, int parts, double* __restrict__ l1,
+                                                              const double* sx, const int* gate) {
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(128) double gsm[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(gsm + kBulkStages * kBulkStage);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t rg = blockIdx.x / (size_t)parts, part = blockIdx.x % (size_t)parts;
+  const size_t row0 = rg * kGemvWarps;
+  const size_t G1 = cols / 1024;
+  const size_t gp = (G1 + parts - 1) / parts;
+  const size_t g0 = part * gp, g1 = g0 + gp < G1 ? g0 + gp : G1;
+  const double s = sx ? *sx : 1.0;
+  auto issue = [&](size_t g) {  // thread 0 only
+    if (g >= g1) return;
+    const unsigned st = (unsigned)((g - g0) % kBulkStages);
+    double* d = gsm + (size_t)st * kBulkStage;
+    mbar_arrive_expect(bars + st, 8192u * (1 + kGemvWarps));
+    bulk_load(d, x + g * 1024, 8192u, bars + st);
+#pragma unroll
+    for (int r = 0; r < kGemvWarps; ++r) bulk_load(d + 1024 * (1 + r), A + (row0 + r) * cols + g * 1024, 8192u, bars + st);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kBulkStages; ++k) mbar_init(bars + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kBulkStages - 1; ++k) issue(g0 + k);
+  for (size_t g = g0; g < g1; ++g) {
+    const unsigned it = (unsigned)(g - g0), st = it % kBulkStages;
+    // the stage refilled now was read in the previous iteration: everyone is past it
+    __syncthreads();
+    if (threadIdx.x == 0) issue(g + kBulkStages - 1);
+    mbar_wait(bars + st, (it / kBulkStages) & 1u);
+    const double2* ap = reinterpret_cast<const double2*>(gsm + (size_t)st * kBulkStage + 1024 * (1 + w) + 32 * lane);
+    const double2* xp = reinterpret_cast<const double2*>(gsm + (size_t)st * kBulkStage + 32 * lane);
+    double2 P[8], T[8];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int q = (jj + lane) & 15;
+      const double2 av = ap[q];
+      double2 xv = xp[q];
+      if (sx) {
+        xv.x = xv.x * s;
+        xv.y = xv.y * s;
+      }
+      const double2 pr = make_double2(av.x * xv.x, av.y * xv.y);
+      if (jj < 8) {
+        P[jj] = pr;
+      } else {  // tree32_serial level 1: v[i] + v[i + 16]
+        T[jj - 8] = make_double2(P[jj - 8].x + pr.x, P[jj - 8].y + pr.y);
+      }
+    }
+    // levels 2..5 (sums i, i + 8 of 16; i, i + 4 of 8; i, i + 2 of 4; 0, 1)
+    double2 U[4], V[2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) U[k] = make_double2(T[k].x + T[k + 4].x, T[k].y + T[k + 4].y);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) V[k] = make_double2(U[k].x + U[k + 2].x, U[k].y + U[k + 2].y);
+    const double2 Z = make_double2(V[0].x + V[1].x, V[0].y + V[1].y);
+    const double t = tree32(Z.x + Z.y);  // level 1 across the group's 32 segments
+    if (lane == 0) l1[(row0 + w) * G1 + g] = t;
   }
 }
 
@@ -241,6 +338,7 @@ class DenseOp final : public Op {
     l1_.alloc(rows * (((cols + 31) / 32 + 31) / 32));
     // set outside any graph capture (the first A x may run inside the captured LSQR iteration)
     MLSQR_CUDA(cudaFuncSetAttribute(gemv_l1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    MLSQR_CUDA(cudaFuncSetAttribute(gemv_l1_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem));
   }
   static constexpr int kSmem = sizeof(double) * kGrpDoubles * (1 + kGemvWarps);
   DevBuf<double> a_;
@@ -257,9 +355,28 @@ class DenseOp final : public Op {
     size_t parts = (want + groups - 1) / groups;
     if (parts < 1) parts = 1;
     if (parts > G1) parts = G1;
-    const size_t ctas = (rows + kGemvWarps - 1) / kGemvWarps * parts;
-    gemv_l1_kernel<<<(unsigned)ctas, 32 * kGemvWarps, kSmem, ctx->stream>>>(a_.p, x, rows, cols, (int)parts, l1_.p, e.sx,
-                                                                       e.gate);
+    static const bool bulk_on = !(getenv("MLSQR_GEMV_BULK") && getenv("MLSQR_GEMV_BULK")[0] == '0');
+    const bool bulk = bulk_on && rows % kGemvWarps == 0 && cols % 1024 == 0 &&
+                      reinterpret_cast<uintptr_t>(a_.p) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
+    if (bulk) {
+      // one CTA per SM: the column split that fills whole waves best (at least four of them)
+      double best = -1.0;
+      for (size_t p = 1; p <= 16 && p <= G1; ++p) {
+        const double w = (double)(groups * p) / ctx->sm_count;
+        const double eff = w / std::ceil(w) * (w >= 4.0 ? 1.0 : 0.5) * (G1 % p == 0 ? 1.0 : 0.98);
+        if (eff > best + 1e-9) {
+          best = eff;
+          parts = p;
+        }
+      }
+    }
+    const size_t ctas = groups * parts;
+    if (bulk)
+      gemv_l1_bulk_kernel<<<(unsigned)ctas, 32 * kGemvWarps, kBulkSmem, ctx->stream>>>(a_.p, x, rows, cols, (int)parts,
+                                                                                      l1_.p, e.sx, e.gate);
+    else
+      gemv_l1_kernel<<<(unsigned)ctas, 32 * kGemvWarps, kSmem, ctx->stream>>>(a_.p, x, rows, cols, (int)parts, l1_.p,
+                                                                         e.sx, e.gate);
     gemv_top_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, ctx->stream>>>(l1_.p, rows, G1, dst, e.gate);
     ctx->count(2);
     ctx->check_launch();

@@ -100,7 +100,8 @@ def test_operator_dimension_errors(ctx):
         mb.SeparableGaussianBlur((16, 16, 16), taps=np.ones(2 * 40 + 1))  # 3D radius > 36
 
 
-@pytest.mark.parametrize("m,n,L", [(17, 23, 0), (40, 30, 0), (64, 512, 8), (96, 4096, 16), (8, 100000, 0)])
+@pytest.mark.parametrize("m,n,L", [(17, 23, 0), (40, 30, 0), (64, 512, 8), (96, 4096, 16), (8, 100000, 0),
+                                   (16, 20480, 0), (24, 7168, 0)])  # whole 8-row / 1024-column groups: the bulk-copy-fed A x
 def test_dense_bit_exact(ctx, dev, m, n, L):
     rng = np.random.default_rng(m + n)
     a = rng.uniform(-1, 1, (m, n))
