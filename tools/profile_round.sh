@@ -16,8 +16,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 # one full capture per hot kernel, aimed at a level-0 launch of the 512^3 driver:
 #   blur: 6th launch (mlsqr iteration 1's K_A, with the xpby/norm epilogue); the V-cycle kernels: every
 #   launch of the driver's 2nd V-cycle (all levels), of which summarize.py keeps the longest; update: first.
+# (gpurun brings back at most 64 MiB: only the single-launch C5 captures carry the SASS/source pages)
 cap() {  # name regex skip count   (summarize.py keeps the longest captured launch = level 0)
-  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  local src="--import-source on"; [ "${4:-1}" != 1 ] && src=""
+  timeout 600 ncu --set full --clock-control none $src --kernel-name-base demangled \
     -k "regex:$2" -s $3 -c ${4:-1} -o $O/${TAG}_full_$1 python profiles/kernel_driver.py --reps 2 --iters 2 \
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
@@ -37,7 +39,7 @@ done
 # one full capture per hot kernel of the small / dense configs (C2 2D blur + fused first sweeps, C3 128^3 blur,
 # C4 dense A x / A^T y), aimed at launches inside the first timed outer step
 capc() {  # name config regex skip
-  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  timeout 600 ncu --set full --clock-control none --kernel-name-base demangled \
     -k "regex:$3" -s $4 -c 1 -o $O/${TAG}_full_$1 python bench.py --config $2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
     > $O/${TAG}_full_$1.log 2>&1; echo "full $1 rc=$?"
 }
@@ -47,3 +49,4 @@ capc c3_blur c3 'blur3d_(mma|pipe)' 40
 capc c3_sweep_fn c3 'sweep_fn(_tma)?_kernel' 20
 capc c4_gemv c4 'gemv_l1_kernel' 10
 capc c4_gemvt c4 'gemvt_kernel' 10
+du -sh $O
