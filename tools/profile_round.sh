@@ -47,6 +47,16 @@ capc c2_blur2d c2 'blur2d_reg_kernel' 40
 capc c2_sweep_fn2d c2 'sweep_fn2d_kernel<.int.32' 20
 capc c3_blur c3 'blur3d_(mma|pipe)' 40
 capc c3_sweep_fn c3 'sweep_fn(_tma)?_kernel' 20
-capc c4_gemv c4 'gemv_l1_kernel' 10
+capc c4_gemv c4 'gemv_l1_(bulk_)?kernel' 10
 capc c4_gemvt c4 'gemvt_kernel' 10
+# summaries are made here, on the box (gpurun brings back at most 64 MiB): only the blur capture travels
+python profiles/summarize.py launches $O/${TAG}_launches.csv $O/${TAG}_launches.md > /dev/null
+python profiles/summarize.py dram_iter $O/${TAG}_launches.csv $O/${TAG}_dram_per_iter.json > /dev/null
+: > $O/${TAG}_ncu_full.md
+for k in blur sweep_fn sweep_prolong sweep_normal restrict update c2_blur2d c2_sweep_fn2d c3_blur c3_sweep_fn c4_gemv c4_gemvt; do
+  python profiles/summarize.py full $O/${TAG}_full_$k.ncu-rep $O/_x.md > /dev/null 2>&1 && cat $O/_x.md >> $O/${TAG}_ncu_full.md
+done
+rm -f $O/_x.md
+python profiles/summarize.py traffic $TAG $O/${TAG}_traffic.json > /dev/null
+find $O -name '*.ncu-rep' ! -name "${TAG}_full_blur.ncu-rep" -delete
 du -sh $O
