@@ -359,17 +359,20 @@ class DenseOp final : public Op {
     const bool bulk = bulk_on && rows % kGemvWarps == 0 && cols % 1024 == 0 &&
                       reinterpret_cast<uintptr_t>(a_.p) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
     if (bulk) {
-      // one CTA per SM: the column split that fills whole waves best (at least four of them)
+      // one CTA per SM: the column split that fills whole waves best, with at least ~24 waves of
+      // short CTAs where the matrix allows (C4: 8 parts 396 it/s, 2 parts 389)
       double best = -1.0;
       for (size_t p = 1; p <= 16 && p <= G1; ++p) {
         const double w = (double)(groups * p) / ctx->sm_count;
-        const double eff = w / std::ceil(w) * (w >= 4.0 ? 1.0 : 0.5) * (G1 % p == 0 ? 1.0 : 0.98);
+        const double eff = w / std::ceil(w) * (w >= 24.0 ? 1.0 : 0.9 + 0.1 * w / 24.0) * (G1 % p == 0 ? 1.0 : 0.98);
         if (eff > best + 1e-9) {
           best = eff;
           parts = p;
         }
       }
     }
+    static const long parts_env = getenv("MLSQR_GEMV_PARTS") ? atol(getenv("MLSQR_GEMV_PARTS")) : 0;
+    if (parts_env > 0 && (size_t)parts_env <= G1) parts = (size_t)parts_env;
     const size_t ctas = groups * parts;
     if (bulk)
       gemv_l1_bulk_kernel<<<(unsigned)ctas, 32 * kGemvWarps, kBulkSmem, ctx->stream>>>(a_.p, x, rows, cols, (int)parts,
