@@ -311,7 +311,11 @@ int mlsqr_nonlinear_solve(mlsqr_op* op, const double* g, int dims, size_t nx, si
 
 /* Stateful driver for one outer step at a time (outer.cpp:59-87): D update at f_prev,
  * hierarchy + auto shift, mlsqr from zero (capped at inner_cap), R(f^k).  Keeps the
- * V-cycle and the Krylov workspace resident between steps (bench / serving loop). */
+ * V-cycle and the Krylov workspace resident between steps (bench / serving loop).
+ * With MLSQR_HOST buffers (pinned memory copies at full PCIe speed) f_prev is copied first,
+ * g follows on the context's side stream while the hierarchy is built, and f_out returns
+ * on the side stream as soon as the solve ends, next to R(f); the call still returns only
+ * after every copy has completed. */
 typedef struct mlsqr_outer mlsqr_outer;
 int mlsqr_outer_create(mlsqr_op* op, int dims, size_t nx, size_t ny, size_t nz, double h,
                        const mlsqr_outer_cfg* cfg, mlsqr_outer** out);
