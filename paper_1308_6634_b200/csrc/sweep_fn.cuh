@@ -171,7 +171,10 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
 namespace fnt {
 constexpr int BX = 36, BY = fn::TY + 3;  // box: columns x0-2 .., rows y0-2 ..
 constexpr int BOX = (BX * BY + 15) / 16 * 16;  // TMA destinations are 128-byte aligned
-constexpr int NS = 4;                    // ring stages (planes)
+#ifndef MLSQR_FN_NS
+#define MLSQR_FN_NS 8
+#endif
+constexpr int NS = MLSQR_FN_NS;         // ring stages (planes)
 constexpr int STAGE = 4 * BOX;           // b, cx, cy, cz
 constexpr size_t SMEM = sizeof(double) * ((size_t)NS * STAGE + 3 * fn::ROWS * fn::COLS) + NS * 8;
 constexpr unsigned STAGE_BYTES = 4u * BX * BY * 8u;  // the bytes the four boxes deliver
