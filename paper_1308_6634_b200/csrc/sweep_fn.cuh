@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(fn::THREADS, fn::MINB) sweep_fn_kernel(Lvl L, 
 // TMA-fed variant (the default where the four streams can be tensor-mapped): one thread issues,
 // per plane, four TMA boxes -- b, cx, cy, cz over columns x0-2 .. x0+33 and rows y0-2 .. y0+16, the
 // tile's x1 region plus the x- / y- neighbour of its first column / row -- into an NS-stage ring
-// completed by mbarriers, three planes ahead of the plane whose x1 is formed.  Every thread then
+// completed by mbarriers, NS - 1 planes ahead of the plane whose x1 is formed.  Every thread then
 // reads its point's six values from shared memory instead of issuing six 64-bit-addressed loads
 // and L2 prefetches.  A box (or a plane outside the grid) is zero-filled by the hardware, which
 // gives x1 = 0 there, as the plain kernel's predicates do; the arithmetic is the plain kernel's,
