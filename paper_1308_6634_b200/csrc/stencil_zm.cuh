@@ -29,6 +29,10 @@ constexpr int kZmAhead = MLSQR_ZM_AHEAD;  // planes ahead of the z march
 #ifndef MLSQR_RZ_MINB
 #define MLSQR_RZ_MINB 0  // restriction: no block target
 #endif
+#ifndef MLSQR_ZM_UNROLL_P
+#define MLSQR_ZM_UNROLL_P 1
+#endif
+constexpr int kZmUnrollP = MLSQR_ZM_UNROLL_P;  // z-loop unroll of the prolongation sweep
 #ifndef MLSQR_ZM_MINB_P
 #define MLSQR_ZM_MINB_P 0  // 0: no block target (the compiler settles on 64 registers)
 #endif
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(256, MODE == kProlong ? MLSQR_ZM_MINB_P : MLSQ
       xn = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z0 + 1, i + nxy);
     }
   }
-#pragma unroll 2
+#pragma unroll(MODE == kProlong ? kZmUnrollP : 2)
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (kZmPrefetch && D >= 3 && z + kZmAhead < z1) {  // L2 prefetch of plane z+kZmAhead (no registers)
       const I j = i + kZmAhead * nxy;
