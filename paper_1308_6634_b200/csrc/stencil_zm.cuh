@@ -33,6 +33,14 @@ constexpr int kZmAhead = MLSQR_ZM_AHEAD;  // planes ahead of the z march
 #define MLSQR_ZM_UNROLL_P 1
 #endif
 constexpr int kZmUnrollP = MLSQR_ZM_UNROLL_P;  // z-loop unroll of the prolongation sweep
+#ifndef MLSQR_ZM_UNROLL_N
+#define MLSQR_ZM_UNROLL_N 1
+#endif
+constexpr int kZmUnrollN = MLSQR_ZM_UNROLL_N;  // ... of the plain / first sweeps
+#ifndef MLSQR_ZM_UNROLL_R
+#define MLSQR_ZM_UNROLL_R 2
+#endif
+constexpr int kZmUnrollR = MLSQR_ZM_UNROLL_R;  // ... of the restriction
 #ifndef MLSQR_ZM_MINB_P
 #define MLSQR_ZM_MINB_P 0  // 0: no block target (the compiler settles on 64 registers)
 #endif
@@ -88,7 +96,7 @@ __global__ void __launch_bounds__(256, MODE == kProlong ? MLSQR_ZM_MINB_P : MLSQ
       xn = xv_zm<D, P, I>(x, xc, cnx, cny, xx, yy, z0 + 1, i + nxy);
     }
   }
-#pragma unroll(MODE == kProlong ? kZmUnrollP : 2)
+#pragma unroll(MODE == kProlong ? kZmUnrollP : kZmUnrollN)
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (kZmPrefetch && D >= 3 && z + kZmAhead < z1) {  // L2 prefetch of plane z+kZmAhead (no registers)
       const I j = i + kZmAhead * nxy;
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(256, MLSQR_RZ_MINB) restrict_zm_kernel(Lvl L, 
   }
   const bool owner = ok && (tx % 2 == 0) && (D < 2 || ty % 2 == 0);
   double s = 0.0;
-#pragma unroll 2
+#pragma unroll(kZmUnrollR)
   for (int z = z0; z < z1; ++z, i += nxy) {
     if (kZmPrefetch && D >= 3 && z + kZmAhead < z1) {  // L2 prefetch of plane z+kZmAhead (no registers)
       const I j = i + kZmAhead * nxy;
